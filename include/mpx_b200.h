@@ -1,0 +1,133 @@
+/*
+ * mpx_b200.h — C ABI of the B200-native mixed-precision training step.
+ *
+ * The reference (`mpsim`, /root/reference/pkg) is pure Python/numpy and has
+ * no FFI: its hot path is a set of Python functions.  Each entry point below
+ * is the native body of one of those functions; the Python host layer
+ * (paper_2507_03312_b200/) keeps the reference names and calls these through
+ * ctypes with raw device pointers and the caller's CUDA stream.
+ *
+ * Conventions
+ *   - every pointer named d_* is a device pointer owned by the caller;
+ *   - arrays of per-leaf pointers/sizes (h_*) are HOST arrays, read before the
+ *     call returns (a leaf table is packed into the kernel's parameter block,
+ *     no host->device copy, no allocation);
+ *   - `stream` is a cudaStream_t (0 = legacy default stream);
+ *   - every call is stream-ordered and asynchronous: nothing synchronises the
+ *     host;
+ *   - return value 0 = success, otherwise a cudaError_t / MPX_E* code; the
+ *     message is available from mpx_last_error() on the calling thread.
+ *
+ * Numerics contract: casts are IEEE round-to-nearest-
+ * even with subnormals and overflow to inf; unscale is an IEEE f32 division;
+ * Adam uses single-rounded f32 operations in the reference's order with no
+ * FMA contraction, so results are bit-identical to the reference.
+ */
+#ifndef MPX_B200_H
+#define MPX_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* dtype codes — mirror mpsim.dtypes.DType (dtypes.py:31-46) */
+enum {
+  MPX_F32 = 0,
+  MPX_F16 = 1,
+  MPX_BF16 = 2,
+};
+
+/* error codes beyond cudaError_t */
+enum {
+  MPX_EINVAL = 10001,     /* bad argument (dtype, size, null pointer) */
+  MPX_ETOOMANY = 10002,   /* internal: leaf table overflow */
+};
+
+/* Device-resident dynamic loss-scaling state.  Field-for-field the
+ * reference's LossScaling NamedTuple (precision.py:120-132); fp64 so the
+ * trajectory is bit-identical to the Python-double state machine. */
+typedef struct mpx_scaling_state {
+  double loss_scale;
+  double growth_factor;
+  double backoff_factor;
+  double min_scale;
+  int64_t growth_interval;
+  int64_t steps_since_growth;
+} mpx_scaling_state;
+
+/* Adam/SGD hyper-parameters, already rounded the way the reference rounds
+ * its weak Python scalars (np.float32(x) at use, tensors.py:187,235-236):
+ *   b1 = f32(beta1), omb1 = f32(1.0 - beta1), b2 = f32(beta2),
+ *   omb2 = f32(1.0 - beta2), lr = f32(lr), eps = f32(eps),
+ *   neg_lr = f32(-lr) (SGD, optim.py:60-66), neg_lr_wd = f32(-lr*wd)
+ *   (decoupled weight decay; 0 => the exact reference Adam path). */
+typedef struct mpx_adam_hparams {
+  float b1, omb1, b2, omb2, lr, eps, neg_lr, neg_lr_wd;
+} mpx_adam_hparams;
+
+const char* mpx_last_error(void);
+int mpx_version(void);
+int mpx_num_sms(int device);
+
+/* K1 — multi-tensor cast/scale: dst[i] = round_{dst_dtype}(f32(src[i]) * s).
+ * Replaces cast_tree/cast_to_* (precision.py:53-85, T.cast tensors.py:529,
+ * quantize_array dtypes.py:100-123) and LossScaling.scale (precision.py:134-143,
+ * T.mul(leaf, s)).  The multiplier is taken from d_scale (a device fp64, e.g.
+ * &state->loss_scale) when non-NULL, else from `scale` (host fp64); 1.0 means a
+ * plain cast (the multiply is skipped).  src/dst dtypes are per call. */
+int mpx_cast(const void* const* h_src, void* const* h_dst, const int64_t* h_numel,
+             int n_leaves, int src_dtype, int dst_dtype, double scale,
+             const double* d_scale, void* stream);
+
+/* K2 — fused unscale + non-finite check (precision.py:145-154 and
+ * tree.py:125-131 run back to back at precision.py:225-226):
+ *   g32 = f32(g) / f32(loss_scale)   (IEEE division; x * 2^-k when exact)
+ *   *d_flag &= all(isfinite(g32))
+ * h_out may be NULL (flag only, nothing written) or an array of f32 outputs
+ * (NULL entries allowed).  The divisor comes from d_scale (device fp64) when
+ * non-NULL, else from `scale`.  If reset_flag != 0 the flag is set to 1 first
+ * (stream-ordered), so one call computes all_finite of the whole table. */
+int mpx_unscale_finite(const void* const* h_g, float* const* h_out, const int64_t* h_numel,
+                       int n_leaves, int g_dtype, double scale, const double* d_scale,
+                       uint32_t* d_flag, int reset_flag, void* stream);
+
+/* K3 — LossScaling.adjust on the device (precision.py:156-173), fp64, one
+ * thread, no host sync.  If d_step_count is non-NULL it is incremented when
+ * the flag is set (optimizer step counter: only applied steps count,
+ * optim.py:102-103).  d_used_scale (optional) receives the pre-adjust scale. */
+int mpx_scaling_adjust(mpx_scaling_state* d_state, const uint32_t* d_flag,
+                       int64_t* d_step_count, double* d_used_scale, void* stream);
+
+/* K4 — finite-gated fused optimizer step (optim.py:58-113).
+ *   mode 0 = Adam (compute_updates Adam branch + apply_leaf),
+ *   mode 1 = SGD.
+ * Per leaf: master p (f32/f16/bf16, updated in place and re-rounded to its own
+ * dtype), moments m, v (f32, in place; ignored for SGD), gradient g of g_dtype
+ * (f32 grads are used as-is; f16/bf16 grads are *scaled* grads, unscaled in
+ * the kernel with the same division as K2), optional half working copy
+ * h_half[i] of half_dtype written in the same pass (NULL = none), optional
+ * h_upd[i] (if non-NULL the f32 update u is written there and p is NOT
+ * modified: compute_updates without apply).
+ * The whole call is a no-op when *d_flag == 0 (d_flag may be NULL = always).
+ * Bias correction: t = d_counter[0] + 1 (applied steps only);
+ * d_bc_table[2*(t-1)+{0,1}] = f32(1 - beta{1,2}**t) computed on the host in
+ * double (optim.py:73-76); t is clamped to bc_len.
+ * d_counter is int64[2] = {step_count, scratch}: when the step is applied the
+ * last block to finish increments step_count (optim.py:77 `step_count=t`,
+ * SGD optim.py:66) and leaves scratch at 0, so the call needs no extra launch
+ * and never syncs.  scratch must be 0 on entry (it is after every call). */
+int mpx_optimizer_step(void* const* h_p, const int32_t* h_p_dtype, float* const* h_m,
+                       float* const* h_v, const void* const* h_g, void* const* h_half,
+                       float* const* h_upd, const int64_t* h_numel, int n_leaves,
+                       int g_dtype, int half_dtype, int mode, mpx_adam_hparams hp,
+                       const float* d_bc_table, int64_t bc_len, int64_t* d_counter,
+                       double scale, const double* d_scale, const uint32_t* d_flag,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPX_B200_H */

@@ -1,0 +1,113 @@
+"""ctypes binding of libmpx_b200.so (the C ABI declared in include/mpx_b200.h).
+
+There is no CPU fallback anywhere in this package: if the library is missing
+or no CUDA device is present, every compute entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libmpx_b200.so"
+
+MPX_F32, MPX_F16, MPX_BF16 = 0, 1, 2
+
+_P = ctypes.c_void_p
+_PP = ctypes.POINTER(ctypes.c_void_p)
+_I64P = ctypes.POINTER(ctypes.c_int64)
+_I32P = ctypes.POINTER(ctypes.c_int32)
+
+
+class ScalingStateC(ctypes.Structure):
+    """mpx_scaling_state (include/mpx_b200.h) — 48 bytes."""
+
+    _fields_ = [
+        ("loss_scale", ctypes.c_double),
+        ("growth_factor", ctypes.c_double),
+        ("backoff_factor", ctypes.c_double),
+        ("min_scale", ctypes.c_double),
+        ("growth_interval", ctypes.c_int64),
+        ("steps_since_growth", ctypes.c_int64),
+    ]
+
+
+class AdamHParamsC(ctypes.Structure):
+    """mpx_adam_hparams (include/mpx_b200.h)."""
+
+    _fields_ = [(n, ctypes.c_float) for n in ("b1", "omb1", "b2", "omb2", "lr", "eps", "neg_lr", "neg_lr_wd")]
+
+
+# every symbol include/mpx_b200.h declares: (name, restype, argtypes)
+SIGNATURES = {
+    "mpx_last_error": (ctypes.c_char_p, []),
+    "mpx_version": (ctypes.c_int, []),
+    "mpx_num_sms": (ctypes.c_int, [ctypes.c_int]),
+    "mpx_cast": (ctypes.c_int, [_PP, _PP, _I64P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_double, _P, _P]),
+    "mpx_unscale_finite": (ctypes.c_int, [_PP, _PP, _I64P, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                          _P, _P, ctypes.c_int, _P]),
+    "mpx_scaling_adjust": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "mpx_optimizer_step": (ctypes.c_int, [_PP, _I32P, _PP, _PP, _PP, _PP, _PP, _I64P, ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_int, AdamHParamsC,
+                                          _P, ctypes.c_int64, _P, ctypes.c_double, _P, _P, _P]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: Path | str | None = None):
+    """Load (once) and return the native library; raise loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = Path(path or os.environ.get("MPX_B200_LIB", LIB_PATH))
+        if not p.exists():
+            raise RuntimeError(
+                f"mpx_b200 native library not found at {p}; build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        msg = load().mpx_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed (code {rc}): {msg}")
+
+
+def ptr_array(values) -> "ctypes.Array":
+    arr = (ctypes.c_void_p * max(len(values), 1))()
+    for i, v in enumerate(values):
+        arr[i] = v
+    return arr
+
+
+def i64_array(values):
+    a = np.ascontiguousarray(np.asarray(values, dtype=np.int64))
+    return a, a.ctypes.data_as(_I64P)
+
+
+def i32_array(values):
+    a = np.ascontiguousarray(np.asarray(values, dtype=np.int32))
+    return a, a.ctypes.data_as(_I32P)
+
+
+def as_pp(arr) -> "_PP":
+    return ctypes.cast(arr, _PP)

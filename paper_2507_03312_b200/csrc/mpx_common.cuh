@@ -1,0 +1,170 @@
+// Shared helpers for the mpx_b200 kernels (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/mpx_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "mpx_b200 kernels target sm_100a only"
+#endif
+
+namespace mpx {
+
+// ---------------------------------------------------------------------------
+// error plumbing: every C entry point returns an int status and leaves a
+// message in a thread-local buffer (mpx_last_error()).
+// ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define MPX_CUDA_CHECK(expr)                                                       \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      return ::mpx::fail((int)_e, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define MPX_LAUNCH_CHECK(what)                                                     \
+  do {                                                                             \
+    cudaError_t _e = cudaGetLastError();                                           \
+    if (_e != cudaSuccess)                                                         \
+      return ::mpx::fail((int)_e, std::string(what) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+int current_num_sms();
+
+// ---------------------------------------------------------------------------
+// element conversions.  All rounding is IEEE RNE with subnormals (no FTZ:
+// the library is built with -ftz=false -prec-div=true -prec-sqrt=true).
+// ---------------------------------------------------------------------------
+template <int DT> struct Storage;
+template <> struct Storage<MPX_F32>  { using T = float;    };
+template <> struct Storage<MPX_F16>  { using T = uint16_t; };
+template <> struct Storage<MPX_BF16> { using T = uint16_t; };
+
+template <int DT> __device__ __forceinline__ float to_f32(typename Storage<DT>::T x);
+template <> __device__ __forceinline__ float to_f32<MPX_F32>(float x) { return x; }
+template <> __device__ __forceinline__ float to_f32<MPX_F16>(uint16_t x) {
+  return __half2float(__ushort_as_half(x));
+}
+template <> __device__ __forceinline__ float to_f32<MPX_BF16>(uint16_t x) {
+  return __uint_as_float(((uint32_t)x) << 16);
+}
+
+template <int DT> __device__ __forceinline__ typename Storage<DT>::T from_f32(float x);
+template <> __device__ __forceinline__ float from_f32<MPX_F32>(float x) { return x; }
+template <> __device__ __forceinline__ uint16_t from_f32<MPX_F16>(float x) {
+  return __half_as_ushort(__float2half_rn(x));
+}
+template <> __device__ __forceinline__ uint16_t from_f32<MPX_BF16>(float x) {
+  return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+
+// round an f32 onto DT's grid, staying in f32 (quantize_array semantics)
+template <int DT> __device__ __forceinline__ float quantize_f32(float x) {
+  return to_f32<DT>(from_f32<DT>(x));
+}
+
+// ---------------------------------------------------------------------------
+// 4-wide vector access.  A tile is 256 threads x 2 groups x 4 elements; thread
+// t owns elements [4t, 4t+4) and [1024+4t, 1024+4t+4) of its tile, so every
+// load/store instruction of a warp covers one contiguous span (fully
+// coalesced for 2-byte and 4-byte element types alike).
+// ---------------------------------------------------------------------------
+constexpr int kThreads = 256;
+constexpr int kGroups = 2;
+constexpr int kVec = 4;
+constexpr int kTile = kThreads * kGroups * kVec;  // 2048 elements
+constexpr int kGroupStride = kThreads * kVec;       // 1024 elements
+
+template <int DT> struct Vec4;
+template <> struct Vec4<MPX_F32> {
+  __device__ __forceinline__ static void load(const void* base, int64_t i, float* o) {
+    float4 v = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + i);
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  }
+  __device__ __forceinline__ static void load_cs(const void* base, int64_t i, float* o) {
+    float4 v = __ldcs(reinterpret_cast<const float4*>(static_cast<const float*>(base) + i));
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  }
+  __device__ __forceinline__ static void store(void* base, int64_t i, const float* x) {
+    *reinterpret_cast<float4*>(static_cast<float*>(base) + i) = make_float4(x[0], x[1], x[2], x[3]);
+  }
+  __device__ __forceinline__ static void store_cs(void* base, int64_t i, const float* x) {
+    __stcs(reinterpret_cast<float4*>(static_cast<float*>(base) + i), make_float4(x[0], x[1], x[2], x[3]));
+  }
+};
+
+template <int DT> struct Vec4Half {
+  __device__ __forceinline__ static void unpack(uint2 w, float* o) {
+    o[0] = to_f32<DT>((uint16_t)(w.x & 0xFFFFu));
+    o[1] = to_f32<DT>((uint16_t)(w.x >> 16));
+    o[2] = to_f32<DT>((uint16_t)(w.y & 0xFFFFu));
+    o[3] = to_f32<DT>((uint16_t)(w.y >> 16));
+  }
+  __device__ __forceinline__ static uint2 pack(const float* x) {
+    uint2 w;
+    w.x = (uint32_t)from_f32<DT>(x[0]) | ((uint32_t)from_f32<DT>(x[1]) << 16);
+    w.y = (uint32_t)from_f32<DT>(x[2]) | ((uint32_t)from_f32<DT>(x[3]) << 16);
+    return w;
+  }
+  __device__ __forceinline__ static void load(const void* base, int64_t i, float* o) {
+    unpack(*reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(base) + i), o);
+  }
+  __device__ __forceinline__ static void load_cs(const void* base, int64_t i, float* o) {
+    unpack(__ldcs(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(base) + i)), o);
+  }
+  __device__ __forceinline__ static void store(void* base, int64_t i, const float* x) {
+    *reinterpret_cast<uint2*>(static_cast<uint16_t*>(base) + i) = pack(x);
+  }
+  __device__ __forceinline__ static void store_cs(void* base, int64_t i, const float* x) {
+    __stcs(reinterpret_cast<uint2*>(static_cast<uint16_t*>(base) + i), pack(x));
+  }
+};
+template <> struct Vec4<MPX_F16> : Vec4Half<MPX_F16> {};
+template <> struct Vec4<MPX_BF16> : Vec4Half<MPX_BF16> {};
+
+template <int DT> __device__ __forceinline__ float load1(const void* base, int64_t i) {
+  return to_f32<DT>(static_cast<const typename Storage<DT>::T*>(base)[i]);
+}
+template <int DT> __device__ __forceinline__ void store1(void* base, int64_t i, float x) {
+  static_cast<typename Storage<DT>::T*>(base)[i] = from_f32<DT>(x);
+}
+
+__device__ __forceinline__ bool aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+// ---------------------------------------------------------------------------
+// The unscale divisor.  The reference divides by f32(loss_scale)
+// (precision.py:151, np.float32(s) at tensors.py:236).  When f32(scale) is a
+// normal power of two, x / s == x * (1/s) bit-for-bit (both are one rounding
+// of the same exact real), so the kernels multiply; otherwise they divide.
+// ---------------------------------------------------------------------------
+struct Divisor {
+  float s;
+  float inv;
+  bool pow2;
+  __device__ __forceinline__ void init(float sf) {
+    s = sf;
+    uint32_t b = __float_as_uint(sf);
+    uint32_t e = (b >> 23) & 0xFFu;
+    pow2 = ((b & 0x807FFFFFu) == 0u) && e >= 1u && e <= 254u;
+    inv = pow2 ? __uint_as_float((254u - e) << 23) : 0.f;  // exact 2^-k (subnormal when e == 254)
+    if (pow2 && e == 254u) inv = __uint_as_float(0x00400000u);  // 2^-127
+  }
+  __device__ __forceinline__ float apply(float x) const {
+    return pow2 ? __fmul_rn(x, inv) : __fdiv_rn(x, s);
+  }
+};
+
+__device__ __forceinline__ bool f32_finite(float x) {
+  return (__float_as_uint(x) & 0x7F800000u) != 0x7F800000u;
+}
+
+}  // namespace mpx

@@ -1,0 +1,169 @@
+"""The fused mixed-precision step on flat HBM arenas — the hot path.
+
+One step after backward is three stream-ordered launches and no host sync:
+
+    K2  unscale+finite over the half-grad arena      reads 2 B/param
+    [   all_reduce(flag, MIN) across DP ranks        4 bytes          ]
+    K4  gated Adam(W): g/scale, m, v, p32, p_half     reads 14, writes 14 B/param
+    K3  loss-scale state machine (fp64, 1 thread)
+
+= 30 algorithmic bytes per parameter on a finite step, 2 on a skipped one.
+
+Layout (SURVEY.md §8a ViT-B: 152 leaves, 86,567,656 params): every leaf is a
+view into one arena per stream — p32 / m / v (f32), p_half and grads (f16 or
+bf16) — each leaf starting on a 16-byte boundary, in the reference's
+traversal order.  The arenas make the whole step a single-leaf
+multi-tensor-apply (one table entry, ~42K full tiles, grid = resident blocks
+x 148 SMs) and let the DP gradient exchange bucket contiguous memory.
+
+The leaf-level drop-in API (cast_tree / LossScaling / optimizer_update)
+calls exactly the same kernels with per-leaf tables.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native as N
+from . import kernels as K
+from .dtypes import F16, as_dtype
+from .precision import DeviceBool, DynamicLossScaling
+from .tree import float_leaves, tree_map
+
+
+class FlatArena:
+    """Views of one allocation laid out like a pytree's float leaves."""
+
+    def __init__(self, leaves, dtype: torch.dtype, device):
+        self.offsets = []
+        total = 0
+        for t in leaves:
+            self.offsets.append(total)
+            total += -(-t.numel() // 8) * 8
+        self.numel = total
+        self.buf = torch.empty(max(total, 8), dtype=dtype, device=device)
+        self.views = [self.buf[o:o + t.numel()].view(t.shape) for o, t in zip(self.offsets, leaves)]
+
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+
+class FusedMPStep:
+    """Master weights, Adam moments, half working copy and half grads of a
+    parameter tree, resident in flat device arenas, stepped by K2/K4/K3.
+
+    `params` is a tree whose float leaves are f32 CUDA tensors (copied in);
+    `tree(kind)` rebuilds the tree over the arena views ('p32', 'half',
+    'grad', 'm', 'v')."""
+
+    def __init__(self, params, lr: float, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                 weight_decay: float = 0.0, half_dtype=F16, scaling: DynamicLossScaling | None = None,
+                 process_group=None):
+        self.structure = params
+        fl = float_leaves(params)
+        if not fl:
+            raise ValueError("params contain no float tensor leaves")
+        self.paths = [p for p, _ in fl]
+        leaves = [x for _, x in fl]
+        K.require_cuda(leaves, "FusedMPStep")
+        dev = leaves[0].device
+        self.device = dev
+        self.half = as_dtype(half_dtype)
+        self.p32 = FlatArena(leaves, torch.float32, dev)
+        self.m = FlatArena(leaves, torch.float32, dev)
+        self.v = FlatArena(leaves, torch.float32, dev)
+        self.p_half = FlatArena(leaves, self.half.torch, dev)
+        self.grad = FlatArena(leaves, self.half.torch, dev)
+        self.p32.buf.zero_()  # alignment pads stay 0 (finite) in every arena
+        for dst, src in zip(self.p32.views, leaves):
+            dst.copy_(src)
+        self.m.buf.zero_()
+        self.v.buf.zero_()
+        self.grad.buf.zero_()
+        self.n_params = sum(t.numel() for t in leaves)
+        self.numel = self.p32.numel  # padded arena length (pads stay 0 / finite)
+        K.cast_into([self.p32.buf], [self.p_half.buf])
+        self.scaling = scaling if scaling is not None else DynamicLossScaling(2.0 ** 15, device=dev)
+        self.flag = torch.ones((), dtype=torch.int32, device=dev)
+        self.counter = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.used_scale = torch.zeros((), dtype=torch.float64, device=dev)
+        self.hp = K.adam_hparams(lr, beta1, beta2, eps, weight_decay)
+        self.bc = K.bias_correction_table(beta1, beta2, dev)
+        self.group = process_group
+        self._lib = N.load()
+        self._build_tables()
+
+    # ------------------------------------------------------------------
+    def _build_tables(self):
+        one = lambda p: (ctypes.c_void_p * 1)(p)  # noqa: E731
+        self._n = (ctypes.c_int64 * 1)(self.numel)
+        self._g_tab = one(self.grad.ptr())
+        self._p_tab = one(self.p32.ptr())
+        self._pd_tab = (ctypes.c_int32 * 1)(N.MPX_F32)
+        self._m_tab = one(self.m.ptr())
+        self._v_tab = one(self.v.ptr())
+        self._h_tab = one(self.p_half.ptr())
+        self._grad_src = self.grad.ptr()
+
+    def tree(self, kind: str):
+        arena = {"p32": self.p32, "half": self.p_half, "grad": self.grad, "m": self.m, "v": self.v}[kind]
+        it = iter(arena.views)
+        return tree_map(lambda x: next(it) if isinstance(x, torch.Tensor) and x.is_floating_point() else x,
+                        self.structure)
+
+    @property
+    def step_count(self) -> int:
+        return int(self.counter[0].item())
+
+    @property
+    def grads_finite(self) -> DeviceBool:
+        return DeviceBool(self.flag)
+
+    # ------------------------------------------------------------------
+    def step(self, grad_ptr: int | None = None, stream: int | None = None):
+        """K2 -> (flag all-reduce) -> K4 -> K3 on the arenas.  `grad_ptr`
+        selects another half-grad arena of the same layout (e.g. a second
+        buffer being filled by a copy engine)."""
+        lib = self._lib
+        st = stream if stream is not None else K.stream_handle(self.device)
+        g = self._g_tab if grad_ptr is None else (ctypes.c_void_p * 1)(grad_ptr)
+        d_scale = self.scaling.state.data_ptr()
+        code = self.half.code
+        N.check(lib.mpx_unscale_finite(N.as_pp(g), None, self._n, 1, code, 1.0, d_scale, self.flag.data_ptr(), 1,
+                                       st), "mpx_unscale_finite")
+        if self.group is not None:
+            torch.distributed.all_reduce(self.flag, op=torch.distributed.ReduceOp.MIN, group=self.group)
+        N.check(lib.mpx_optimizer_step(N.as_pp(self._p_tab), self._pd_tab, N.as_pp(self._m_tab),
+                                       N.as_pp(self._v_tab), N.as_pp(g), N.as_pp(self._h_tab), None, self._n, 1,
+                                       code, code, 0, self.hp, self.bc.data_ptr(), self.bc.numel() // 2,
+                                       self.counter.data_ptr(), 1.0, d_scale, self.flag.data_ptr(), st),
+                "mpx_optimizer_step")
+        N.check(lib.mpx_scaling_adjust(self.scaling.state.data_ptr(), self.flag.data_ptr(), None,
+                                       self.used_scale.data_ptr(), st), "mpx_scaling_adjust")
+
+    # per-kernel entry points (timing / profiling)
+    def k2(self, grad_ptr=None, stream=None):
+        st = stream if stream is not None else K.stream_handle(self.device)
+        g = self._g_tab if grad_ptr is None else (ctypes.c_void_p * 1)(grad_ptr)
+        N.check(self._lib.mpx_unscale_finite(N.as_pp(g), None, self._n, 1, self.half.code, 1.0,
+                                             self.scaling.state.data_ptr(), self.flag.data_ptr(), 1, st), "k2")
+
+    def k4(self, grad_ptr=None, stream=None):
+        st = stream if stream is not None else K.stream_handle(self.device)
+        g = self._g_tab if grad_ptr is None else (ctypes.c_void_p * 1)(grad_ptr)
+        code = self.half.code
+        N.check(self._lib.mpx_optimizer_step(N.as_pp(self._p_tab), self._pd_tab, N.as_pp(self._m_tab),
+                                             N.as_pp(self._v_tab), N.as_pp(g), N.as_pp(self._h_tab), None, self._n,
+                                             1, code, code, 0, self.hp, self.bc.data_ptr(), self.bc.numel() // 2,
+                                             self.counter.data_ptr(), 1.0, self.scaling.state.data_ptr(),
+                                             self.flag.data_ptr(), st), "k4")
+
+    def k3(self, stream=None):
+        st = stream if stream is not None else K.stream_handle(self.device)
+        N.check(self._lib.mpx_scaling_adjust(self.scaling.state.data_ptr(), self.flag.data_ptr(), None,
+                                             self.used_scale.data_ptr(), st), "k3")
+
+    ALGO_BYTES_FINITE = 30  # per parameter: K2 2 + K4 (2+4+4+4 read, 4+4+4+2 write)
+    ALGO_BYTES_SKIPPED = 2  # K2 only; K4 exits on the flag
+    K4_BYTES = 28
