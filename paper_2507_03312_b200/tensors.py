@@ -27,7 +27,7 @@ def tensor(data, dtype=F32, device=None) -> torch.Tensor:
         if arr.size and (arr.max() > _MAX_I32 or arr.min() < _MIN_I32):
             raise ValueError("value out of 32-bit signed integer range")
         return torch.from_numpy(arr.astype(np.int32)).to(dev)
-    f32 = torch.from_numpy(np.ascontiguousarray(np.asarray(data, dtype=np.float32))).to(dev)
+    f32 = torch.from_numpy(np.array(data, dtype=np.float32, order="C")).to(dev)
     if d is F32:
         return f32
     return K.cast_leaves([f32], d)[0]
