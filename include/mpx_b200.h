@@ -126,6 +126,47 @@ int mpx_optimizer_step(void* const* h_p, const int32_t* h_p_dtype, float* const*
                        double scale, const double* d_scale, const uint32_t* d_flag,
                        void* stream);
 
+/* K5 — tcgen05 GEMM with f32 accumulation (tensors.py:387-422 matmul and its
+ * backward rule autodiff.py:193-205, at half precision with f32 accumulate):
+ *   C[z][m,n] = epi(alpha * sum_k A[z][m,k] * B[z][k,n]),  z = b1 + nb1*b2
+ * A is K-major (element (m,k) at A[m*lda + k]) or MN-major (A[k*lda + m]);
+ * B is K-major (B[n*ldb + k]) or MN-major (B[k*ldb + n]); *_sb1/_sb2 are the
+ * element strides of the two batch dims (0 = dense).  Strides must be
+ * multiples of 8 elements (16-byte TMA rule).  When N is not a multiple of 8
+ * the epilogue writes whole 8-column groups (the pad columns get the value of
+ * zero-filled operands), so ldc must be >= round_up(N, 8).
+ * Epilogue (fused, per element, f32): + bias[n]; act GELU (aux receives the
+ * rounded pre-activation) or GELU-backward (multiplies by gelu'(aux[m,n]));
+ * + residual[m,n]; store as c_dtype (f32/f16/bf16).  bias/residual/aux share
+ * ab_dtype.  split_k > 1 (batch 1, no act) reduces through `workspace`
+ * (split*M*N f32) with a second deterministic pass. */
+typedef struct mpx_gemm_desc {
+  int ab_dtype; /* MPX_F16 / MPX_BF16 */
+  int M, N, K;
+  const void* A;
+  int64_t lda, a_sb1, a_sb2;
+  int a_mn_major;
+  const void* B;
+  int64_t ldb, b_sb1, b_sb2;
+  int b_mn_major;
+  int nb1, nb2;
+  void* C;
+  int64_t ldc, c_sb1, c_sb2;
+  int c_dtype;
+  const void* bias;
+  const void* residual;
+  int64_t ldr, r_sb1, r_sb2;
+  void* aux;
+  int64_t ld_aux;
+  float alpha; /* 0 means 1 */
+  int act;     /* 0 none, 1 GELU, 2 GELU backward */
+  int block_n; /* 0 = auto */
+  int split_k; /* <= 1: none */
+  void* workspace;
+} mpx_gemm_desc;
+
+int mpx_gemm(const mpx_gemm_desc* desc, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,6 +41,26 @@ class AdamHParamsC(ctypes.Structure):
     _fields_ = [(n, ctypes.c_float) for n in ("b1", "omb1", "b2", "omb2", "lr", "eps", "neg_lr", "neg_lr_wd")]
 
 
+class GemmDescC(ctypes.Structure):
+    """mpx_gemm_desc (include/mpx_b200.h)."""
+
+    _fields_ = [
+        ("ab_dtype", ctypes.c_int), ("M", ctypes.c_int), ("N", ctypes.c_int), ("K", ctypes.c_int),
+        ("A", ctypes.c_void_p), ("lda", ctypes.c_int64), ("a_sb1", ctypes.c_int64), ("a_sb2", ctypes.c_int64),
+        ("a_mn_major", ctypes.c_int),
+        ("B", ctypes.c_void_p), ("ldb", ctypes.c_int64), ("b_sb1", ctypes.c_int64), ("b_sb2", ctypes.c_int64),
+        ("b_mn_major", ctypes.c_int),
+        ("nb1", ctypes.c_int), ("nb2", ctypes.c_int),
+        ("C", ctypes.c_void_p), ("ldc", ctypes.c_int64), ("c_sb1", ctypes.c_int64), ("c_sb2", ctypes.c_int64),
+        ("c_dtype", ctypes.c_int),
+        ("bias", ctypes.c_void_p), ("residual", ctypes.c_void_p), ("ldr", ctypes.c_int64),
+        ("r_sb1", ctypes.c_int64), ("r_sb2", ctypes.c_int64),
+        ("aux", ctypes.c_void_p), ("ld_aux", ctypes.c_int64),
+        ("alpha", ctypes.c_float), ("act", ctypes.c_int), ("block_n", ctypes.c_int), ("split_k", ctypes.c_int),
+        ("workspace", ctypes.c_void_p),
+    ]
+
+
 # every symbol include/mpx_b200.h declares: (name, restype, argtypes)
 SIGNATURES = {
     "mpx_last_error": (ctypes.c_char_p, []),
@@ -54,6 +74,7 @@ SIGNATURES = {
     "mpx_optimizer_step": (ctypes.c_int, [_PP, _I32P, _PP, _PP, _PP, _PP, _PP, _I64P, ctypes.c_int,
                                           ctypes.c_int, ctypes.c_int, ctypes.c_int, AdamHParamsC,
                                           _P, ctypes.c_int64, _P, ctypes.c_double, _P, _P, _P]),
+    "mpx_gemm": (ctypes.c_int, [ctypes.POINTER(GemmDescC), _P]),
 }
 
 _lib = None

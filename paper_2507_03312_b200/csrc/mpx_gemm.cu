@@ -1,0 +1,457 @@
+// K5 — tcgen05 GEMM for the ViT forward/backward contractions (sm_100a).
+//
+// Replaces the reference's stepwise matmul (tensors.py:387-422) and its
+// backward rule (autodiff.py:193-205) with half-precision operands and f32
+// accumulation in TMEM (the north star's mandate).
+//
+//   C[z][m, n] = epilogue( alpha * sum_k A[z][m, k] * B[z][k, n] )
+//
+// A and B are each either K-major (k contiguous) or MN-major (m / n
+// contiguous), so one kernel serves forward (x @ W), dgrad (dY @ W^T) and
+// wgrad (X^T @ dY) without any transpose copies, and batched attention
+// (Q K^T, P V, ...) through 4-D TMA tensor maps over the [B, N, 3, H, hd]
+// qkv layout.
+//
+// Structure (one CTA per SM, persistent, 192 threads):
+//   warp 0      TMA producer: 128B-swizzled A/B tiles into a 4-stage smem ring
+//   warp 1      MMA issuer: tcgen05.mma M=128 x N=BN x K=16, f32 accumulators in
+//               TMEM, double-buffered (2 x 256 columns) so the epilogue of tile
+//               i overlaps the MMAs of tile i+1; owns TMEM alloc/dealloc
+//   warps 2..5  epilogue: tcgen05.ld -> alpha, +bias, GELU (saving the
+//               pre-activation), GELU' (backward), +residual -> f16/bf16/f32
+// Tiles are rastered in groups of 16 M-blocks so the A panels and the whole
+// B operand of the CTAs in flight stay L2-resident.
+#include "mpx_common.cuh"
+#include "sm100_ptx.cuh"
+
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+namespace mpx {
+
+using namespace ptx;
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kBNMax = 256;
+constexpr int kStages = 4;
+constexpr int kATileBytes = kBM * kBK * 2;       // 16 KB
+constexpr int kBTileBytes = kBNMax * kBK * 2;    // 32 KB
+constexpr int kGemmThreads = 192;
+constexpr int kGroupM = 16;
+constexpr size_t kGemmSmem = 1024 + kStages * (kATileBytes + kBTileBytes) + 256;
+
+enum { ACT_NONE = 0, ACT_GELU = 1, ACT_GELU_BWD = 2 };
+
+struct GemmParams {
+  int M, N, K, BN;
+  int N_store;     // N rounded up to 8: stores cover whole 8-column groups
+  int a_mn, b_mn;  // operand majorness: 0 = K-major, 1 = MN-major
+  int nb1, nbatch, split;
+  int m_blocks, n_blocks, k_blocks, kb_per_split;
+  long long total_tiles;
+  uint32_t idesc;
+  int ab_fmt;  // 0 = f16, 1 = bf16 (also the dtype of bias/residual/aux)
+  // epilogue
+  void* C;
+  long long ldc, c_sb1, c_sb2;
+  int c_dtype;  // MPX_F32 / MPX_F16 / MPX_BF16
+  const void* bias;
+  const void* res;
+  long long ldr, r_sb1, r_sb2;
+  void* aux;  // ACT_GELU: pre-activation out; ACT_GELU_BWD: pre-activation in
+  long long ld_aux;
+  float alpha;
+  int act;
+  float* ws;  // split-K partials [split][M][N] (f32)
+};
+
+__device__ __forceinline__ float half_to_f32(uint16_t h, int fmt) {
+  return fmt ? to_f32<MPX_BF16>(h) : to_f32<MPX_F16>(h);
+}
+__device__ __forceinline__ uint16_t f32_to_half(float x, int fmt) {
+  return fmt ? from_f32<MPX_BF16>(x) : from_f32<MPX_F16>(x);
+}
+
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// tanh-approximation GELU and its derivative (tensors.py:196-200, autodiff.py:173-185)
+__device__ __forceinline__ float gelu_f(float x) {
+  const float c0 = 0.7978845608028654f, c1 = 0.044715f;
+  return 0.5f * x * (1.f + tanh_fast(c0 * (x + c1 * x * x * x)));
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  const float c0 = 0.7978845608028654f, c1 = 0.044715f;
+  const float t = tanh_fast(c0 * (x + c1 * x * x * x));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c0 * (1.f + 3.f * c1 * x * x);
+}
+
+struct TileCoord {
+  int z, s, m_blk, n_blk;
+};
+__device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, long long t) {
+  const long long per_mn = (long long)P.m_blocks * P.n_blocks;
+  const long long zs = t / per_mn;
+  const int r = (int)(t - zs * per_mn);
+  TileCoord c;
+  c.z = (int)(zs / P.split);
+  c.s = (int)(zs - (long long)c.z * P.split);
+  const int group = r / (kGroupM * P.n_blocks);
+  const int first_m = group * kGroupM;
+  const int gm = min(kGroupM, P.m_blocks - first_m);
+  const int in = r - group * kGroupM * P.n_blocks;
+  c.m_blk = first_m + in % gm;
+  c.n_blk = in / gm;
+  return c;
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ GemmParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kATileBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBTileBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const uint32_t a_bytes = kATileBytes;
+  const uint32_t b_bytes = (uint32_t)P.BN * kBK * 2;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+        const TileCoord tc = tile_coord(P, t);
+        const int b1 = tc.z % P.nb1, b2 = tc.z / P.nb1;
+        const int m0 = tc.m_blk * kBM, n0 = tc.n_blk * P.BN;
+        const int kb0 = tc.s * P.kb_per_split;
+        const int kb1 = min(P.k_blocks, kb0 + P.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], a_bytes + b_bytes);
+          uint8_t* a = sA + stage * kATileBytes;
+          uint8_t* b = sB + stage * kBTileBytes;
+          const int k0 = kb * kBK;
+          if (!P.a_mn) {
+            tma_load_4d(a, &tmA, &full[stage], k0, m0, b1, b2);
+          } else {
+            tma_load_4d(a, &tmA, &full[stage], m0, k0, b1, b2);
+            tma_load_4d(a + 8192, &tmA, &full[stage], m0 + 64, k0, b1, b2);
+          }
+          if (!P.b_mn) {
+            tma_load_4d(b, &tmB, &full[stage], k0, n0, b1, b2);
+          } else {
+            for (int c = 0; c < P.BN / 64; ++c) tma_load_4d(b + c * 8192, &tmB, &full[stage], n0 + 64 * c, k0, b1, b2);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (long long t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+        const TileCoord tc = tile_coord(P, t);
+        const int kb0 = tc.s * P.kb_per_split;
+        const int kb1 = min(P.k_blocks, kb0 + P.kb_per_split);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * 256;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a = smem_u32(sA + stage * kATileBytes);
+          const uint32_t b = smem_u32(sB + stage * kBTileBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t ad = P.a_mn ? sw128_desc(a + k * 2048, 8192, 1024) : sw128_desc(a + k * 32, 16, 1024);
+            const uint64_t bd = P.b_mn ? sw128_desc(b + k * 2048, 8192, 1024) : sw128_desc(b + k * 32, 16, 1024);
+            umma_f16(d, ad, bd, P.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);  // smem slot free once these MMAs have read it
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // -------------------------------------------------- epilogue (128 thr)
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (long long t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+      const TileCoord tc = tile_coord(P, t);
+      const int b1 = tc.z % P.nb1, b2 = tc.z / P.nb1;
+      const int row = tc.m_blk * kBM + q * 32 + lane;
+      const int n0 = tc.n_blk * P.BN;
+      const bool row_ok = row < P.M;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
+      for (int c = 0; c < P.BN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(taddr + c, r);
+        tmem_ld_wait();
+        const int col = n0 + c;
+        if (col >= P.N_store || !row_ok) continue;
+        const int ncols = min(16, P.N_store - col);  // 8 or 16
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]) * P.alpha;
+        if (P.split > 1) {
+          float* w = P.ws + ((long long)tc.s * P.M + row) * P.N + col;
+          for (int i = 0; i < ncols; i += 4) *reinterpret_cast<float4*>(w + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          continue;
+        }
+        if (P.bias) {
+          const uint16_t* bb = static_cast<const uint16_t*>(P.bias) + col;
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (i < ncols) v[i] += half_to_f32(bb[i], P.ab_fmt);
+        }
+        if (P.act == ACT_GELU) {
+          if (P.aux) {
+            uint16_t* ax = static_cast<uint16_t*>(P.aux) + (long long)row * P.ld_aux + col;
+            uint32_t pk[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint16_t lo = f32_to_half(v[2 * i], P.ab_fmt), hi = f32_to_half(v[2 * i + 1], P.ab_fmt);
+              pk[i] = (uint32_t)lo | ((uint32_t)hi << 16);
+              v[2 * i] = half_to_f32(lo, P.ab_fmt);  // GELU of the rounded pre-activation
+              v[2 * i + 1] = half_to_f32(hi, P.ab_fmt);
+            }
+            *reinterpret_cast<uint4*>(ax) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            if (ncols == 16) *reinterpret_cast<uint4*>(ax + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = gelu_f(v[i]);
+        } else if (P.act == ACT_GELU_BWD) {
+          const uint16_t* ax = static_cast<const uint16_t*>(P.aux) + (long long)row * P.ld_aux + col;
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (i < ncols) v[i] *= gelu_grad_f(half_to_f32(ax[i], P.ab_fmt));
+        }
+        if (P.res) {
+          const uint16_t* rr = static_cast<const uint16_t*>(P.res) + b1 * P.r_sb1 + b2 * P.r_sb2 +
+                               (long long)row * P.ldr + col;
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (i < ncols) v[i] += half_to_f32(rr[i], P.ab_fmt);
+        }
+        const long long off = b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ldc + col;
+        if (P.c_dtype == MPX_F32) {
+          float* o = static_cast<float*>(P.C) + off;
+          for (int i = 0; i < ncols; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
+          const int f = P.c_dtype == MPX_BF16 ? 1 : 0;
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            pk[i] = (uint32_t)f32_to_half(v[2 * i], f) | ((uint32_t)f32_to_half(v[2 * i + 1], f) << 16);
+          uint16_t* o = static_cast<uint16_t*>(P.C) + off;
+          *reinterpret_cast<uint4*>(o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          if (ncols == 16) *reinterpret_cast<uint4*>(o + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// split-K: C = cast(sum_s ws[s]) (+ bias)
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int split, long long mn, int N, void* C,
+                                     long long ldc, int c_dtype, const void* bias, int ab_fmt) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < mn; i += (long long)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < split; ++k) s += ws[k * mn + i];
+    const long long row = i / N, col = i - row * N;
+    if (bias) s += half_to_f32(static_cast<const uint16_t*>(bias)[col], ab_fmt);
+    const long long o = row * ldc + col;
+    if (c_dtype == MPX_F32)
+      static_cast<float*>(C)[o] = s;
+    else
+      static_cast<uint16_t*>(C)[o] = f32_to_half(s, c_dtype == MPX_BF16 ? 1 : 0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 4-D map: (inner, outer, b1, b2) with byte strides for dims 1..3
+static int make_map(CUtensorMap* m, const void* ptr, int ab_fmt, uint64_t inner, uint64_t outer, uint64_t nb1,
+                    uint64_t nb2, uint64_t s_outer, uint64_t s_b1, uint64_t s_b2, uint32_t box_inner,
+                    uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return fail(MPX_EINVAL, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {inner, outer, nb1, nb2};
+  cuuint64_t strides[3] = {s_outer, s_b1, s_b2};
+  cuuint32_t box[4] = {box_inner, box_outer, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, ab_fmt ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+                  const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MPX_EINVAL, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return 0;
+}
+
+static uint64_t nz_stride(int64_t s, uint64_t fallback) { return s > 0 ? (uint64_t)s : fallback; }
+
+}  // namespace mpx
+
+using namespace mpx;
+
+extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
+  if (!g) return fail(MPX_EINVAL, "mpx_gemm: null desc");
+  if (g->ab_dtype != MPX_F16 && g->ab_dtype != MPX_BF16) return fail(MPX_EINVAL, "mpx_gemm: A/B must be f16/bf16");
+  if (g->M <= 0 || g->N <= 0 || g->K <= 0) return fail(MPX_EINVAL, "mpx_gemm: empty problem");
+  const int n_store = (g->N + 7) / 8 * 8;
+  if (n_store != g->N && (g->split_k > 1 || g->ldc < n_store))
+    return fail(MPX_EINVAL, "mpx_gemm: N not a multiple of 8 needs ldc >= round_up(N, 8) and no split-K");
+  const int fmt = g->ab_dtype == MPX_BF16 ? 1 : 0;
+  const int nb1 = g->nb1 > 0 ? g->nb1 : 1, nb2 = g->nb2 > 0 ? g->nb2 : 1;
+  int BN = g->block_n;
+  if (BN <= 0) BN = g->N >= kBNMax ? kBNMax : ((g->N + 15) / 16) * 16;
+  if (g->b_mn_major) BN = ((BN + 63) / 64) * 64;
+  if (BN > kBNMax || BN % 16) return fail(MPX_EINVAL, "mpx_gemm: bad block_n");
+  const int split = g->split_k > 1 ? g->split_k : 1;
+  if (split > 1 && (nb1 * nb2 != 1 || !g->workspace)) return fail(MPX_EINVAL, "mpx_gemm: split-K needs batch 1 + workspace");
+  if (split > 1 && g->act != ACT_NONE) return fail(MPX_EINVAL, "mpx_gemm: split-K supports no activation");
+
+  const uint64_t es = 2;
+  CUtensorMap ta, tb;
+  int rc;
+  // A: K-major dims (K, M), MN-major dims (M, K); lda = element stride of the outer dim
+  if (!g->a_mn_major)
+    rc = make_map(&ta, g->A, fmt, g->K, g->M, nb1, nb2, g->lda * es, nz_stride(g->a_sb1 * es, g->lda * es * g->M),
+                  nz_stride(g->a_sb2 * es, g->lda * es * g->M * nb1), 64, kBM);
+  else
+    rc = make_map(&ta, g->A, fmt, g->M, g->K, nb1, nb2, g->lda * es, nz_stride(g->a_sb1 * es, g->lda * es * g->K),
+                  nz_stride(g->a_sb2 * es, g->lda * es * g->K * nb1), 64, 64);
+  if (rc) return rc;
+  if (!g->b_mn_major)
+    rc = make_map(&tb, g->B, fmt, g->K, g->N, nb1, nb2, g->ldb * es, nz_stride(g->b_sb1 * es, g->ldb * es * g->N),
+                  nz_stride(g->b_sb2 * es, g->ldb * es * g->N * nb1), 64, BN);
+  else
+    rc = make_map(&tb, g->B, fmt, g->N, g->K, nb1, nb2, g->ldb * es, nz_stride(g->b_sb1 * es, g->ldb * es * g->K),
+                  nz_stride(g->b_sb2 * es, g->ldb * es * g->K * nb1), 64, 64);
+  if (rc) return rc;
+
+  GemmParams P{};
+  P.M = g->M;
+  P.N = g->N;
+  P.N_store = n_store;
+  P.K = g->K;
+  P.BN = BN;
+  P.a_mn = g->a_mn_major;
+  P.b_mn = g->b_mn_major;
+  P.nb1 = nb1;
+  P.nbatch = nb1 * nb2;
+  P.split = split;
+  P.m_blocks = (g->M + kBM - 1) / kBM;
+  P.n_blocks = (g->N + BN - 1) / BN;
+  P.k_blocks = (g->K + kBK - 1) / kBK;
+  P.kb_per_split = (P.k_blocks + split - 1) / split;
+  P.total_tiles = (long long)P.nbatch * split * P.m_blocks * P.n_blocks;
+  P.idesc = ptx::idesc_f16(fmt, kBM, BN, g->a_mn_major, g->b_mn_major);
+  P.ab_fmt = fmt;
+  P.C = g->C;
+  P.ldc = g->ldc;
+  P.c_sb1 = g->c_sb1;
+  P.c_sb2 = g->c_sb2;
+  P.c_dtype = g->c_dtype;
+  P.bias = g->bias;
+  P.res = g->residual;
+  P.ldr = g->ldr;
+  P.r_sb1 = g->r_sb1;
+  P.r_sb2 = g->r_sb2;
+  P.aux = g->aux;
+  P.ld_aux = g->ld_aux;
+  P.alpha = g->alpha == 0.f ? 1.f : g->alpha;
+  P.act = g->act;
+  P.ws = static_cast<float*>(g->workspace);
+  if (split > 1 && (long long)(split - 1) * P.kb_per_split >= P.k_blocks)
+    return fail(MPX_EINVAL, "mpx_gemm: split_k too large for K");
+
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [] {
+    attr_err = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+  });
+  if (attr_err != cudaSuccess) return fail((int)attr_err, "cudaFuncSetAttribute(gemm_kernel)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const long long grid = std::min<long long>(P.total_tiles, current_num_sms());
+  gemm_kernel<<<(unsigned)grid, kGemmThreads, kGemmSmem, st>>>(ta, tb, P);
+  MPX_LAUNCH_CHECK("gemm_kernel");
+  if (split > 1) {
+    const long long mn = (long long)g->M * g->N;
+    splitk_reduce_kernel<<<current_num_sms() * 4, 256, 0, st>>>(P.ws, split, mn, g->N, g->C, g->ldc, g->c_dtype,
+                                                               g->bias, fmt);
+    MPX_LAUNCH_CHECK("splitk_reduce_kernel");
+  }
+  return 0;
+}

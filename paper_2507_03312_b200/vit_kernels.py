@@ -1,0 +1,83 @@
+"""Tensor-level wrappers of the ViT kernels (K5 GEMM, K6 attention softmax,
+K7 LayerNorm, K9 cross-entropy, patchify, column sums).  torch provides
+memory and streams; every arithmetic op runs in libmpx_b200.so."""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native as _nat
+from .kernels import require_cuda, stream_handle
+
+_CODE = {torch.float32: _nat.MPX_F32, torch.float16: _nat.MPX_F16, torch.bfloat16: _nat.MPX_BF16}
+ACT_NONE, ACT_GELU, ACT_GELU_BWD = 0, 1, 2
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None else None
+
+
+def gemm(A, B, *, M, N, K, lda, ldb, a_mn=False, b_mn=False, out=None, ldc=None, out_dtype=None, bias=None,
+         residual=None, ldr=None, aux=None, ld_aux=None, act=ACT_NONE, alpha=1.0, nb=(1, 1), a_sb=(0, 0),
+         b_sb=(0, 0), c_sb=(0, 0), r_sb=(0, 0), split_k=1, workspace=None, block_n=0):
+    """C = epi(alpha * A @ B) on the tcgen05 GEMM (see mpx_gemm_desc)."""
+    require_cuda([A, B], "gemm")
+    if A.dtype != B.dtype or A.dtype not in (torch.float16, torch.bfloat16):
+        raise TypeError("gemm operands must share f16/bf16")
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype or A.dtype, device=A.device)
+        ldc = N
+    if split_k > 1 and workspace is None:
+        workspace = torch.empty(split_k * M * N, dtype=torch.float32, device=A.device)
+    d = _nat.GemmDescC()
+    d.ab_dtype = _CODE[A.dtype]
+    d.M, d.N, d.K = M, N, K
+    d.A, d.lda, d.a_sb1, d.a_sb2, d.a_mn_major = A.data_ptr(), lda, a_sb[0], a_sb[1], int(a_mn)
+    d.B, d.ldb, d.b_sb1, d.b_sb2, d.b_mn_major = B.data_ptr(), ldb, b_sb[0], b_sb[1], int(b_mn)
+    d.nb1, d.nb2 = nb
+    d.C, d.ldc, d.c_sb1, d.c_sb2, d.c_dtype = out.data_ptr(), ldc if ldc is not None else N, c_sb[0], c_sb[1], \
+        _CODE[out.dtype]
+    d.bias = _ptr(bias)
+    d.residual = _ptr(residual)
+    d.ldr = ldr if ldr is not None else N
+    d.r_sb1, d.r_sb2 = r_sb
+    d.aux = _ptr(aux)
+    d.ld_aux = ld_aux if ld_aux is not None else N
+    d.alpha = alpha
+    d.act = act
+    d.block_n = block_n
+    d.split_k = split_k
+    d.workspace = _ptr(workspace)
+    _nat.check(_nat.load().mpx_gemm(ctypes.byref(d), stream_handle(A.device)), "mpx_gemm")
+    return out
+
+
+# ---------------------------------------------------------------- linears
+def linear_fwd(x, w, bias=None, act=ACT_NONE, aux=None, residual=None, out=None):
+    """y[M,N] = x[M,K] @ w[K,N] (+bias, GELU saving pre-act in aux, +residual)."""
+    M, K = x.shape
+    N_ = w.shape[1]
+    return gemm(x, w, M=M, N=N_, K=K, lda=K, ldb=N_, b_mn=True, bias=bias, act=act, aux=aux, residual=residual,
+                out=out, ldc=N_ if out is not None else None)
+
+
+def linear_dgrad(dy, w, aux=None, out=None):
+    """dx[M,K] = dy[M,N] @ w[K,N]^T; with aux (the GELU pre-activation of
+    this layer's input) the GELU derivative is applied in the epilogue."""
+    M, N_ = dy.shape
+    K = w.shape[0]
+    return gemm(dy, w, M=M, N=K, K=N_, lda=N_, ldb=N_, aux=aux, ld_aux=K,
+                act=ACT_GELU_BWD if aux is not None else ACT_NONE, out=out, ldc=K if out is not None else None)
+
+
+def linear_wgrad(x, dy, out=None, split_k=None):
+    """dw[K,N] = x[M,K]^T @ dy[M,N] (reduction over the M tokens)."""
+    M, K = x.shape
+    N_ = dy.shape[1]
+    if split_k is None:
+        tiles = -(-K // 128) * -(-N_ // 256)
+        sms = torch.cuda.get_device_properties(x.device).multi_processor_count
+        split_k = max(1, min(8, sms // max(tiles, 1), M // 2048))
+    return gemm(x, dy, M=K, N=N_, K=M, lda=K, ldb=N_, a_mn=True, b_mn=True, out=out,
+                ldc=N_ if out is not None else None, split_k=split_k)

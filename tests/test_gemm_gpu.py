@@ -1,0 +1,90 @@
+"""K5 tcgen05 GEMM vs a plain fp32 torch reference of the same op (same
+half-precision inputs; f32 accumulation; output rounded once)."""
+import pytest
+import torch
+
+from paper_2507_03312_b200 import vit_kernels as VK
+
+pytestmark = pytest.mark.gpu
+
+
+def close(got, want, rel=None):
+    want = want.float()
+    got = got.float()
+    tol = rel if rel is not None else (1e-2 if got.dtype == torch.bfloat16 else 4e-3)
+    err = (got - want).abs().max().item()
+    scale = want.abs().max().item() + 1e-6
+    assert err <= tol * scale, f"max err {err} vs scale {scale}"
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (384, 768, 768), (200, 1000, 96), (50, 64, 48), (1000, 2304, 256)])
+def test_linear_fwd_dgrad_wgrad(cuda, dt, M, N, K):
+    g = torch.Generator(device=cuda).manual_seed(M * 7 + N)
+    x = torch.randn(M, K, device=cuda, generator=g).to(dt)
+    w = (torch.randn(K, N, device=cuda, generator=g) / K ** 0.5).to(dt)
+    y = VK.linear_fwd(x, w)
+    close(y, x.float() @ w.float())
+    dy = torch.randn(M, N, device=cuda, generator=g).to(dt)
+    dx = VK.linear_dgrad(dy, w)
+    close(dx, dy.float() @ w.float().t())
+    for split in (1, 2):
+        if (M + 63) // 64 < split:
+            continue
+        dw = VK.linear_wgrad(x, dy, split_k=split)
+        close(dw, x.float().t() @ dy.float())
+
+
+def test_epilogue_bias_gelu_residual_alpha(cuda):
+    dt = torch.bfloat16
+    M, N, K = 300, 512, 192
+    x = torch.randn(M, K, device=cuda).to(dt)
+    w = (torch.randn(K, N, device=cuda) / K ** 0.5).to(dt)
+    b = torch.randn(N, device=cuda).to(dt)
+    r = torch.randn(M, N, device=cuda).to(dt)
+    pre = torch.empty(M, N, device=cuda, dtype=dt)
+    y = VK.linear_fwd(x, w, bias=b, act=VK.ACT_GELU, aux=pre)
+    z = x.float() @ w.float() + b.float()
+    close(pre, z)
+    close(y, torch.nn.functional.gelu(pre.float(), approximate="tanh"))
+    y2 = VK.linear_fwd(x, w, bias=b, residual=r)
+    close(y2, z + r.float())
+    # GELU backward in the dgrad epilogue
+    dh = torch.randn(M, N, device=cuda).to(dt)
+    w2 = (torch.randn(K, N, device=cuda) / N ** 0.5).to(dt)
+    dz = VK.linear_dgrad(dh, w2)
+    close(dz, dh.float() @ w2.float().t())
+    zin = torch.randn(M, K, device=cuda).to(dt)
+    dzg = VK.linear_dgrad(dh, w2, aux=zin)
+    zz = zin.float().requires_grad_(True)
+    torch.nn.functional.gelu(zz, approximate="tanh").backward(dh.float() @ w2.float().t())
+    close(dzg, zz.grad, rel=2e-2)
+    # alpha + f32 output
+    o = VK.gemm(x, w, M=M, N=N, K=K, lda=K, ldb=N, b_mn=True, alpha=0.125, out_dtype=torch.float32)
+    close(o, 0.125 * (x.float() @ w.float()), rel=1e-3)
+
+
+def test_batched_strided_attention_shapes(cuda):
+    """Q K^T and P V straight out of the [B, N, 3, H, hd] qkv layout."""
+    dt = torch.float16
+    Bsz, Nt, H, hd = 3, 197, 4, 64
+    D = H * hd
+    qkv = torch.randn(Bsz * Nt, 3 * D, device=cuda).to(dt)
+    q = qkv.view(Bsz, Nt, 3, H, hd)[:, :, 0]
+    k = qkv.view(Bsz, Nt, 3, H, hd)[:, :, 1]
+    v = qkv.view(Bsz, Nt, 3, H, hd)[:, :, 2]
+    ldS = 208
+    S = torch.zeros(Bsz, H, Nt, ldS, device=cuda, dtype=dt)
+    VK.gemm(qkv, qkv[:, D:], M=Nt, N=Nt, K=hd, lda=3 * D, ldb=3 * D, nb=(H, Bsz), a_sb=(hd, Nt * 3 * D),
+            b_sb=(hd, Nt * 3 * D), out=S, ldc=ldS, c_sb=(Nt * ldS, H * Nt * ldS), alpha=0.125)
+    ref = torch.einsum("bnhd,bmhd->bhnm", q.float(), k.float()) * 0.125
+    close(S[..., :Nt], ref)
+    P = torch.softmax(S[..., :Nt].float(), -1).to(dt)
+    Ppad = torch.zeros(Bsz, H, Nt, ldS, device=cuda, dtype=dt)
+    Ppad[..., :Nt] = P
+    O = torch.empty(Bsz * Nt, D, device=cuda, dtype=dt)
+    # O[b, n, h, :] = P[b,h] @ V[b,:,h,:]  (B operand MN-major: hd contiguous)
+    VK.gemm(Ppad, qkv[:, 2 * D:], M=Nt, N=hd, K=Nt, lda=ldS, ldb=3 * D, b_mn=True, nb=(H, Bsz),
+            a_sb=(Nt * ldS, H * Nt * ldS), b_sb=(hd, Nt * 3 * D), out=O, ldc=D, c_sb=(hd, Nt * D))
+    refO = torch.einsum("bhnm,bmhd->bnhd", P.float(), v.float()).reshape(Bsz * Nt, D)
+    close(O, refO)
