@@ -131,7 +131,8 @@ int mpx_optimizer_step(void* const* h_p, const int32_t* h_p_dtype, float* const*
  *   C[z][m,n] = epi(alpha * sum_k A[z][m,k] * B[z][k,n]),  z = b1 + nb1*b2
  * A is K-major (element (m,k) at A[m*lda + k]) or MN-major (A[k*lda + m]);
  * B is K-major (B[n*ldb + k]) or MN-major (B[k*ldb + n]); *_sb1/_sb2 are the
- * element strides of the two batch dims (0 = dense).  Strides must be
+ * element strides of the two batch dims (0 = the operand is shared across that
+ * dim, e.g. one weight for every image; likewise r_sb* for the residual).  Strides must be
  * multiples of 8 elements (16-byte TMA rule).  When N is not a multiple of 8
  * the epilogue writes whole 8-column groups (the pad columns get the value of
  * zero-filled operands), so ldc must be >= round_up(N, 8).
@@ -166,6 +167,46 @@ typedef struct mpx_gemm_desc {
 } mpx_gemm_desc;
 
 int mpx_gemm(const mpx_gemm_desc* desc, void* stream);
+
+/* ---- ViT kernels around the GEMMs (f32 islands + reductions) ----------- */
+/* K7 LayerNorm over the last dim, f32 inside (tensors.py:459-491, used as an
+ * island at bench.py:185-187).  x/y rows have element strides ldx/ldy; mean
+ * and rstd (f32 per row) are saved for the backward. */
+int mpx_layernorm_fwd(int dtype, const void* x, int64_t ldx, const void* gain, const void* bias, void* y,
+                      int64_t ldy, float* mean, float* rstd, int rows, int D, float eps, void* stream);
+/* backward (autodiff.py:243-262): dx (+ dres residual cotangent), dgain and
+ * dbias (column sums, written as dtype).  workspace: 2*mpx_layernorm_bwd_blocks(rows)*D f32 */
+int mpx_layernorm_bwd_blocks(int rows);
+int mpx_layernorm_bwd(int dtype, const void* x, int64_t ldx, const void* gain, const float* mean, const float* rstd,
+                      const void* dy, int64_t lddy, const void* dres, int64_t ldres, void* dx, int64_t lddx,
+                      void* dgain, void* dbias, float* workspace, int rows, int D, void* stream);
+/* out[z][c] = alpha * sum_r x[z][r][c]: bias / position gradients
+ * (_unbroadcast, autodiff.py:88-99) and the mean-pool island; deterministic
+ * two passes through workspace (>= splits*cols*batches f32). */
+int mpx_colsum(int dtype, const void* x, int64_t ldx, int64_t sbx, int rows, int cols, int batches, float* workspace,
+               int64_t workspace_floats, void* out, int64_t ld_out, int out_dtype, float alpha, void* stream);
+/* K6 softmax over rows of length L (row stride ld, pad columns written 0),
+ * f32 inside (tensors.py:431-446); backward dS = y*(dP - sum(dP*y)) with y
+ * recomputed from S in f32 (autodiff.py:233-240). */
+int mpx_softmax_fwd(int dtype, const void* S, void* P, int64_t rows, int L, int64_t ld, void* stream);
+int mpx_softmax_bwd(int dtype, const void* S, const void* dP, void* dS, int64_t rows, int L, int64_t ld, void* stream);
+/* K9 mean cross-entropy in f32 (tensors.py:494-522): nll_ws[B] scratch,
+ * *loss (device f32).  Backward (autodiff.py:265-276): dlogits =
+ * (softmax - onehot) * (*d_dloss) / B, columns >= C of each ld_d row zeroed. */
+int mpx_cross_entropy_fwd(int dtype, const void* logits, int64_t ld, const int32_t* labels, int B, int C,
+                          float* nll_ws, float* loss, void* stream);
+int mpx_cross_entropy_bwd(int dtype, const void* logits, int64_t ld, const int32_t* labels, int B, int C,
+                          const float* d_dloss, void* dlogits, int64_t ld_d, void* stream);
+/* image [B,H,W,C] -> patch rows [B*(H/P)*(W/P), P*P*C], order (py, px, c) */
+int mpx_patchify(int dtype, const void* img, void* patches, int B, int H, int W, int C, int P, void* stream);
+/* strided row copy dst[b][r][c] = src[b][r][c] */
+int mpx_copy_rows(int dtype, const void* src, int64_t ld_src, int64_t sb_src, void* dst, int64_t ld_dst,
+                  int64_t sb_dst, int rows, int batches, int cols, void* stream);
+/* dst[b*sb + c] = a[c] + b[c] (cls token + its position embedding) */
+int mpx_rows_add(int dtype, const void* a, const void* b, void* dst, int64_t sb, int B, int D, void* stream);
+/* dst[b][r][c] = alpha * src[b][c] (mean-pool backward) */
+int mpx_bcast_rows(int dtype, const void* src, int64_t ld_src, void* dst, int64_t ld_dst, int64_t sb_dst, int rows,
+                   int B, int D, float alpha, void* stream);
 
 #ifdef __cplusplus
 }

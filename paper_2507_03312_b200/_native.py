@@ -75,6 +75,28 @@ SIGNATURES = {
                                           ctypes.c_int, ctypes.c_int, ctypes.c_int, AdamHParamsC,
                                           _P, ctypes.c_int64, _P, ctypes.c_double, _P, _P, _P]),
     "mpx_gemm": (ctypes.c_int, [ctypes.POINTER(GemmDescC), _P]),
+    "mpx_layernorm_fwd": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, _P, _P, _P, ctypes.c_int64, _P, _P,
+                                         ctypes.c_int, ctypes.c_int, ctypes.c_float, _P]),
+    "mpx_layernorm_bwd_blocks": (ctypes.c_int, [ctypes.c_int]),
+    "mpx_layernorm_bwd": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, _P, _P, _P, _P, ctypes.c_int64, _P,
+                                         ctypes.c_int64, _P, ctypes.c_int64, _P, _P, _P, ctypes.c_int, ctypes.c_int,
+                                         _P]),
+    "mpx_colsum": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_int, _P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_float,
+                                  _P]),
+    "mpx_softmax_fwd": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, _P]),
+    "mpx_softmax_bwd": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, _P]),
+    "mpx_cross_entropy_fwd": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, _P, ctypes.c_int, ctypes.c_int, _P,
+                                             _P, _P]),
+    "mpx_cross_entropy_bwd": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, _P, ctypes.c_int, ctypes.c_int, _P,
+                                             _P, ctypes.c_int64, _P]),
+    "mpx_patchify": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_int, _P]),
+    "mpx_copy_rows": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, ctypes.c_int64, _P, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]),
+    "mpx_rows_add": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P]),
+    "mpx_bcast_rows": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.c_int64,
+                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_float, _P]),
 }
 
 _lib = None

@@ -49,6 +49,7 @@ struct GemmParams {
   int N_store;     // N rounded up to 8: stores cover whole 8-column groups
   int a_mn, b_mn;  // operand majorness: 0 = K-major, 1 = MN-major
   int nb1, nbatch, split;
+  int a_bc1, a_bc2, b_bc1, b_bc2;  // operand shared across that batch dim (coordinate 0)
   int m_blocks, n_blocks, k_blocks, kb_per_split;
   long long total_tiles;
   uint32_t idesc;
@@ -164,16 +165,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint8_t* a = sA + stage * kATileBytes;
           uint8_t* b = sB + stage * kBTileBytes;
           const int k0 = kb * kBK;
+          const int ab1 = P.a_bc1 ? 0 : b1, ab2 = P.a_bc2 ? 0 : b2;
+          const int bb1 = P.b_bc1 ? 0 : b1, bb2 = P.b_bc2 ? 0 : b2;
           if (!P.a_mn) {
-            tma_load_4d(a, &tmA, &full[stage], k0, m0, b1, b2);
+            tma_load_4d(a, &tmA, &full[stage], k0, m0, ab1, ab2);
           } else {
-            tma_load_4d(a, &tmA, &full[stage], m0, k0, b1, b2);
-            tma_load_4d(a + 8192, &tmA, &full[stage], m0 + 64, k0, b1, b2);
+            tma_load_4d(a, &tmA, &full[stage], m0, k0, ab1, ab2);
+            tma_load_4d(a + 8192, &tmA, &full[stage], m0 + 64, k0, ab1, ab2);
           }
           if (!P.b_mn) {
-            tma_load_4d(b, &tmB, &full[stage], k0, n0, b1, b2);
+            tma_load_4d(b, &tmB, &full[stage], k0, n0, bb1, bb2);
           } else {
-            for (int c = 0; c < P.BN / 64; ++c) tma_load_4d(b + c * 8192, &tmB, &full[stage], n0 + 64 * c, k0, b1, b2);
+            for (int c = 0; c < P.BN / 64; ++c) tma_load_4d(b + c * 8192, &tmB, &full[stage], n0 + 64 * c, k0, bb1, bb2);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -359,7 +362,10 @@ static int make_map(CUtensorMap* m, const void* ptr, int ab_fmt, uint64_t inner,
   return 0;
 }
 
+// a zero batch stride means "shared across that batch dim": the map gets
+// extent 1 there (TMA strides must be non-zero) and the kernel uses coordinate 0
 static uint64_t nz_stride(int64_t s, uint64_t fallback) { return s > 0 ? (uint64_t)s : fallback; }
+static uint64_t ext(int64_t s, int n) { return s > 0 ? (uint64_t)n : 1u; }
 
 }  // namespace mpx
 
@@ -386,19 +392,20 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   CUtensorMap ta, tb;
   int rc;
   // A: K-major dims (K, M), MN-major dims (M, K); lda = element stride of the outer dim
+  const uint64_t an1 = ext(g->a_sb1, nb1), an2 = ext(g->a_sb2, nb2), bn1 = ext(g->b_sb1, nb1), bn2 = ext(g->b_sb2, nb2);
   if (!g->a_mn_major)
-    rc = make_map(&ta, g->A, fmt, g->K, g->M, nb1, nb2, g->lda * es, nz_stride(g->a_sb1 * es, g->lda * es * g->M),
-                  nz_stride(g->a_sb2 * es, g->lda * es * g->M * nb1), 64, kBM);
+    rc = make_map(&ta, g->A, fmt, g->K, g->M, an1, an2, g->lda * es, nz_stride(g->a_sb1 * es, g->lda * es * g->M),
+                  nz_stride(g->a_sb2 * es, g->lda * es * g->M), 64, kBM);
   else
-    rc = make_map(&ta, g->A, fmt, g->M, g->K, nb1, nb2, g->lda * es, nz_stride(g->a_sb1 * es, g->lda * es * g->K),
-                  nz_stride(g->a_sb2 * es, g->lda * es * g->K * nb1), 64, 64);
+    rc = make_map(&ta, g->A, fmt, g->M, g->K, an1, an2, g->lda * es, nz_stride(g->a_sb1 * es, g->lda * es * g->K),
+                  nz_stride(g->a_sb2 * es, g->lda * es * g->K), 64, 64);
   if (rc) return rc;
   if (!g->b_mn_major)
-    rc = make_map(&tb, g->B, fmt, g->K, g->N, nb1, nb2, g->ldb * es, nz_stride(g->b_sb1 * es, g->ldb * es * g->N),
-                  nz_stride(g->b_sb2 * es, g->ldb * es * g->N * nb1), 64, BN);
+    rc = make_map(&tb, g->B, fmt, g->K, g->N, bn1, bn2, g->ldb * es, nz_stride(g->b_sb1 * es, g->ldb * es * g->N),
+                  nz_stride(g->b_sb2 * es, g->ldb * es * g->N), 64, BN);
   else
-    rc = make_map(&tb, g->B, fmt, g->N, g->K, nb1, nb2, g->ldb * es, nz_stride(g->b_sb1 * es, g->ldb * es * g->K),
-                  nz_stride(g->b_sb2 * es, g->ldb * es * g->K * nb1), 64, 64);
+    rc = make_map(&tb, g->B, fmt, g->N, g->K, bn1, bn2, g->ldb * es, nz_stride(g->b_sb1 * es, g->ldb * es * g->K),
+                  nz_stride(g->b_sb2 * es, g->ldb * es * g->K), 64, 64);
   if (rc) return rc;
 
   GemmParams P{};
@@ -411,6 +418,10 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   P.b_mn = g->b_mn_major;
   P.nb1 = nb1;
   P.nbatch = nb1 * nb2;
+  P.a_bc1 = g->a_sb1 <= 0;
+  P.a_bc2 = g->a_sb2 <= 0;
+  P.b_bc1 = g->b_sb1 <= 0;
+  P.b_bc2 = g->b_sb2 <= 0;
   P.split = split;
   P.m_blocks = (g->M + kBM - 1) / kBM;
   P.n_blocks = (g->N + BN - 1) / BN;

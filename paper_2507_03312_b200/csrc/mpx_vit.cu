@@ -1,0 +1,553 @@
+// ViT kernels around the GEMMs (sm_100a): the MPX full-precision islands
+// (LayerNorm, attention softmax, cross-entropy, mean-pool: f32 inside, half
+// at the boundary — precision.py:106-114 force_full_precision), patchify and
+// the reductions that produce bias / LayerNorm / position gradients.
+//
+//   K6 softmax fwd/bwd   tensors.py:431-446, autodiff.py:233-240 (island, bench.py:196-197)
+//   K7 layernorm fwd/bwd tensors.py:459-491, autodiff.py:243-262 (island, bench.py:185-187)
+//   K9 cross-entropy     tensors.py:494-522, autodiff.py:265-276
+//   colsum               _unbroadcast / reduce-sum backward (autodiff.py:88-99, 208-222)
+//
+// All are HBM-bound row/column sweeps: one warp per row for row ops (16-byte
+// loads when D % 256 == 0), deterministic two-pass column reductions (no
+// float atomics, so reruns are bit-identical).
+#include "mpx_common.cuh"
+
+namespace mpx {
+
+__device__ __forceinline__ float ld_h(const void* p, long long i, int fmt) {
+  const uint16_t h = static_cast<const uint16_t*>(p)[i];
+  return fmt ? to_f32<MPX_BF16>(h) : to_f32<MPX_F16>(h);
+}
+__device__ __forceinline__ void st_h(void* p, long long i, float x, int fmt) {
+  static_cast<uint16_t*>(p)[i] = fmt ? from_f32<MPX_BF16>(x) : from_f32<MPX_F16>(x);
+}
+__device__ __forceinline__ void unpack8(uint4 w, float* o, int fmt) {
+  const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint16_t lo = (uint16_t)(u[i] & 0xFFFF), hi = (uint16_t)(u[i] >> 16);
+    o[2 * i] = fmt ? to_f32<MPX_BF16>(lo) : to_f32<MPX_F16>(lo);
+    o[2 * i + 1] = fmt ? to_f32<MPX_BF16>(hi) : to_f32<MPX_F16>(hi);
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float* x, int fmt) {
+  uint32_t u[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint16_t lo = fmt ? from_f32<MPX_BF16>(x[2 * i]) : from_f32<MPX_F16>(x[2 * i]);
+    const uint16_t hi = fmt ? from_f32<MPX_BF16>(x[2 * i + 1]) : from_f32<MPX_F16>(x[2 * i + 1]);
+    u[i] = (uint32_t)lo | ((uint32_t)hi << 16);
+  }
+  return make_uint4(u[0], u[1], u[2], u[3]);
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ===========================================================================
+// K7 LayerNorm forward: y = (x - mean) * rstd * g + b over the last dim (f32)
+// ===========================================================================
+template <int V>  // V = 16-byte vectors per lane (D = 256 * V); V = 0: generic
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const void* __restrict__ x, long long ldx,
+                                                     const void* __restrict__ g, const void* __restrict__ b,
+                                                     void* __restrict__ y, long long ldy, float* __restrict__ mean,
+                                                     float* __restrict__ rstd, int rows, int D, float eps, int fmt) {
+  const int lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const void* xr = static_cast<const uint16_t*>(x) + row * ldx;
+  if (V > 0) {
+    float v[V > 0 ? V : 1][8];
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      unpack8(*reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(xr) + (j * 32 + lane) * 8), v[j], fmt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += v[j][e];
+    }
+    const float mu = warp_sum(s) / (float)D;
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float c = v[j][e] - mu;
+        q += c * c;
+      }
+    const float rs = rsqrtf(warp_sum(q) / (float)D + eps);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int c0 = (j * 32 + lane) * 8;
+      float gg[8], bb[8], o[8];
+      unpack8(*reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g) + c0), gg, fmt);
+      unpack8(*reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(b) + c0), bb, fmt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = (v[j][e] - mu) * rs * gg[e] + bb[e];
+      *reinterpret_cast<uint4*>(static_cast<uint16_t*>(y) + row * ldy + c0) = pack8(o, fmt);
+    }
+    if (lane == 0) {
+      mean[row] = mu;
+      rstd[row] = rs;
+    }
+  } else {
+    float s = 0.f;
+    for (int c = lane; c < D; c += 32) s += ld_h(xr, c, fmt);
+    const float mu = warp_sum(s) / (float)D;
+    float q = 0.f;
+    for (int c = lane; c < D; c += 32) {
+      const float d = ld_h(xr, c, fmt) - mu;
+      q += d * d;
+    }
+    const float rs = rsqrtf(warp_sum(q) / (float)D + eps);
+    for (int c = lane; c < D; c += 32)
+      st_h(y, row * ldy + c, (ld_h(xr, c, fmt) - mu) * rs * ld_h(g, c, fmt) + ld_h(b, c, fmt), fmt);
+    if (lane == 0) {
+      mean[row] = mu;
+      rstd[row] = rs;
+    }
+  }
+}
+
+// ===========================================================================
+// K7 LayerNorm backward.  dx = rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat))
+// (+ dres, the residual branch's cotangent); per-block partial column sums of
+// dy*xhat (dgain) and dy (dbias) into ws[2][gridDim][D].
+// ===========================================================================
+__global__ void __launch_bounds__(256) ln_bwd_kernel(const void* __restrict__ x, long long ldx,
+                                                     const void* __restrict__ g, const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd, const void* __restrict__ dy,
+                                                     long long lddy, const void* __restrict__ dres, long long ldres,
+                                                     void* __restrict__ dx, long long lddx, float* __restrict__ ws,
+                                                     int rows, int D, int fmt) {
+  extern __shared__ float sh[];  // [8 warps][2][D]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* my_dg = sh + warp * 2 * D;
+  float* my_db = my_dg + D;
+  for (int c = lane; c < D; c += 32) {
+    my_dg[c] = 0.f;
+    my_db[c] = 0.f;
+  }
+  for (long long row = (long long)blockIdx.x * 8 + warp; row < rows; row += (long long)gridDim.x * 8) {
+    const float mu = mean[row], rs = rstd[row];
+    float s1 = 0.f, s2 = 0.f;
+    for (int c = lane; c < D; c += 32) {
+      const float xh = (ld_h(x, row * ldx + c, fmt) - mu) * rs;
+      const float d = ld_h(dy, row * lddy + c, fmt);
+      const float dg = d * ld_h(g, c, fmt);
+      s1 += dg;
+      s2 += dg * xh;
+      my_dg[c] += d * xh;
+      my_db[c] += d;
+    }
+    s1 = warp_sum(s1) / (float)D;
+    s2 = warp_sum(s2) / (float)D;
+    for (int c = lane; c < D; c += 32) {
+      const float xh = (ld_h(x, row * ldx + c, fmt) - mu) * rs;
+      const float dg = ld_h(dy, row * lddy + c, fmt) * ld_h(g, c, fmt);
+      float o = rs * (dg - s1 - xh * s2);
+      if (dres) o += ld_h(dres, row * ldres + c, fmt);
+      st_h(dx, row * lddx + c, o, fmt);
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < D; c += blockDim.x) {
+    float a = 0.f, bsum = 0.f;
+    for (int w = 0; w < 8; ++w) {
+      a += sh[w * 2 * D + c];
+      bsum += sh[w * 2 * D + D + c];
+    }
+    ws[(long long)blockIdx.x * D + c] = a;
+    ws[(long long)gridDim.x * D + (long long)blockIdx.x * D + c] = bsum;
+  }
+}
+
+// sum ws partials over blocks -> half outputs (ws[0..nb) -> out0, ws[nb..2nb) -> out1)
+__global__ void partials_reduce_kernel(const float* __restrict__ ws, int nb, int D, void* out0, void* out1,
+                                       float alpha, int fmt) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < D; c += gridDim.x * blockDim.x) {
+    float a = 0.f, b = 0.f;
+    for (int k = 0; k < nb; ++k) {
+      a += ws[(long long)k * D + c];
+      b += ws[(long long)(nb + k) * D + c];
+    }
+    if (out0) st_h(out0, c, a * alpha, fmt);
+    if (out1) st_h(out1, c, b * alpha, fmt);
+  }
+}
+
+// ===========================================================================
+// column sums: out[z][c] = alpha * sum_r x[z][r][c]   (two deterministic passes)
+// block = 256 threads = 32 column-vectors of 8 x 8 row lanes
+// ===========================================================================
+__global__ void __launch_bounds__(256) colsum_partial_kernel(const void* __restrict__ x, long long ldx,
+                                                             long long sbx, int rows, int cols, int rows_per_split,
+                                                             float* __restrict__ ws, int fmt) {
+  __shared__ float sh[8][256];
+  const int cv = threadIdx.x & 31, rl = threadIdx.x >> 5;
+  const int c0 = blockIdx.x * 256 + cv * 8;
+  const int split = blockIdx.y, z = blockIdx.z;
+  const int r0 = split * rows_per_split, r1 = min(rows, r0 + rows_per_split);
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const uint16_t* base = static_cast<const uint16_t*>(x) + (long long)z * sbx;
+  const bool vec = (c0 + 8 <= cols) && ((ldx & 7) == 0) && ((sbx & 7) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  for (int r = r0 + rl; r < r1; r += 8) {
+    if (vec) {
+      float v[8];
+      unpack8(*reinterpret_cast<const uint4*>(base + (long long)r * ldx + c0), v, fmt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += v[e];
+    } else {
+      for (int e = 0; e < 8; ++e)
+        if (c0 + e < cols) acc[e] += ld_h(base, (long long)r * ldx + c0 + e, fmt);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) sh[rl][cv * 8 + e] = acc[e];
+  __syncthreads();
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c < cols) {
+    float s = 0.f;
+    for (int k = 0; k < 8; ++k) s += sh[k][threadIdx.x];
+    ws[((long long)z * gridDim.y + split) * cols + c] = s;
+  }
+}
+
+__global__ void colsum_final_kernel(const float* __restrict__ ws, int splits, int cols, int batches, void* out,
+                                    long long ld_out, int out_dtype, float alpha) {
+  const long long n = (long long)cols * batches;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long z = i / cols, c = i - z * cols;
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += ws[(z * splits + k) * cols + c];
+    s *= alpha;
+    if (out_dtype == MPX_F32)
+      static_cast<float*>(out)[z * ld_out + c] = s;
+    else
+      st_h(out, z * ld_out + c, s, out_dtype == MPX_BF16 ? 1 : 0);
+  }
+}
+
+// ===========================================================================
+// K6 attention softmax over rows of length L (row stride ld >= L, pads -> 0)
+// ===========================================================================
+__global__ void __launch_bounds__(256) softmax_fwd_kernel(const void* __restrict__ S, void* __restrict__ P,
+                                                          long long rows, int L, long long ld, int fmt) {
+  const int lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const long long base = row * ld;
+  float m = -INFINITY;
+  for (int c = lane; c < L; c += 32) m = fmaxf(m, ld_h(S, base + c, fmt));
+  m = warp_max(m);
+  float s = 0.f;
+  for (int c = lane; c < L; c += 32) s += expf(ld_h(S, base + c, fmt) - m);
+  s = warp_sum(s);
+  const float inv = 1.f / s;
+  for (int c = lane; c < ld; c += 32) st_h(P, base + c, c < L ? expf(ld_h(S, base + c, fmt) - m) * inv : 0.f, fmt);
+}
+
+// dS = y * (dP - sum(dP * y)),  y = softmax(S) recomputed in f32
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(const void* __restrict__ S, const void* __restrict__ dP,
+                                                          void* __restrict__ dS, long long rows, int L, long long ld,
+                                                          int fmt) {
+  const int lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const long long base = row * ld;
+  float m = -INFINITY;
+  for (int c = lane; c < L; c += 32) m = fmaxf(m, ld_h(S, base + c, fmt));
+  m = warp_max(m);
+  float s = 0.f;
+  for (int c = lane; c < L; c += 32) s += expf(ld_h(S, base + c, fmt) - m);
+  const float inv = 1.f / warp_sum(s);
+  float t = 0.f;
+  for (int c = lane; c < L; c += 32) t += ld_h(dP, base + c, fmt) * expf(ld_h(S, base + c, fmt) - m) * inv;
+  t = warp_sum(t);
+  for (int c = lane; c < ld; c += 32) {
+    float o = 0.f;
+    if (c < L) o = expf(ld_h(S, base + c, fmt) - m) * inv * (ld_h(dP, base + c, fmt) - t);
+    st_h(dS, base + c, o, fmt);
+  }
+}
+
+// ===========================================================================
+// K9 cross-entropy (f32 island): nll[b] = lse(z_b) - z_b[y_b]; loss = mean
+// ===========================================================================
+__global__ void __launch_bounds__(256) ce_fwd_kernel(const void* __restrict__ logits, long long ld,
+                                                     const int32_t* __restrict__ labels, int B, int C,
+                                                     float* __restrict__ nll, int fmt) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= B) return;
+  const long long base = (long long)row * ld;
+  float m = -INFINITY;
+  for (int c = lane; c < C; c += 32) m = fmaxf(m, ld_h(logits, base + c, fmt));
+  m = warp_max(m);
+  float s = 0.f;
+  for (int c = lane; c < C; c += 32) s += expf(ld_h(logits, base + c, fmt) - m);
+  s = warp_sum(s);
+  if (lane == 0) nll[row] = logf(s) - (ld_h(logits, base + labels[row], fmt) - m);
+}
+__global__ void ce_mean_kernel(const float* __restrict__ nll, int B, float* __restrict__ loss) {
+  __shared__ float sh[32];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) s += nll[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x + 31) / 32 ? sh[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) *loss = v / (float)B;
+  }
+}
+// dlogits = (softmax(z) - onehot(y)) * dloss / B   (dloss read on the device)
+__global__ void __launch_bounds__(256) ce_bwd_kernel(const void* __restrict__ logits, long long ld,
+                                                     const int32_t* __restrict__ labels, int B, int C,
+                                                     const float* __restrict__ dloss, void* __restrict__ dz,
+                                                     long long ldd, int fmt) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= B) return;
+  const long long base = (long long)row * ld;
+  float m = -INFINITY;
+  for (int c = lane; c < C; c += 32) m = fmaxf(m, ld_h(logits, base + c, fmt));
+  m = warp_max(m);
+  float s = 0.f;
+  for (int c = lane; c < C; c += 32) s += expf(ld_h(logits, base + c, fmt) - m);
+  const float inv = 1.f / warp_sum(s);
+  const float k = *dloss / (float)B;
+  const int y = labels[row];
+  for (int c = lane; c < ldd; c += 32) {
+    float o = 0.f;
+    if (c < C) o = (expf(ld_h(logits, base + c, fmt) - m) * inv - (c == y ? 1.f : 0.f)) * k;
+    st_h(dz, (long long)row * ldd + c, o, fmt);
+  }
+}
+
+// ===========================================================================
+// patchify: img [B, H, W, C] -> patches [B*(H/p)*(W/p), p*p*C], vector order
+// (py, px, c) — reshape [B,h,p,w,p,C] / transpose (0,1,3,2,4,5)
+// ===========================================================================
+__global__ void patchify_kernel(const uint16_t* __restrict__ img, uint16_t* __restrict__ out, int B, int H, int W,
+                                int C, int p) {
+  const int nh = H / p, nw = W / p, K = p * p * C;
+  const long long n = (long long)B * nh * nw * K;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / K;
+    const int k = (int)(i - r * K);
+    const int b = (int)(r / (nh * nw));
+    const int t = (int)(r - (long long)b * nh * nw);
+    const int ih = t / nw, iw = t - ih * nw;
+    const int py = k / (p * C), rem = k - py * p * C, px = rem / C, c = rem - px * C;
+    out[i] = img[(((long long)b * H + ih * p + py) * W + iw * p + px) * C + c];
+  }
+}
+
+// out[b][r][c] = src[b][r][c] (strided row copy), optional add of a
+// broadcast row (add[c]) and scaling
+__global__ void copy_rows_kernel(const uint16_t* __restrict__ src, long long ld_src, long long sb_src,
+                                 uint16_t* __restrict__ dst, long long ld_dst, long long sb_dst, int rows, int batches,
+                                 int cols) {
+  const long long n = (long long)batches * rows * cols;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long bc = i / cols;
+    const int c = (int)(i - bc * cols);
+    const int b = (int)(bc / rows), r = (int)(bc - (long long)b * rows);
+    dst[b * sb_dst + r * ld_dst + c] = src[b * sb_src + r * ld_src + c];
+  }
+}
+
+// dst[b*sb + c] = round(a[c] + b[c])  (cls token + its position embedding)
+__global__ void rows_add_kernel(const void* __restrict__ a, const void* __restrict__ b2, void* __restrict__ dst,
+                                long long sb, int B, int D, int fmt) {
+  const long long n = (long long)B * D;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / D;
+    const int c = (int)(i - b * D);
+    st_h(dst, b * sb + c, ld_h(a, c, fmt) + ld_h(b2, c, fmt), fmt);
+  }
+}
+
+// dst[b][r][c] = alpha * src[b][c]   (mean-pool backward broadcast)
+__global__ void bcast_rows_kernel(const void* __restrict__ src, long long ld_src, void* __restrict__ dst,
+                                  long long ld_dst, long long sb_dst, int rows, int B, int D, float alpha, int fmt) {
+  const long long n = (long long)B * rows * D;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long bc = i / D;
+    const int c = (int)(i - bc * D);
+    const int b = (int)(bc / rows), r = (int)(bc - (long long)b * rows);
+    st_h(dst, b * sb_dst + r * ld_dst + c, alpha * ld_h(src, (long long)b * ld_src + c, fmt), fmt);
+  }
+}
+
+static int fmt_of(int dtype) { return dtype == MPX_BF16 ? 1 : 0; }
+static bool half_dtype(int dt) { return dt == MPX_F16 || dt == MPX_BF16; }
+static int ew_grid(long long n) {
+  long long g = (n + 255) / 256;
+  const long long cap = (long long)current_num_sms() * 8;
+  return (int)std::max<long long>(1, std::min(g, cap));
+}
+
+}  // namespace mpx
+
+using namespace mpx;
+
+extern "C" {
+
+int mpx_layernorm_fwd(int dtype, const void* x, int64_t ldx, const void* gain, const void* bias, void* y,
+                      int64_t ldy, float* mean, float* rstd, int rows, int D, float eps, void* stream) {
+  if (!half_dtype(dtype)) return fail(MPX_EINVAL, "layernorm: f16/bf16 only");
+  if (rows <= 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = (rows + 7) / 8;
+  const bool vec = (ldx % 8 == 0) && (ldy % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+                                                         reinterpret_cast<uintptr_t>(gain) |
+                                                         reinterpret_cast<uintptr_t>(bias)) % 16 == 0);
+  const int f = fmt_of(dtype);
+  if (vec && D == 768)
+    ln_fwd_kernel<3><<<grid, 256, 0, st>>>(x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f);
+  else if (vec && D == 1024)
+    ln_fwd_kernel<4><<<grid, 256, 0, st>>>(x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f);
+  else if (vec && D == 512)
+    ln_fwd_kernel<2><<<grid, 256, 0, st>>>(x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f);
+  else
+    ln_fwd_kernel<0><<<grid, 256, 0, st>>>(x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f);
+  MPX_LAUNCH_CHECK("ln_fwd_kernel");
+  return 0;
+}
+
+int mpx_layernorm_bwd_blocks(int rows) {
+  return std::max(1, std::min((rows + 7) / 8, current_num_sms() * 2));
+}
+
+int mpx_layernorm_bwd(int dtype, const void* x, int64_t ldx, const void* gain, const float* mean, const float* rstd,
+                      const void* dy, int64_t lddy, const void* dres, int64_t ldres, void* dx, int64_t lddx,
+                      void* dgain, void* dbias, float* workspace, int rows, int D, void* stream) {
+  if (!half_dtype(dtype)) return fail(MPX_EINVAL, "layernorm_bwd: f16/bf16 only");
+  if (rows <= 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nb = mpx_layernorm_bwd_blocks(rows);
+  const size_t sh = (size_t)8 * 2 * D * sizeof(float);
+  if (sh > 48 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      MPX_CUDA_CHECK(cudaFuncSetAttribute(ln_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+  }
+  const int f = fmt_of(dtype);
+  ln_bwd_kernel<<<nb, 256, sh, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace, rows, D, f);
+  MPX_LAUNCH_CHECK("ln_bwd_kernel");
+  partials_reduce_kernel<<<(D + 255) / 256, 256, 0, st>>>(workspace, nb, D, dgain, dbias, 1.f, f);
+  MPX_LAUNCH_CHECK("partials_reduce_kernel");
+  return 0;
+}
+
+int mpx_colsum(int dtype, const void* x, int64_t ldx, int64_t sbx, int rows, int cols, int batches, float* workspace,
+               int64_t workspace_floats, void* out, int64_t ld_out, int out_dtype, float alpha, void* stream) {
+  if (!half_dtype(dtype)) return fail(MPX_EINVAL, "colsum: f16/bf16 input only");
+  if (rows <= 0 || cols <= 0 || batches <= 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int cblocks = (cols + 255) / 256;
+  const long long target = (long long)current_num_sms() * 4;
+  int splits = (int)std::max<long long>(1, target / ((long long)cblocks * batches));
+  splits = std::min(splits, std::max(1, rows / 64));
+  while ((long long)splits * cols * batches > workspace_floats && splits > 1) splits /= 2;
+  if ((long long)splits * cols * batches > workspace_floats) return fail(MPX_EINVAL, "colsum: workspace too small");
+  const int rps = (rows + splits - 1) / splits;
+  dim3 grid(cblocks, splits, batches);
+  colsum_partial_kernel<<<grid, 256, 0, st>>>(x, ldx, sbx, rows, cols, rps, workspace, fmt_of(dtype));
+  MPX_LAUNCH_CHECK("colsum_partial_kernel");
+  colsum_final_kernel<<<ew_grid((long long)cols * batches), 256, 0, st>>>(workspace, splits, cols, batches, out, ld_out,
+                                                                         out_dtype, alpha);
+  MPX_LAUNCH_CHECK("colsum_final_kernel");
+  return 0;
+}
+
+int mpx_softmax_fwd(int dtype, const void* S, void* P, int64_t rows, int L, int64_t ld, void* stream) {
+  if (!half_dtype(dtype) || ld < L) return fail(MPX_EINVAL, "softmax_fwd: bad args");
+  if (rows <= 0) return 0;
+  softmax_fwd_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(S, P, rows, L, ld,
+                                                                                                 fmt_of(dtype));
+  MPX_LAUNCH_CHECK("softmax_fwd_kernel");
+  return 0;
+}
+
+int mpx_softmax_bwd(int dtype, const void* S, const void* dP, void* dS, int64_t rows, int L, int64_t ld, void* stream) {
+  if (!half_dtype(dtype) || ld < L) return fail(MPX_EINVAL, "softmax_bwd: bad args");
+  if (rows <= 0) return 0;
+  softmax_bwd_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(S, dP, dS, rows, L, ld,
+                                                                                                 fmt_of(dtype));
+  MPX_LAUNCH_CHECK("softmax_bwd_kernel");
+  return 0;
+}
+
+int mpx_cross_entropy_fwd(int dtype, const void* logits, int64_t ld, const int32_t* labels, int B, int C,
+                          float* nll_ws, float* loss, void* stream) {
+  if (!half_dtype(dtype)) return fail(MPX_EINVAL, "cross_entropy: f16/bf16 logits only");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ce_fwd_kernel<<<(B + 7) / 8, 256, 0, st>>>(logits, ld, labels, B, C, nll_ws, fmt_of(dtype));
+  MPX_LAUNCH_CHECK("ce_fwd_kernel");
+  ce_mean_kernel<<<1, 1024, 0, st>>>(nll_ws, B, loss);
+  MPX_LAUNCH_CHECK("ce_mean_kernel");
+  return 0;
+}
+
+int mpx_cross_entropy_bwd(int dtype, const void* logits, int64_t ld, const int32_t* labels, int B, int C,
+                          const float* d_dloss, void* dlogits, int64_t ld_d, void* stream) {
+  if (!half_dtype(dtype)) return fail(MPX_EINVAL, "cross_entropy_bwd: f16/bf16 only");
+  ce_bwd_kernel<<<(B + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(logits, ld, labels, B, C, d_dloss, dlogits,
+                                                                             ld_d, fmt_of(dtype));
+  MPX_LAUNCH_CHECK("ce_bwd_kernel");
+  return 0;
+}
+
+int mpx_patchify(int dtype, const void* img, void* patches, int B, int H, int W, int C, int P, void* stream) {
+  if (!half_dtype(dtype) || P <= 0 || H % P || W % P) return fail(MPX_EINVAL, "patchify: bad args");
+  const long long n = (long long)B * H * W * C;
+  patchify_kernel<<<ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint16_t*>(img), static_cast<uint16_t*>(patches), B, H, W, C, P);
+  MPX_LAUNCH_CHECK("patchify_kernel");
+  return 0;
+}
+
+int mpx_copy_rows(int dtype, const void* src, int64_t ld_src, int64_t sb_src, void* dst, int64_t ld_dst,
+                  int64_t sb_dst, int rows, int batches, int cols, void* stream) {
+  if (!half_dtype(dtype)) return fail(MPX_EINVAL, "copy_rows: f16/bf16 only");
+  const long long n = (long long)rows * batches * cols;
+  if (n <= 0) return 0;
+  copy_rows_kernel<<<ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint16_t*>(src), ld_src, sb_src, static_cast<uint16_t*>(dst), ld_dst, sb_dst, rows, batches,
+      cols);
+  MPX_LAUNCH_CHECK("copy_rows_kernel");
+  return 0;
+}
+
+int mpx_rows_add(int dtype, const void* a, const void* b, void* dst, int64_t sb, int B, int D, void* stream) {
+  if (!half_dtype(dtype)) return fail(MPX_EINVAL, "rows_add: f16/bf16 only");
+  rows_add_kernel<<<ew_grid((long long)B * D), 256, 0, static_cast<cudaStream_t>(stream)>>>(a, b, dst, sb, B, D,
+                                                                                            fmt_of(dtype));
+  MPX_LAUNCH_CHECK("rows_add_kernel");
+  return 0;
+}
+
+int mpx_bcast_rows(int dtype, const void* src, int64_t ld_src, void* dst, int64_t ld_dst, int64_t sb_dst, int rows,
+                   int B, int D, float alpha, void* stream) {
+  if (!half_dtype(dtype)) return fail(MPX_EINVAL, "bcast_rows: f16/bf16 only");
+  bcast_rows_kernel<<<ew_grid((long long)B * rows * D), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      src, ld_src, dst, ld_dst, sb_dst, rows, B, D, alpha, fmt_of(dtype));
+  MPX_LAUNCH_CHECK("bcast_rows_kernel");
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,358 @@
+"""ViT forward/backward on the sm_100a kernels (configs 1, 3-5 of BASELINE.json).
+
+The reference has no ViT; this is the model its primitives
+compose, with MPX's precision rules:
+
+    patchify -> x @ W_patch + b + pos (+cls)                       half
+    per block:  LN1 (f32 island) -> qkv -> S = QK^T/sqrt(hd) -> softmax (f32
+                island) -> P V -> proj + residual -> LN2 (island) -> fc1+GELU
+                -> fc2 + residual                                  half, f32 accumulate
+    head:       LN_f (island) on the cls token (or mean-pool island) -> head
+                -> cross-entropy (f32 island, bench.py:185-198)
+
+Every contraction is the tcgen05 GEMM (K5) with the elementwise work fused
+into its epilogue (bias, GELU saving the pre-activation, GELU' in the fc2
+dgrad, residual adds); attention contractions run straight out of the
+[B, N, 3, H, hd] qkv layout through 4-D TMA maps.  Activations are kept for
+the backward in preallocated buffers sized for (config, batch); gradients
+are written into caller-provided tensors (the flat half grad arena of
+step.FusedMPStep), so a training step allocates nothing.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import _native as _nat
+from . import vit_kernels as VK
+from .dtypes import F16, as_dtype
+from . import kernels as K
+from .kernels import stream_handle
+from .vit_config import ViTConfig
+
+LN_EPS = 1e-5  # tensors.py:449 _LAYERNORM_EPS
+
+
+def _r8(n: int) -> int:
+    return -(-n // 8) * 8
+
+
+class ViTEngine:
+    """Buffers + kernel sequence for one (config, batch, half dtype)."""
+
+    def __init__(self, cfg: ViTConfig, batch: int, half=F16, device=None):
+        self.cfg = cfg
+        self.B = batch
+        self.half = as_dtype(half)
+        self.dt = self.half.torch
+        self.code = self.half.code
+        self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        c = cfg
+        B, S, D, H = batch, c.seq, c.dim, c.heads
+        self.S, self.D, self.H, self.hd = S, D, H, D // H
+        self.np = c.n_patches
+        self.Kp = c.patch * c.patch * c.chans
+        self.ldS = _r8(S)
+        self.ldl = _r8(c.classes)
+        self.M = B * S
+        e = lambda *shape, dt=self.dt: torch.empty(*shape, dtype=dt, device=self.dev)  # noqa: E731
+        M = self.M
+        self.patches = e(B * self.np, self.Kp)
+        self.x = [e(M, D) for _ in range(c.depth + 1)]  # residual stream at each block input (+ final)
+        self.a = [e(M, D) for _ in range(c.depth)]  # LN1 out
+        self.qkv = [e(M, 3 * D) for _ in range(c.depth)]
+        self.Sm = [e(B * H * S, self.ldS) for _ in range(c.depth)]  # scaled scores
+        self.P = [e(B * H * S, self.ldS) for _ in range(c.depth)]
+        self.O = [e(M, D) for _ in range(c.depth)]
+        self.xm = [e(M, D) for _ in range(c.depth)]  # after attention residual
+        self.bn = [e(M, D) for _ in range(c.depth)]  # LN2 out
+        self.pre = [e(M, c.mlp) for _ in range(c.depth)]  # fc1 pre-activation
+        self.h = [e(M, c.mlp) for _ in range(c.depth)]  # GELU out
+        f = lambda n: torch.empty(n, dtype=torch.float32, device=self.dev)  # noqa: E731
+        self.mu1 = [f(M) for _ in range(c.depth)]
+        self.rs1 = [f(M) for _ in range(c.depth)]
+        self.mu2 = [f(M) for _ in range(c.depth)]
+        self.rs2 = [f(M) for _ in range(c.depth)]
+        nf = B if c.pool == "cls" else M
+        self.fin = e(nf, D)  # LN_f out (cls rows, or all rows for mean-pool)
+        self.muf, self.rsf = f(nf), f(nf)
+        self.pooled = e(B, D)
+        self.logits = e(B, self.ldl)
+        self.nll = f(B)
+        self.loss = torch.zeros((), dtype=torch.float32, device=self.dev)
+        # backward scratch (reused across blocks)
+        self.dX = e(M, D)
+        self.dXm = e(M, D)
+        self.dO = e(M, D)
+        self.dqkv = e(M, 3 * D)
+        self.dP = e(B * H * S, self.ldS)
+        self.dpre = e(M, c.mlp)
+        self.dA = e(M, D)
+        self.dlogits = e(B, self.ldl)
+        self.dfin = e(nf, D)
+        self.dpool = e(B, D)
+        self._dloss32 = torch.zeros((), dtype=torch.float32, device=self.dev)
+        self._one32 = torch.ones((), dtype=torch.float32, device=self.dev)
+        self.dpatch = e(B * self.np, D)
+        self.hw_pad = e(D, self.ldl) if c.classes % 8 else None  # head weight with 16-byte rows
+        if self.hw_pad is not None:
+            self.hw_pad.zero_()
+        self.dhw_pad = e(D, self.ldl) if c.classes % 8 else None
+        self.ws_floats = max(8 * 1024 * 1024, 2 * (D * 3 * D), 3 * c.mlp * D)
+        self.ws = f(self.ws_floats)
+        self.lib = _nat.load()
+
+    # ------------------------------------------------------------------
+    def _st(self):
+        return stream_handle(self.dev)
+
+    def _ck(self, rc, what):
+        _nat.check(rc, what)
+
+    def _ln_fwd(self, x, ldx, g, b, y, ldy, mu, rs, rows):
+        self._ck(self.lib.mpx_layernorm_fwd(self.code, x.data_ptr(), ldx, g.data_ptr(), b.data_ptr(), y.data_ptr(),
+                                            ldy, mu.data_ptr(), rs.data_ptr(), rows, self.D, LN_EPS, self._st()),
+                 "layernorm_fwd")
+
+    def _ln_bwd(self, x, ldx, g, mu, rs, dy, lddy, dres, dx, lddx, dg, db, rows):
+        self._ck(self.lib.mpx_layernorm_bwd(self.code, x.data_ptr(), ldx, g.data_ptr(), mu.data_ptr(), rs.data_ptr(),
+                                            dy.data_ptr(), lddy, dres.data_ptr() if dres is not None else None,
+                                            self.D if dres is not None else 0, dx.data_ptr(), lddx, dg.data_ptr(),
+                                            db.data_ptr(), self.ws.data_ptr(), rows, self.D, self._st()),
+                 "layernorm_bwd")
+
+    def _colsum(self, x, ldx, rows, cols, out, sbx=0, batches=1, ld_out=0, alpha=1.0, out_dtype=None):
+        self._ck(self.lib.mpx_colsum(self.code, x.data_ptr(), ldx, sbx, rows, cols, batches, self.ws.data_ptr(),
+                                     self.ws_floats, out.data_ptr(), ld_out or cols,
+                                     out_dtype if out_dtype is not None else self.code, alpha, self._st()), "colsum")
+
+    # ------------------------------------------------------------------
+    def forward(self, p: dict, images: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
+        """p: path -> half tensor; images [B, H, W, C] half; labels [B] int32.
+        Returns the mean cross-entropy (f32 0-d device tensor)."""
+        c, B, S, D, H, hd = self.cfg, self.B, self.S, self.D, self.H, self.hd
+        M, st, lib = self.M, self._st(), self.lib
+        cls = c.pool == "cls"
+        self._ck(lib.mpx_patchify(self.code, images.data_ptr(), self.patches.data_ptr(), B, c.img, c.img, c.chans,
+                                  c.patch, st), "patchify")
+        x0 = self.x[0]
+        # patch embedding + bias + position embedding, written into the token rows
+        VK.gemm(self.patches, p["patch.w"], M=self.np, N=D, K=self.Kp, lda=self.Kp, ldb=D, b_mn=True,
+                nb=(1, B), a_sb=(0, self.np * self.Kp), out=x0[1:] if cls else x0, ldc=D, c_sb=(0, S * D),
+                bias=p["patch.b"], residual=p["pos"][1:] if cls else p["pos"], ldr=D, r_sb=(0, 0))
+        if cls:
+            self._ck(lib.mpx_rows_add(self.code, p["cls"].data_ptr(), p["pos"].data_ptr(), x0.data_ptr(), S * D, B, D,
+                                      st), "rows_add")
+        scale = 1.0 / math.sqrt(hd)
+        for i in range(c.depth):
+            q = f"blocks.{i}."
+            x, a, qkv = self.x[i], self.a[i], self.qkv[i]
+            self._ln_fwd(x, D, p[q + "ln1.g"], p[q + "ln1.b"], a, D, self.mu1[i], self.rs1[i], M)
+            VK.linear_fwd(a, p[q + "qkv.w"], bias=p[q + "qkv.b"], out=qkv)
+            Sm, P_, O = self.Sm[i], self.P[i], self.O[i]
+            VK.gemm(qkv, qkv[:, D:], M=S, N=S, K=hd, lda=3 * D, ldb=3 * D, nb=(H, B), a_sb=(hd, S * 3 * D),
+                    b_sb=(hd, S * 3 * D), out=Sm, ldc=self.ldS, c_sb=(S * self.ldS, H * S * self.ldS), alpha=scale)
+            self._ck(lib.mpx_softmax_fwd(self.code, Sm.data_ptr(), P_.data_ptr(), B * H * S, S, self.ldS, st),
+                     "softmax_fwd")
+            VK.gemm(P_, qkv[:, 2 * D:], M=S, N=hd, K=S, lda=self.ldS, ldb=3 * D, b_mn=True, nb=(H, B),
+                    a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * 3 * D), out=O, ldc=D, c_sb=(hd, S * D))
+            xm = self.xm[i]
+            VK.linear_fwd(O, p[q + "proj.w"], bias=p[q + "proj.b"], residual=x, out=xm)
+            bn = self.bn[i]
+            self._ln_fwd(xm, D, p[q + "ln2.g"], p[q + "ln2.b"], bn, D, self.mu2[i], self.rs2[i], M)
+            VK.linear_fwd(bn, p[q + "fc1.w"], bias=p[q + "fc1.b"], act=VK.ACT_GELU, aux=self.pre[i], out=self.h[i])
+            VK.linear_fwd(self.h[i], p[q + "fc2.w"], bias=p[q + "fc2.b"], residual=xm, out=self.x[i + 1])
+        xl = self.x[c.depth]
+        if cls:
+            self._ln_fwd(xl, S * D, p["ln_f.g"], p["ln_f.b"], self.fin, D, self.muf, self.rsf, B)
+            feat = self.fin
+        else:
+            self._ln_fwd(xl, D, p["ln_f.g"], p["ln_f.b"], self.fin, D, self.muf, self.rsf, M)
+            self._colsum(self.fin, D, S, D, self.pooled, sbx=S * D, batches=B, ld_out=D, alpha=1.0 / S)
+            feat = self.pooled
+        hw = p["head.w"]
+        if self.hw_pad is not None:
+            self._ck(lib.mpx_copy_rows(self.code, hw.data_ptr(), c.classes, 0, self.hw_pad.data_ptr(), self.ldl, 0, D,
+                                       1, c.classes, st), "copy_rows")
+            hw = self.hw_pad
+        VK.gemm(feat, hw, M=B, N=c.classes, K=D, lda=D, ldb=self.ldl if self.hw_pad is not None else c.classes,
+                b_mn=True, bias=p["head.b"], out=self.logits, ldc=self.ldl)
+        self._ck(lib.mpx_cross_entropy_fwd(self.code, self.logits.data_ptr(), self.ldl, labels.data_ptr(), B,
+                                           c.classes, self.nll.data_ptr(), self.loss.data_ptr(), st), "ce_fwd")
+        self._labels = labels
+        self._images = images
+        return self.loss
+
+    # ------------------------------------------------------------------
+    def backward(self, p: dict, g: dict, dloss_f32: torch.Tensor | None = None, dloss_f64: torch.Tensor | None = None):
+        """Gradients of (dloss * loss) into g (path -> half tensors).  The loss
+        cotangent is read on the device: an f32 0-d tensor (autograd) or the
+        fp64 loss scale of a DynamicLossScaling state (fused training step)."""
+        c, B, S, D, H, hd = self.cfg, self.B, self.S, self.D, self.H, self.hd
+        M, st, lib = self.M, self._st(), self.lib
+        cls = c.pool == "cls"
+        if dloss_f32 is None:
+            if dloss_f64 is None:
+                raise ValueError("backward needs the loss cotangent")
+            # f32(scale) = 1.0f * f32(*d_scale): K1 with a device multiplier (the
+            # weak-scalar rounding of T.mul(loss, s), autodiff.py:131-138)
+            dloss_f32 = self._dloss32
+            K.cast_into([self._one32], [dloss_f32], d_scale=dloss_f64)
+        self._ck(lib.mpx_cross_entropy_bwd(self.code, self.logits.data_ptr(), self.ldl, self._labels.data_ptr(), B,
+                                           c.classes, dloss_f32.data_ptr(), self.dlogits.data_ptr(), self.ldl, st),
+                 "ce_bwd")
+        feat = self.fin if cls else self.pooled
+        # head: logits = feat @ Wh + bh
+        if self.dhw_pad is not None:
+            VK.gemm(feat, self.dlogits, M=D, N=c.classes, K=B, lda=D, ldb=self.ldl, a_mn=True, b_mn=True,
+                    out=self.dhw_pad, ldc=self.ldl)
+            self._ck(lib.mpx_copy_rows(self.code, self.dhw_pad.data_ptr(), self.ldl, 0, g["head.w"].data_ptr(),
+                                       c.classes, 0, D, 1, c.classes, st), "copy_rows")
+            hw, ldhw = self.hw_pad, self.ldl
+        else:
+            VK.linear_wgrad(feat, self.dlogits, out=g["head.w"])
+            hw, ldhw = p["head.w"], c.classes
+        self._colsum(self.dlogits, self.ldl, B, c.classes, g["head.b"])
+        dfeat = self.dfin if cls else self.dpool
+        VK.gemm(self.dlogits, hw, M=B, N=D, K=c.classes, lda=self.ldl, ldb=ldhw, out=dfeat, ldc=D)
+        dX = self.dX
+        xl = self.x[c.depth]
+        if cls:
+            dX.zero_()
+            self._ln_bwd(xl, S * D, p["ln_f.g"], self.muf, self.rsf, dfeat, D, None, dX, S * D, g["ln_f.g"],
+                         g["ln_f.b"], B)
+        else:
+            self._ck(lib.mpx_bcast_rows(self.code, dfeat.data_ptr(), D, self.dfin.data_ptr(), D, S * D, S, B, D,
+                                        1.0 / S, st), "bcast_rows")
+            self._ln_bwd(xl, D, p["ln_f.g"], self.muf, self.rsf, self.dfin, D, None, dX, D, g["ln_f.g"], g["ln_f.b"],
+                         M)
+        scale = 1.0 / math.sqrt(hd)
+        for i in reversed(range(c.depth)):
+            q = f"blocks.{i}."
+            # fc2: x_{i+1} = h @ W2 + b2 + xm
+            VK.linear_wgrad(self.h[i], dX, out=g[q + "fc2.w"])
+            self._colsum(dX, D, M, D, g[q + "fc2.b"])
+            VK.linear_dgrad(dX, p[q + "fc2.w"], aux=self.pre[i], out=self.dpre)  # dpre = (dX W2^T) * gelu'(pre)
+            # fc1: pre = bn @ W1 + b1
+            VK.linear_wgrad(self.bn[i], self.dpre, out=g[q + "fc1.w"])
+            self._colsum(self.dpre, c.mlp, M, c.mlp, g[q + "fc1.b"])
+            VK.linear_dgrad(self.dpre, p[q + "fc1.w"], out=self.dA)
+            # LN2 (+ residual): dxm = LN2'(dA) + dX
+            self._ln_bwd(self.xm[i], D, p[q + "ln2.g"], self.mu2[i], self.rs2[i], self.dA, D, dX, self.dXm, D,
+                         g[q + "ln2.g"], g[q + "ln2.b"], M)
+            dXm = self.dXm
+            # proj: xm = O @ Wp + bp + x
+            VK.linear_wgrad(self.O[i], dXm, out=g[q + "proj.w"])
+            self._colsum(dXm, D, M, D, g[q + "proj.b"])
+            VK.linear_dgrad(dXm, p[q + "proj.w"], out=self.dO)
+            # attention
+            qkv, dqkv, P_, Sm = self.qkv[i], self.dqkv, self.P[i], self.Sm[i]
+            # dV[b,h] = P^T dO
+            VK.gemm(P_, self.dO, M=S, N=hd, K=S, lda=self.ldS, ldb=D, a_mn=True, b_mn=True, nb=(H, B),
+                    a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * D), out=dqkv[:, 2 * D:], ldc=3 * D,
+                    c_sb=(hd, S * 3 * D))
+            # dP = dO V^T
+            VK.gemm(self.dO, qkv[:, 2 * D:], M=S, N=S, K=hd, lda=D, ldb=3 * D, nb=(H, B), a_sb=(hd, S * D),
+                    b_sb=(hd, S * 3 * D), out=self.dP, ldc=self.ldS, c_sb=(S * self.ldS, H * S * self.ldS))
+            # dS = softmax'(dP) (in place), then the 1/sqrt(hd) of the score scaling folds into alpha
+            self._ck(lib.mpx_softmax_bwd(self.code, Sm.data_ptr(), self.dP.data_ptr(), self.dP.data_ptr(), B * H * S,
+                                         S, self.ldS, st), "softmax_bwd")
+            dS = self.dP
+            # dQ = dS K * scale
+            VK.gemm(dS, qkv[:, D:], M=S, N=hd, K=S, lda=self.ldS, ldb=3 * D, b_mn=True, nb=(H, B),
+                    a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * 3 * D), out=dqkv, ldc=3 * D,
+                    c_sb=(hd, S * 3 * D), alpha=scale)
+            # dK = dS^T Q * scale
+            VK.gemm(dS, qkv, M=S, N=hd, K=S, lda=self.ldS, ldb=3 * D, a_mn=True, b_mn=True, nb=(H, B),
+                    a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * 3 * D), out=dqkv[:, D:], ldc=3 * D,
+                    c_sb=(hd, S * 3 * D), alpha=scale)
+            # qkv = a @ Wqkv + bqkv
+            VK.linear_wgrad(self.a[i], dqkv, out=g[q + "qkv.w"])
+            self._colsum(dqkv, 3 * D, M, 3 * D, g[q + "qkv.b"])
+            VK.linear_dgrad(dqkv, p[q + "qkv.w"], out=self.dA)
+            # LN1 (+ residual): dX = LN1'(dA) + dXm
+            self._ln_bwd(self.x[i], D, p[q + "ln1.g"], self.mu1[i], self.rs1[i], self.dA, D, dXm, dX, D,
+                         g[q + "ln1.g"], g[q + "ln1.b"], M)
+        # embedding: tokens = patches @ Wp + bp + pos (+ cls row)
+        self._colsum(dX, S * D, B, S * D, g["pos"])  # sum over the batch
+        if cls:
+            self._colsum(dX, S * D, B, D, g["cls"])
+            self._ck(lib.mpx_copy_rows(self.code, dX[1:].data_ptr(), D, S * D, self.dpatch.data_ptr(), D,
+                                       self.np * D, self.np, B, D, st), "copy_rows")
+            dpatch = self.dpatch
+        else:
+            dpatch = dX
+        self._colsum(dpatch, D, B * self.np, D, g["patch.b"])
+        VK.linear_wgrad(self.patches, dpatch, out=g["patch.w"])
+
+
+# ---------------------------------------------------------------------------
+# drop-in: a loss function usable with filter_value_and_grad
+# ---------------------------------------------------------------------------
+_ENGINES: dict = {}
+
+
+def engine_for(cfg: ViTConfig, batch: int, half, device) -> ViTEngine:
+    key = (cfg, batch, as_dtype(half), str(device))
+    eng = _ENGINES.get(key)
+    if eng is None:
+        eng = ViTEngine(cfg, batch, half, device)
+        _ENGINES[key] = eng
+    return eng
+
+
+class _ViTLoss(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, engine, paths, images, labels, *leaves):
+        p = dict(zip(paths, leaves))
+        loss = engine.forward(p, images, labels).clone()
+        ctx.engine, ctx.paths = engine, paths
+        ctx.save_for_backward(*leaves)
+        return loss
+
+    @staticmethod
+    def backward(ctx, dloss):
+        leaves = ctx.saved_tensors
+        p = dict(zip(ctx.paths, leaves))
+        g = {k: torch.empty_like(v) for k, v in p.items()}
+        ctx.engine.backward(p, g, dloss_f32=dloss.float().contiguous())
+        return (None, None, None, None) + tuple(g[k] for k in ctx.paths)
+
+
+def vit_loss(cfg: ViTConfig):
+    """f(params, batch) -> mean cross-entropy (f32), differentiable w.r.t. the
+    float leaves of `params` (path -> tensor, the shapes of cfg.param_shapes())
+    — the function filter_value_and_grad transforms.  batch = {"x": images
+    [B, H, W, C], "y": int32 labels [B]}; params and images arrive already
+    cast to the half dtype by the transform (precision.py:209-210)."""
+    paths = [n for n, _ in cfg.param_shapes()]
+
+    def f(params, batch):
+        x, y = batch["x"], batch["y"]
+        leaves = [params[k] for k in paths]
+        half = leaves[0].dtype
+        if x.dtype != half:
+            raise TypeError("images must be cast to the parameters' half dtype")
+        eng = engine_for(cfg, x.shape[0], half, x.device)
+        return _ViTLoss.apply(eng, paths, x.contiguous(), y.to(torch.int32).contiguous(), *leaves)
+
+    return f
+
+
+def init_params(cfg: ViTConfig, device, seed: int = 0, std: float = 0.02) -> dict:
+    """Synthetic f32 init (random weights of the architecture; no checkpoints
+    offline): N(0, std^2) matrices, ones/zeros LayerNorms, zero biases."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    out = {}
+    for name, shape in cfg.param_shapes():
+        leaf = name.rsplit(".", 1)[-1]
+        if leaf == "g":
+            out[name] = torch.ones(shape, device=device)
+        elif leaf == "b":
+            out[name] = torch.zeros(shape, device=device)
+        else:
+            out[name] = torch.randn(shape, generator=g, device=device) * std
+    return out

@@ -1,0 +1,110 @@
+"""ViT forward/backward on the sm_100a kernels vs a plain fp32 torch
+reference of the same model on the same half-rounded parameters and inputs.
+
+Tolerance: the reference's own mixed-vs-full bar (test_precision.py:345-376):
+per-leaf max |g_ours - g_ref| <= 5e-2 * max |g_ref| (leaves with max |g_ref| >
+1e-4 after unscaling); loss within 1e-2 relative."""
+import math
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+import paper_2507_03312_b200 as mpx
+from paper_2507_03312_b200.vit import ViTEngine, init_params, vit_loss
+from paper_2507_03312_b200.vit_config import VIT_TINY, ViTConfig
+
+pytestmark = pytest.mark.gpu
+
+
+def ref_loss(cfg: ViTConfig, p: dict, images: torch.Tensor, labels: torch.Tensor):
+    """fp32 torch restatement of vit.py's model (same op order)."""
+    B = images.shape[0]
+    P, C = cfg.patch, cfg.chans
+    nh = cfg.img // P
+    x = images.reshape(B, nh, P, nh, P, C).permute(0, 1, 3, 2, 4, 5).reshape(B * nh * nh, P * P * C)
+    D, H = cfg.dim, cfg.heads
+    hd = D // H
+    z = (x @ p["patch.w"] + p["patch.b"]).reshape(B, nh * nh, D)
+    if cfg.pool == "cls":
+        z = torch.cat([p["cls"].expand(B, 1, D), z], 1)
+    z = z + p["pos"]
+    S = z.shape[1]
+    for i in range(cfg.depth):
+        q = f"blocks.{i}."
+        a = F.layer_norm(z, (D,), p[q + "ln1.g"], p[q + "ln1.b"], 1e-5)
+        qkv = (a @ p[q + "qkv.w"] + p[q + "qkv.b"]).reshape(B, S, 3, H, hd)
+        Q, K, V = qkv[:, :, 0].transpose(1, 2), qkv[:, :, 1].transpose(1, 2), qkv[:, :, 2].transpose(1, 2)
+        att = torch.softmax((Q @ K.transpose(-1, -2)) / math.sqrt(hd), -1)
+        o = (att @ V).transpose(1, 2).reshape(B, S, D)
+        z = z + o @ p[q + "proj.w"] + p[q + "proj.b"]
+        b = F.layer_norm(z, (D,), p[q + "ln2.g"], p[q + "ln2.b"], 1e-5)
+        h = F.gelu(b @ p[q + "fc1.w"] + p[q + "fc1.b"], approximate="tanh")
+        z = z + h @ p[q + "fc2.w"] + p[q + "fc2.b"]
+    if cfg.pool == "cls":
+        feat = F.layer_norm(z[:, 0], (D,), p["ln_f.g"], p["ln_f.b"], 1e-5)
+    else:
+        feat = F.layer_norm(z, (D,), p["ln_f.g"], p["ln_f.b"], 1e-5).mean(1)
+    logits = feat @ p["head.w"] + p["head.b"]
+    return F.cross_entropy(logits, labels.long())
+
+
+CFGS = {
+    "tiny-mean": VIT_TINY,
+    "small-cls": ViTConfig(img=32, patch=4, dim=128, depth=2, heads=2, mlp=256, classes=16, pool="cls"),
+    "vitb-shape": ViTConfig(img=64, patch=16, dim=768, depth=1, heads=12, mlp=3072, classes=1000, pool="cls"),
+}
+
+
+@pytest.mark.parametrize("name", list(CFGS))
+@pytest.mark.parametrize("half", [torch.float16, torch.bfloat16])
+def test_engine_matches_fp32_reference(cuda, name, half):
+    cfg = CFGS[name]
+    B = 4
+    p32 = init_params(cfg, cuda, seed=3, std=0.05)
+    for k in p32:  # non-trivial LayerNorm parameters
+        if k.endswith(".g") or k.endswith(".b"):
+            p32[k] = p32[k] + 0.1 * torch.randn_like(p32[k])
+    ph = {k: v.to(half) for k, v in p32.items()}
+    g = torch.Generator(device=cuda).manual_seed(1)
+    images = torch.randn(B, cfg.img, cfg.img, cfg.chans, device=cuda, generator=g).to(half)
+    labels = torch.randint(0, cfg.classes, (B,), device=cuda, generator=g).to(torch.int32)
+    eng = ViTEngine(cfg, B, mpx.as_dtype(half), cuda)
+    loss = eng.forward(ph, images, labels).item()
+    scale = 1024.0
+    grads = {k: torch.empty_like(v) for k, v in ph.items()}
+    eng.backward(ph, grads, dloss_f32=torch.tensor(scale, device=cuda))
+    torch.cuda.synchronize()
+
+    pr = {k: v.float().requires_grad_(True) for k, v in ph.items()}
+    lr = ref_loss(cfg, pr, images.float(), labels)
+    lr.backward()
+    assert abs(loss - lr.item()) <= 1e-2 * abs(lr.item()), (loss, lr.item())
+    for k in ph:
+        want = pr[k].grad
+        got = grads[k].float() / scale
+        mag = want.abs().max().item()
+        if mag <= 1e-4:
+            continue
+        err = (got - want).abs().max().item()
+        assert err <= 5e-2 * mag, f"{name} {half} leaf {k}: err {err:.3g} vs max {mag:.3g}"
+
+
+def test_vit_loss_through_filter_value_and_grad(cuda):
+    cfg = CFGS["small-cls"]
+    params = init_params(cfg, cuda, seed=0)
+    opt = mpx.adam_init(params, 1e-3)
+    scaling = mpx.DynamicLossScaling(2.0 ** 15)
+    f = vit_loss(cfg)
+    g = torch.Generator(device=cuda).manual_seed(0)
+    x = torch.randn(8, cfg.img, cfg.img, cfg.chans, device=cuda, generator=g)
+    y = torch.randint(0, cfg.classes, (8,), device=cuda, generator=g).to(torch.int32)
+    losses = []
+    for _ in range(6):
+        res = mpx.filter_value_and_grad(f, scaling)(params, {"x": x, "y": y})
+        params, opt = mpx.optimizer_update(params, opt, res.grads, res.grads_finite)
+        scaling = res.scaling
+        losses.append(res.value.item())
+        assert bool(res.grads_finite)
+        assert res.grads["blocks.0.qkv.w"].dtype == torch.float32
+    assert losses[-1] < losses[0], losses
