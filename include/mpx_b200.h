@@ -164,6 +164,7 @@ typedef struct mpx_gemm_desc {
   int block_n; /* 0 = auto */
   int split_k; /* <= 1: none */
   void* workspace;
+  int cta_group; /* 0 = auto, 1 = one CTA per 128-row tile, 2 = CTA pair per 256-row tile */
 } mpx_gemm_desc;
 
 int mpx_gemm(const mpx_gemm_desc* desc, void* stream);

@@ -38,7 +38,7 @@ constexpr int kBNMax = 256;
 constexpr int kStages = 4;
 constexpr int kATileBytes = kBM * kBK * 2;       // 16 KB
 constexpr int kBTileBytes = kBNMax * kBK * 2;    // 32 KB
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps
 constexpr int kGroupM = 16;
 constexpr size_t kGemmSmem = 1024 + kStages * (kATileBytes + kBTileBytes) + 256;
 
@@ -110,75 +110,99 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, long long t
   return c;
 }
 
+// CG = 1: one CTA per tile (M = 128).  CG = 2: a CTA pair (cluster of 2)
+// per 256-row tile: each CTA stages its 128 A rows and half of the BN B
+// columns, the leader issues tcgen05.mma.cta_group::2 (M = 256), so each SM
+// streams 2/3 of the bytes per FLOP of the 1-CTA tile.
+template <int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ GemmParams P) {
+  constexpr int S = CG == 1 ? kStages : 6;     // smem ring depth
+  constexpr int BT = kBTileBytes / CG;         // B bytes per stage per CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kStages * kATileBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBTileBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
+  uint8_t* sB = smem + S * kATileBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * BT);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const long long t_first = blockIdx.x / CG, t_step = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 256 * CG);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  if (warp == 1) {
+    if (CG == 2)
+      tmem_alloc_2sm<512>(tmem_slot);
+    else
+      tmem_alloc<512>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync();  // the peer's barriers exist before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const uint32_t a_bytes = kATileBytes;
-  const uint32_t b_bytes = (uint32_t)P.BN * kBK * 2;
+  const int bn_cta = P.BN / CG;  // B columns staged by this CTA
+  const uint32_t b_bytes = (uint32_t)bn_cta * kBK * 2;
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (long long t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+      for (long long t = t_first; t < P.total_tiles; t += t_step) {
         const TileCoord tc = tile_coord(P, t);
         const int b1 = tc.z % P.nb1, b2 = tc.z / P.nb1;
-        const int m0 = tc.m_blk * kBM, n0 = tc.n_blk * P.BN;
+        const int m0 = tc.m_blk * (kBM * CG) + (int)rank * kBM;
+        const int n0 = tc.n_blk * P.BN + (int)rank * bn_cta;
         const int kb0 = tc.s * P.kb_per_split;
         const int kb1 = min(P.k_blocks, kb0 + P.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], a_bytes + b_bytes);
+          if (leader) mbar_arrive_expect_tx(&full[stage], CG * (a_bytes + b_bytes));
           uint8_t* a = sA + stage * kATileBytes;
-          uint8_t* b = sB + stage * kBTileBytes;
+          uint8_t* b = sB + stage * BT;
           const int k0 = kb * kBK;
           const int ab1 = P.a_bc1 ? 0 : b1, ab2 = P.a_bc2 ? 0 : b2;
           const int bb1 = P.b_bc1 ? 0 : b1, bb2 = P.b_bc2 ? 0 : b2;
+          auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3) {
+            if (CG == 2)
+              tma_load_4d_2sm(dst, m, &full[stage], c0, c1, c2, c3);
+            else
+              tma_load_4d(dst, m, &full[stage], c0, c1, c2, c3);
+          };
           if (!P.a_mn) {
-            tma_load_4d(a, &tmA, &full[stage], k0, m0, ab1, ab2);
+            load(a, &tmA, k0, m0, ab1, ab2);
           } else {
-            tma_load_4d(a, &tmA, &full[stage], m0, k0, ab1, ab2);
-            tma_load_4d(a + 8192, &tmA, &full[stage], m0 + 64, k0, ab1, ab2);
+            load(a, &tmA, m0, k0, ab1, ab2);
+            load(a + 8192, &tmA, m0 + 64, k0, ab1, ab2);
           }
           if (!P.b_mn) {
-            tma_load_4d(b, &tmB, &full[stage], k0, n0, bb1, bb2);
+            load(b, &tmB, k0, n0, bb1, bb2);
           } else {
-            for (int c = 0; c < P.BN / 64; ++c) tma_load_4d(b + c * 8192, &tmB, &full[stage], n0 + 64 * c, k0, bb1, bb2);
+            for (int c = 0; c < bn_cta / 64; ++c) load(b + c * 8192, &tmB, n0 + 64 * c, k0, bb1, bb2);
           }
-          if (++stage == kStages) {
+          if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
@@ -186,13 +210,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       // ------------------------------------------------ MMA issuer
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (long long t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+      for (long long t = t_first; t < P.total_tiles; t += t_step) {
         const TileCoord tc = tile_coord(P, t);
         const int kb0 = tc.s * P.kb_per_split;
         const int kb1 = min(P.k_blocks, kb0 + P.kb_per_split);
@@ -203,58 +227,88 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a = smem_u32(sA + stage * kATileBytes);
-          const uint32_t b = smem_u32(sB + stage * kBTileBytes);
+          const uint32_t b = smem_u32(sB + stage * BT);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ad = P.a_mn ? sw128_desc(a + k * 2048, 8192, 1024) : sw128_desc(a + k * 32, 16, 1024);
             const uint64_t bd = P.b_mn ? sw128_desc(b + k * 2048, 8192, 1024) : sw128_desc(b + k * 32, 16, 1024);
-            umma_f16(d, ad, bd, P.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            if (CG == 2)
+              umma_f16_2sm(d, ad, bd, P.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            else
+              umma_f16(d, ad, bd, P.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty[stage]);  // smem slot free once these MMAs have read it
-          if (++stage == kStages) {
+          // smem slot free (in both CTAs) once these MMAs have read it
+          if (CG == 2)
+            umma_commit_2sm_mc(&empty[stage], 3);
+          else
+            umma_commit(&empty[stage]);
+          if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (CG == 2)
+          umma_commit_2sm_mc(&tfull[acc], 3);  // accumulator ready for both epilogues
+        else
+          umma_commit(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
     }
   } else {
-    // -------------------------------------------------- epilogue (128 thr)
+    // -------------------------------------------------- epilogue (256 thr)
+    // two warps per TMEM lane quarter (warp % 4), interleaving 16-column chunks
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int chunk0 = ((warp - 2) >> 2) * 16;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (long long t = blockIdx.x; t < P.total_tiles; t += gridDim.x) {
+    for (long long t = t_first; t < P.total_tiles; t += t_step) {
       const TileCoord tc = tile_coord(P, t);
       const int b1 = tc.z % P.nb1, b2 = tc.z / P.nb1;
-      const int row = tc.m_blk * kBM + q * 32 + lane;
+      const int row = tc.m_blk * (kBM * CG) + (int)rank * kBM + q * 32 + lane;
       const int n0 = tc.n_blk * P.BN;
       const bool row_ok = row < P.M;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
-      for (int c = 0; c < P.BN; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(taddr + c, r);
+      uint32_t r[16];
+      if (chunk0 < P.BN) tmem_ld16(taddr + chunk0, r);
+      for (int c = chunk0; c < P.BN; c += 32) {
         tmem_ld_wait();
-        const int col = n0 + c;
-        if (col >= P.N_store || !row_ok) continue;
-        const int ncols = min(16, P.N_store - col);  // 8 or 16
         float v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]) * P.alpha;
+        if (c + 32 < P.BN) tmem_ld16(taddr + c + 32, r);  // next chunk in flight while this one is processed
+        const int col = n0 + c;
+        if (col >= P.N_store || !row_ok) continue;
+        const int ncols = min(16, P.N_store - col);  // 8 or 16
         if (P.split > 1) {
           float* w = P.ws + ((long long)tc.s * P.M + row) * P.N + col;
           for (int i = 0; i < ncols; i += 4) *reinterpret_cast<float4*>(w + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
           continue;
         }
-        if (P.bias) {
-          const uint16_t* bb = static_cast<const uint16_t*>(P.bias) + col;
+        // epilogue operands: 16-byte vector loads (8 halves), never scalar
+        auto load8 = [&](const void* base, long long idx, float* o) {
+          const uint4 w = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(base) + idx);
+          const uint32_t u[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (i < ncols) v[i] += half_to_f32(bb[i], P.ab_fmt);
+          for (int e = 0; e < 4; ++e) {
+            o[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), P.ab_fmt);
+            o[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), P.ab_fmt);
+          }
+        };
+        if (P.bias) {
+          float bb[16];
+          if (col + 16 <= P.N) {
+            load8(P.bias, col, bb);
+            load8(P.bias, col + 8, bb + 8);
+          } else {  // ragged tail: the bias has exactly N entries
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              bb[i] = col + i < P.N ? half_to_f32(static_cast<const uint16_t*>(P.bias)[col + i], P.ab_fmt) : 0.f;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += bb[i];
         }
         if (P.act == ACT_GELU) {
           if (P.aux) {
@@ -273,17 +327,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = gelu_f(v[i]);
         } else if (P.act == ACT_GELU_BWD) {
-          const uint16_t* ax = static_cast<const uint16_t*>(P.aux) + (long long)row * P.ld_aux + col;
+          float z[16];
+          const long long ai = (long long)row * P.ld_aux + col;
+          load8(P.aux, ai, z);
+          if (ncols == 16) load8(P.aux, ai + 8, z + 8);
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (i < ncols) v[i] *= gelu_grad_f(half_to_f32(ax[i], P.ab_fmt));
+          for (int i = 0; i < 16; ++i) v[i] *= gelu_grad_f(z[i]);
         }
         if (P.res) {
-          const uint16_t* rr = static_cast<const uint16_t*>(P.res) + b1 * P.r_sb1 + b2 * P.r_sb2 +
-                               (long long)row * P.ldr + col;
+          float rr[16];
+          const long long ri = b1 * P.r_sb1 + b2 * P.r_sb2 + (long long)row * P.ldr + col;
+          load8(P.res, ri, rr);
+          if (ncols == 16) load8(P.res, ri + 8, rr + 8);
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (i < ncols) v[i] += half_to_f32(rr[i], P.ab_fmt);
+          for (int i = 0; i < 16; ++i) v[i] += rr[i];
         }
         const long long off = b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ldc + col;
         if (P.c_dtype == MPX_F32) {
@@ -301,15 +358,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if (CG == 2)
+        mbar_arrive_remote(&tempty[acc], 0);  // the leader's MMA reuses this accumulator
+      else
+        mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
   }
   __syncthreads();
+  if (CG == 2) cluster_sync();  // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem_base);
+    if (CG == 2)
+      tmem_dealloc_2sm<512>(tmem_base);
+    else
+      tmem_dealloc<512>(tmem_base);
   }
 }
 
@@ -387,6 +451,12 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   const int split = g->split_k > 1 ? g->split_k : 1;
   if (split > 1 && (nb1 * nb2 != 1 || !g->workspace)) return fail(MPX_EINVAL, "mpx_gemm: split-K needs batch 1 + workspace");
   if (split > 1 && g->act != ACT_NONE) return fail(MPX_EINVAL, "mpx_gemm: split-K supports no activation");
+  // CTA pair (M = 256 tiles) for the large problems; single CTA otherwise
+  int CG = g->cta_group;
+  const bool pair_ok = (BN == 256 || BN == 128) && (!g->b_mn_major || BN % 128 == 0);
+  if (CG == 0) CG = (pair_ok && g->M >= 1024) ? 2 : 1;
+  if (CG != 1 && CG != 2) return fail(MPX_EINVAL, "mpx_gemm: cta_group must be 0, 1 or 2");
+  if (CG == 2 && !pair_ok) return fail(MPX_EINVAL, "mpx_gemm: cta_group 2 needs BN 128/256");
 
   const uint64_t es = 2;
   CUtensorMap ta, tb;
@@ -402,7 +472,7 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   if (rc) return rc;
   if (!g->b_mn_major)
     rc = make_map(&tb, g->B, fmt, g->K, g->N, bn1, bn2, g->ldb * es, nz_stride(g->b_sb1 * es, g->ldb * es * g->N),
-                  nz_stride(g->b_sb2 * es, g->ldb * es * g->N), 64, BN);
+                  nz_stride(g->b_sb2 * es, g->ldb * es * g->N), 64, BN / CG);
   else
     rc = make_map(&tb, g->B, fmt, g->N, g->K, bn1, bn2, g->ldb * es, nz_stride(g->b_sb1 * es, g->ldb * es * g->K),
                   nz_stride(g->b_sb2 * es, g->ldb * es * g->K), 64, 64);
@@ -423,12 +493,12 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   P.b_bc1 = g->b_sb1 <= 0;
   P.b_bc2 = g->b_sb2 <= 0;
   P.split = split;
-  P.m_blocks = (g->M + kBM - 1) / kBM;
+  P.m_blocks = (g->M + kBM * CG - 1) / (kBM * CG);
   P.n_blocks = (g->N + BN - 1) / BN;
   P.k_blocks = (g->K + kBK - 1) / kBK;
   P.kb_per_split = (P.k_blocks + split - 1) / split;
   P.total_tiles = (long long)P.nbatch * split * P.m_blocks * P.n_blocks;
-  P.idesc = ptx::idesc_f16(fmt, kBM, BN, g->a_mn_major, g->b_mn_major);
+  P.idesc = ptx::idesc_f16(fmt, kBM * CG, BN, g->a_mn_major, g->b_mn_major);
   P.ab_fmt = fmt;
   P.C = g->C;
   P.ldc = g->ldc;
@@ -451,12 +521,31 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+    attr_err = cudaFuncSetAttribute(gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
   });
   if (attr_err != cudaSuccess) return fail((int)attr_err, "cudaFuncSetAttribute(gemm_kernel)");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const long long grid = std::min<long long>(P.total_tiles, current_num_sms());
-  gemm_kernel<<<(unsigned)grid, kGemmThreads, kGemmSmem, st>>>(ta, tb, P);
+  if (CG == 1) {
+    const long long grid = std::min<long long>(P.total_tiles, current_num_sms());
+    gemm_kernel<1><<<(unsigned)grid, kGemmThreads, kGemmSmem, st>>>(ta, tb, P);
+  } else {
+    const long long pairs = std::min<long long>(P.total_tiles, current_num_sms() / 2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * pairs));
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = kGemmSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MPX_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_kernel<2>, ta, tb, P));
+  }
   MPX_LAUNCH_CHECK("gemm_kernel");
   if (split > 1) {
     const long long mn = (long long)g->M * g->N;

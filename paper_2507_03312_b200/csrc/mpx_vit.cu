@@ -170,16 +170,29 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const void* __restrict__ x,
 }
 
 // sum ws partials over blocks -> half outputs (ws[0..nb) -> out0, ws[nb..2nb) -> out1)
-__global__ void partials_reduce_kernel(const float* __restrict__ ws, int nb, int D, void* out0, void* out1,
-                                       float alpha, int fmt) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < D; c += gridDim.x * blockDim.x) {
-    float a = 0.f, b = 0.f;
-    for (int k = 0; k < nb; ++k) {
+// block = 32 columns x 8 partial lanes (coalesced 128-byte reads), fixed order
+__global__ void __launch_bounds__(256) partials_reduce_kernel(const float* __restrict__ ws, int nb, int D, void* out0,
+                                                              void* out1, float alpha, int fmt) {
+  __shared__ float sa[8][33], sb[8][33];
+  const int cl = threadIdx.x & 31, kl = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
+  float a = 0.f, b = 0.f;
+  if (c < D)
+    for (int k = kl; k < nb; k += 8) {
       a += ws[(long long)k * D + c];
       b += ws[(long long)(nb + k) * D + c];
     }
-    if (out0) st_h(out0, c, a * alpha, fmt);
-    if (out1) st_h(out1, c, b * alpha, fmt);
+  sa[kl][cl] = a;
+  sb[kl][cl] = b;
+  __syncthreads();
+  if (kl == 0 && c < D) {
+    float x = 0.f, y = 0.f;
+    for (int k = 0; k < 8; ++k) {
+      x += sa[k][cl];
+      y += sb[k][cl];
+    }
+    if (out0) st_h(out0, c, x * alpha, fmt);
+    if (out1) st_h(out1, c, y * alpha, fmt);
   }
 }
 
@@ -233,6 +246,189 @@ __global__ void colsum_final_kernel(const float* __restrict__ ws, int splits, in
       static_cast<float*>(out)[z * ld_out + c] = s;
     else
       st_h(out, z * ld_out + c, s, out_dtype == MPX_BF16 ? 1 : 0);
+  }
+}
+
+// ===========================================================================
+// K6 attention softmax, register-resident rows (ld % 8 == 0, ld <= 256*CH):
+// each lane holds CH 8-element chunks; one 16-byte load and store per chunk.
+// ===========================================================================
+template <int CH>
+__global__ void __launch_bounds__(256) softmax_fwd_vec_kernel(const void* __restrict__ S, void* __restrict__ P,
+                                                              long long rows, int L, long long ld, int fmt) {
+  const int lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const uint16_t* s = static_cast<const uint16_t*>(S) + row * ld;
+  uint16_t* p = static_cast<uint16_t*>(P) + row * ld;
+  float v[CH][8];
+  float m = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const int c0 = (j * 32 + lane) * 8;
+    if (c0 < ld) {
+      unpack8(*reinterpret_cast<const uint4*>(s + c0), v[j], fmt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (c0 + e >= L) v[j][e] = -INFINITY;
+        m = fmaxf(m, v[j][e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[j][e] = -INFINITY;
+    }
+  }
+  m = warp_max(m);
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < CH; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      v[j][e] = v[j][e] == -INFINITY ? 0.f : expf(v[j][e] - m);
+      sum += v[j][e];
+    }
+  const float inv = 1.f / warp_sum(sum);
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const int c0 = (j * 32 + lane) * 8;
+    if (c0 < ld) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[j][e] *= inv;
+      *reinterpret_cast<uint4*>(p + c0) = pack8(v[j], fmt);
+    }
+  }
+}
+
+template <int CH>
+__global__ void __launch_bounds__(256) softmax_bwd_vec_kernel(const void* __restrict__ S, const void* __restrict__ dP,
+                                                              void* __restrict__ dS, long long rows, int L,
+                                                              long long ld, int fmt) {
+  const int lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const uint16_t* s = static_cast<const uint16_t*>(S) + row * ld;
+  const uint16_t* dp = static_cast<const uint16_t*>(dP) + row * ld;
+  uint16_t* ds = static_cast<uint16_t*>(dS) + row * ld;
+  float y[CH][8], g[CH][8];
+  float m = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const int c0 = (j * 32 + lane) * 8;
+    if (c0 < ld) {
+      unpack8(*reinterpret_cast<const uint4*>(s + c0), y[j], fmt);
+      unpack8(*reinterpret_cast<const uint4*>(dp + c0), g[j], fmt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (c0 + e >= L) y[j][e] = -INFINITY;
+        m = fmaxf(m, y[j][e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        y[j][e] = -INFINITY;
+        g[j][e] = 0.f;
+      }
+    }
+  }
+  m = warp_max(m);
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < CH; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      y[j][e] = y[j][e] == -INFINITY ? 0.f : expf(y[j][e] - m);
+      sum += y[j][e];
+    }
+  const float inv = 1.f / warp_sum(sum);
+  float t = 0.f;
+#pragma unroll
+  for (int j = 0; j < CH; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      y[j][e] *= inv;
+      t += g[j][e] * y[j][e];
+    }
+  t = warp_sum(t);
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    const int c0 = (j * 32 + lane) * 8;
+    if (c0 < ld) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) g[j][e] = y[j][e] * (g[j][e] - t);
+      *reinterpret_cast<uint4*>(ds + c0) = pack8(g[j], fmt);
+    }
+  }
+}
+
+// ===========================================================================
+// K7 LayerNorm backward, register-resident rows (D = 256 * V): per-lane
+// column partials of dgain/dbias stay in registers across the warp's rows.
+// ===========================================================================
+template <int V>
+__global__ void __launch_bounds__(256) ln_bwd_vec_kernel(const void* __restrict__ x, long long ldx,
+                                                         const void* __restrict__ g, const float* __restrict__ mean,
+                                                         const float* __restrict__ rstd, const void* __restrict__ dy,
+                                                         long long lddy, const void* __restrict__ dres, long long ldres,
+                                                         void* __restrict__ dx, long long lddx, float* __restrict__ ws,
+                                                         int rows, int D, int fmt) {
+  extern __shared__ float sh[];  // [8 warps][2][D]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float adg[V][8], adb[V][8];
+#pragma unroll
+  for (int j = 0; j < V; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) adg[j][e] = adb[j][e] = 0.f;
+  for (long long row = (long long)blockIdx.x * 8 + warp; row < rows; row += (long long)gridDim.x * 8) {
+    const float mu = mean[row], rs = rstd[row];
+    float xh[V][8], d[V][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int c0 = (j * 32 + lane) * 8;
+      float gg[8];
+      unpack8(*reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + row * ldx + c0), xh[j], fmt);
+      unpack8(*reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dy) + row * lddy + c0), d[j], fmt);
+      unpack8(__ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g) + c0)), gg, fmt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        xh[j][e] = (xh[j][e] - mu) * rs;
+        adg[j][e] += d[j][e] * xh[j][e];
+        adb[j][e] += d[j][e];
+        d[j][e] *= gg[e];  // d <- dy * g
+        s1 += d[j][e];
+        s2 += d[j][e] * xh[j][e];
+      }
+    }
+    s1 = warp_sum(s1) / (float)D;
+    s2 = warp_sum(s2) / (float)D;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int c0 = (j * 32 + lane) * 8;
+      float o[8], r[8];
+      if (dres) unpack8(*reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dres) + row * ldres + c0), r, fmt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = rs * (d[j][e] - s1 - xh[j][e] * s2) + (dres ? r[e] : 0.f);
+      *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dx) + row * lddx + c0) = pack8(o, fmt);
+    }
+  }
+  float* my = sh + warp * 2 * D;
+#pragma unroll
+  for (int j = 0; j < V; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = (j * 32 + lane) * 8 + e;
+      my[c] = adg[j][e];
+      my[D + c] = adb[j][e];
+    }
+  __syncthreads();
+  for (int c = threadIdx.x; c < D; c += blockDim.x) {
+    float a = 0.f, b = 0.f;
+    for (int w = 0; w < 8; ++w) {
+      a += sh[w * 2 * D + c];
+      b += sh[w * 2 * D + D + c];
+    }
+    ws[(long long)blockIdx.x * D + c] = a;
+    ws[(long long)gridDim.x * D + (long long)blockIdx.x * D + c] = b;
   }
 }
 
@@ -446,9 +642,31 @@ int mpx_layernorm_bwd(int dtype, const void* x, int64_t ldx, const void* gain, c
     }
   }
   const int f = fmt_of(dtype);
-  ln_bwd_kernel<<<nb, 256, sh, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace, rows, D, f);
+  const bool vec = ldx % 8 == 0 && lddy % 8 == 0 && lddx % 8 == 0 && (!dres || ldres % 8 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx) |
+                     reinterpret_cast<uintptr_t>(gain) | reinterpret_cast<uintptr_t>(dres)) % 16 == 0);
+  if (sh > 48 * 1024) {
+    static bool attr_vec = false;
+    if (!attr_vec) {
+      MPX_CUDA_CHECK(cudaFuncSetAttribute(ln_bwd_vec_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      MPX_CUDA_CHECK(cudaFuncSetAttribute(ln_bwd_vec_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr_vec = true;
+    }
+  }
+  if (vec && D == 768)
+    ln_bwd_vec_kernel<3><<<nb, 256, sh, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace,
+                                              rows, D, f);
+  else if (vec && D == 1024)
+    ln_bwd_vec_kernel<4><<<nb, 256, sh, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace,
+                                              rows, D, f);
+  else if (vec && D == 256)
+    ln_bwd_vec_kernel<1><<<nb, 256, sh, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace,
+                                              rows, D, f);
+  else
+    ln_bwd_kernel<<<nb, 256, sh, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace, rows, D,
+                                       f);
   MPX_LAUNCH_CHECK("ln_bwd_kernel");
-  partials_reduce_kernel<<<(D + 255) / 256, 256, 0, st>>>(workspace, nb, D, dgain, dbias, 1.f, f);
+  partials_reduce_kernel<<<(D + 31) / 32, 256, 0, st>>>(workspace, nb, D, dgain, dbias, 1.f, f);
   MPX_LAUNCH_CHECK("partials_reduce_kernel");
   return 0;
 }
@@ -477,8 +695,15 @@ int mpx_colsum(int dtype, const void* x, int64_t ldx, int64_t sbx, int rows, int
 int mpx_softmax_fwd(int dtype, const void* S, void* P, int64_t rows, int L, int64_t ld, void* stream) {
   if (!half_dtype(dtype) || ld < L) return fail(MPX_EINVAL, "softmax_fwd: bad args");
   if (rows <= 0) return 0;
-  softmax_fwd_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(S, P, rows, L, ld,
-                                                                                                 fmt_of(dtype));
+  const unsigned grid = (unsigned)((rows + 7) / 8);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool vec = ld % 8 == 0 && ((reinterpret_cast<uintptr_t>(S) | reinterpret_cast<uintptr_t>(P)) % 16 == 0);
+  if (vec && ld <= 256)
+    softmax_fwd_vec_kernel<1><<<grid, 256, 0, st>>>(S, P, rows, L, ld, fmt_of(dtype));
+  else if (vec && ld <= 512)
+    softmax_fwd_vec_kernel<2><<<grid, 256, 0, st>>>(S, P, rows, L, ld, fmt_of(dtype));
+  else
+    softmax_fwd_kernel<<<grid, 256, 0, st>>>(S, P, rows, L, ld, fmt_of(dtype));
   MPX_LAUNCH_CHECK("softmax_fwd_kernel");
   return 0;
 }
@@ -486,8 +711,16 @@ int mpx_softmax_fwd(int dtype, const void* S, void* P, int64_t rows, int L, int6
 int mpx_softmax_bwd(int dtype, const void* S, const void* dP, void* dS, int64_t rows, int L, int64_t ld, void* stream) {
   if (!half_dtype(dtype) || ld < L) return fail(MPX_EINVAL, "softmax_bwd: bad args");
   if (rows <= 0) return 0;
-  softmax_bwd_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(S, dP, dS, rows, L, ld,
-                                                                                                 fmt_of(dtype));
+  const unsigned grid = (unsigned)((rows + 7) / 8);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool vec = ld % 8 == 0 && ((reinterpret_cast<uintptr_t>(S) | reinterpret_cast<uintptr_t>(dP) |
+                                    reinterpret_cast<uintptr_t>(dS)) % 16 == 0);
+  if (vec && ld <= 256)
+    softmax_bwd_vec_kernel<1><<<grid, 256, 0, st>>>(S, dP, dS, rows, L, ld, fmt_of(dtype));
+  else if (vec && ld <= 512)
+    softmax_bwd_vec_kernel<2><<<grid, 256, 0, st>>>(S, dP, dS, rows, L, ld, fmt_of(dtype));
+  else
+    softmax_bwd_kernel<<<grid, 256, 0, st>>>(S, dP, dS, rows, L, ld, fmt_of(dtype));
   MPX_LAUNCH_CHECK("softmax_bwd_kernel");
   return 0;
 }

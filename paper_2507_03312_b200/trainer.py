@@ -1,0 +1,119 @@
+"""Data-parallel mixed-precision ViT training step (configs 3-5).
+
+One step, all stream-ordered, no host sync:
+
+    K1 cast images f32 -> half                       (cast_tree(args, half), precision.py:210)
+    forward / backward (vit.ViTEngine)               loss cotangent = f32(scale) / W read on the
+                                                     device, so the backward emits scaled half grads
+                                                     already divided by the DP world size
+    per-block NCCL all-reduce(sum) of the half grads, launched as soon as each
+    block's gradients exist, overlapping the rest of the backward
+    K2 -> all_reduce(flag, MIN) -> K4 (Adam, writes the next step's half
+    weights) -> K3                                   (step.FusedMPStep)
+
+Every rank holds the full f32 master weights / moments / scaling state
+(replicated) and takes the same skip/scale decision.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import kernels as K
+from .dtypes import F16, as_dtype
+from .precision import DynamicLossScaling
+from .step import FusedMPStep
+from .vit import ViTEngine, init_params
+from .vit_config import ViTConfig
+
+
+class GradBuckets:
+    """Contiguous gradient-arena slices, one per transformer block (plus the
+    head and the embedding), in the order the backward finishes them."""
+
+    def __init__(self, paths: list[str], offsets: list[int], numels: list[int], arena: torch.Tensor):
+        groups: dict[str, list[int]] = {}
+        for i, p in enumerate(paths):
+            key = p.split(".")[0] + ("." + p.split(".")[1] if p.startswith("blocks.") else "")
+            if p in ("ln_f.g", "ln_f.b", "head.w", "head.b"):
+                key = "head"
+            elif p in ("patch.w", "patch.b", "cls", "pos"):
+                key = "embed"
+            groups.setdefault(key, []).append(i)
+        self.views: dict[str, torch.Tensor] = {}
+        for key, idx in groups.items():
+            lo = min(offsets[i] for i in idx)
+            hi = max(offsets[i] + numels[i] for i in idx)
+            hi = -(-hi // 8) * 8
+            self.views[key] = arena[lo:hi]
+        for a in self.views.values():
+            for b in self.views.values():
+                if a is not b:
+                    assert a.data_ptr() + a.numel() * a.element_size() <= b.data_ptr() or \
+                        b.data_ptr() + b.numel() * b.element_size() <= a.data_ptr(), "buckets overlap"
+
+    def order(self, depth: int) -> list[str]:
+        return ["head"] + [f"blocks.{i}" for i in reversed(range(depth))] + ["embed"]
+
+
+class ViTTrainer:
+    def __init__(self, cfg: ViTConfig, batch_per_gpu: int, half=F16, lr: float = 1e-3, device=None,
+                 group=None, world_size: int = 1, seed: int = 0, loss_scale: float = 2.0 ** 15,
+                 weight_decay: float = 0.0):
+        self.cfg = cfg
+        self.B = batch_per_gpu
+        self.half = as_dtype(half)
+        self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.group = group
+        self.W = world_size
+        params = init_params(cfg, self.dev, seed=seed)  # same seed on every rank: replicas start equal
+        self.mp = FusedMPStep(params, lr, weight_decay=weight_decay, half_dtype=self.half,
+                              scaling=DynamicLossScaling(loss_scale, device=self.dev), process_group=group)
+        del params
+        self.engine = ViTEngine(cfg, batch_per_gpu, self.half, self.dev)
+        self.paths = self.mp.paths
+        self.P = dict(zip(self.paths, self.mp.p_half.views))
+        self.G = dict(zip(self.paths, self.mp.grad.views))
+        self.images_h = torch.empty(batch_per_gpu, cfg.img, cfg.img, cfg.chans, dtype=self.half.torch,
+                                    device=self.dev)
+        self.dloss = torch.zeros((), dtype=torch.float32, device=self.dev)
+        self.inv_w = torch.full((), 1.0 / world_size, dtype=torch.float32, device=self.dev)
+        numels = [v.numel() for v in self.mp.grad.views]
+        self.buckets = GradBuckets(self.paths, self.mp.grad.offsets, numels, self.mp.grad.buf)
+        self._pending = []
+
+    # ------------------------------------------------------------------
+    def _on_grads_ready(self, key: str):
+        if self.group is None:
+            return
+        work = torch.distributed.all_reduce(self.buckets.views[key], group=self.group, async_op=True)
+        self._pending.append(work)
+
+    def forward_backward(self, images: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
+        """images: [B, H, W, C] f32 (or already half) on the device."""
+        if images.dtype != self.half.torch:
+            K.cast_into([images], [self.images_h])
+            img = self.images_h
+        else:
+            img = images
+        loss = self.engine.forward(self.P, img, labels)
+        # loss cotangent f32(scale) * (1/W): the scaled, DP-averaged seed
+        K.cast_into([self.inv_w], [self.dloss], d_scale=self.mp.scaling.d_scale)
+        self.engine.backward(self.P, self.G, dloss_f32=self.dloss,
+                             on_grads_ready=self._on_grads_ready if self.group is not None else None)
+        return loss
+
+    def step(self, images: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
+        loss = self.forward_backward(images, labels)
+        for w in self._pending:
+            w.wait()
+        self._pending.clear()
+        self.mp.step()
+        return loss
+
+    @property
+    def grads_finite(self):
+        return self.mp.grads_finite
+
+    @property
+    def scaling(self) -> DynamicLossScaling:
+        return self.mp.scaling

@@ -186,10 +186,15 @@ class ViTEngine:
         return self.loss
 
     # ------------------------------------------------------------------
-    def backward(self, p: dict, g: dict, dloss_f32: torch.Tensor | None = None, dloss_f64: torch.Tensor | None = None):
+    def backward(self, p: dict, g: dict, dloss_f32: torch.Tensor | None = None, dloss_f64: torch.Tensor | None = None,
+                 on_grads_ready=None):
         """Gradients of (dloss * loss) into g (path -> half tensors).  The loss
         cotangent is read on the device: an f32 0-d tensor (autograd) or the
-        fp64 loss scale of a DynamicLossScaling state (fused training step)."""
+        fp64 loss scale of a DynamicLossScaling state (fused training step).
+        on_grads_ready(key) is called (host side, stream order) once the grads
+        of 'head', each 'blocks.<i>' and 'embed' have been launched, so a DP
+        exchange can start while the rest of the backward runs."""
+        ready = on_grads_ready or (lambda key: None)
         c, B, S, D, H, hd = self.cfg, self.B, self.S, self.D, self.H, self.hd
         M, st, lib = self.M, self._st(), self.lib
         cls = c.pool == "cls"
@@ -228,6 +233,7 @@ class ViTEngine:
                                         1.0 / S, st), "bcast_rows")
             self._ln_bwd(xl, D, p["ln_f.g"], self.muf, self.rsf, self.dfin, D, None, dX, D, g["ln_f.g"], g["ln_f.b"],
                          M)
+        ready("head")
         scale = 1.0 / math.sqrt(hd)
         for i in reversed(range(c.depth)):
             q = f"blocks.{i}."
@@ -275,6 +281,7 @@ class ViTEngine:
             # LN1 (+ residual): dX = LN1'(dA) + dXm
             self._ln_bwd(self.x[i], D, p[q + "ln1.g"], self.mu1[i], self.rs1[i], self.dA, D, dXm, dX, D,
                          g[q + "ln1.g"], g[q + "ln1.b"], M)
+            ready(f"blocks.{i}")
         # embedding: tokens = patches @ Wp + bp + pos (+ cls row)
         self._colsum(dX, S * D, B, S * D, g["pos"])  # sum over the batch
         if cls:
@@ -286,6 +293,7 @@ class ViTEngine:
             dpatch = dX
         self._colsum(dpatch, D, B * self.np, D, g["patch.b"])
         VK.linear_wgrad(self.patches, dpatch, out=g["patch.w"])
+        ready("embed")
 
 
 # ---------------------------------------------------------------------------

@@ -20,7 +20,7 @@ def _ptr(t):
 
 def gemm(A, B, *, M, N, K, lda, ldb, a_mn=False, b_mn=False, out=None, ldc=None, out_dtype=None, bias=None,
          residual=None, ldr=None, aux=None, ld_aux=None, act=ACT_NONE, alpha=1.0, nb=(1, 1), a_sb=(0, 0),
-         b_sb=(0, 0), c_sb=(0, 0), r_sb=(0, 0), split_k=1, workspace=None, block_n=0):
+         b_sb=(0, 0), c_sb=(0, 0), r_sb=(0, 0), split_k=1, workspace=None, block_n=0, cta_group=0):
     """C = epi(alpha * A @ B) on the tcgen05 GEMM (see mpx_gemm_desc)."""
     require_cuda([A, B], "gemm")
     if A.dtype != B.dtype or A.dtype not in (torch.float16, torch.bfloat16):
@@ -49,29 +49,31 @@ def gemm(A, B, *, M, N, K, lda, ldb, a_mn=False, b_mn=False, out=None, ldc=None,
     d.block_n = block_n
     d.split_k = split_k
     d.workspace = _ptr(workspace)
+    d.cta_group = cta_group
     _nat.check(_nat.load().mpx_gemm(ctypes.byref(d), stream_handle(A.device)), "mpx_gemm")
     return out
 
 
 # ---------------------------------------------------------------- linears
-def linear_fwd(x, w, bias=None, act=ACT_NONE, aux=None, residual=None, out=None):
+def linear_fwd(x, w, bias=None, act=ACT_NONE, aux=None, residual=None, out=None, cta_group=0):
     """y[M,N] = x[M,K] @ w[K,N] (+bias, GELU saving pre-act in aux, +residual)."""
     M, K = x.shape
     N_ = w.shape[1]
     return gemm(x, w, M=M, N=N_, K=K, lda=K, ldb=N_, b_mn=True, bias=bias, act=act, aux=aux, residual=residual,
-                out=out, ldc=N_ if out is not None else None)
+                out=out, ldc=N_ if out is not None else None, cta_group=cta_group)
 
 
-def linear_dgrad(dy, w, aux=None, out=None):
+def linear_dgrad(dy, w, aux=None, out=None, cta_group=0):
     """dx[M,K] = dy[M,N] @ w[K,N]^T; with aux (the GELU pre-activation of
     this layer's input) the GELU derivative is applied in the epilogue."""
     M, N_ = dy.shape
     K = w.shape[0]
     return gemm(dy, w, M=M, N=K, K=N_, lda=N_, ldb=N_, aux=aux, ld_aux=K,
-                act=ACT_GELU_BWD if aux is not None else ACT_NONE, out=out, ldc=K if out is not None else None)
+                act=ACT_GELU_BWD if aux is not None else ACT_NONE, out=out, ldc=K if out is not None else None,
+                cta_group=cta_group)
 
 
-def linear_wgrad(x, dy, out=None, split_k=None):
+def linear_wgrad(x, dy, out=None, split_k=None, cta_group=0):
     """dw[K,N] = x[M,K]^T @ dy[M,N] (reduction over the M tokens)."""
     M, K = x.shape
     N_ = dy.shape[1]
@@ -80,4 +82,4 @@ def linear_wgrad(x, dy, out=None, split_k=None):
         sms = torch.cuda.get_device_properties(x.device).multi_processor_count
         split_k = max(1, min(8, sms // max(tiles, 1), M // 2048))
     return gemm(x, dy, M=K, N=N_, K=M, lda=K, ldb=N_, a_mn=True, b_mn=True, out=out,
-                ldc=N_ if out is not None else None, split_k=split_k)
+                ldc=N_ if out is not None else None, split_k=split_k, cta_group=cta_group)

@@ -17,50 +17,57 @@ def close(got, want, rel=None):
     assert err <= tol * scale, f"max err {err} vs scale {scale}"
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (384, 768, 768), (200, 1000, 96), (50, 64, 48), (1000, 2304, 256)])
-def test_linear_fwd_dgrad_wgrad(cuda, dt, M, N, K):
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (384, 768, 768), (200, 1000, 96), (50, 64, 48), (1000, 2304, 256),
+                                   (1300, 512, 3072)])
+def test_linear_fwd_dgrad_wgrad(cuda, dt, M, N, K, cg):
+    def ok(n):  # the pair path needs 128/256-wide N tiles
+        return cg == 1 or n >= 256 or n == 128
     g = torch.Generator(device=cuda).manual_seed(M * 7 + N)
     x = torch.randn(M, K, device=cuda, generator=g).to(dt)
     w = (torch.randn(K, N, device=cuda, generator=g) / K ** 0.5).to(dt)
-    y = VK.linear_fwd(x, w)
-    close(y, x.float() @ w.float())
+    if ok(N):
+        y = VK.linear_fwd(x, w, cta_group=cg)
+        close(y, x.float() @ w.float())
     dy = torch.randn(M, N, device=cuda, generator=g).to(dt)
-    dx = VK.linear_dgrad(dy, w)
-    close(dx, dy.float() @ w.float().t())
+    if ok(K):
+        dx = VK.linear_dgrad(dy, w, cta_group=cg)
+        close(dx, dy.float() @ w.float().t())
     for split in (1, 2):
-        if (M + 63) // 64 < split:
+        if (M + 63) // 64 < split or not ok(N):
             continue
-        dw = VK.linear_wgrad(x, dy, split_k=split)
+        dw = VK.linear_wgrad(x, dy, split_k=split, cta_group=cg)
         close(dw, x.float().t() @ dy.float())
 
 
-def test_epilogue_bias_gelu_residual_alpha(cuda):
+@pytest.mark.parametrize("cg", [1, 2])
+def test_epilogue_bias_gelu_residual_alpha(cuda, cg):
     dt = torch.bfloat16
-    M, N, K = 300, 512, 192
+    M, N, K = 1300, 512, 256
     x = torch.randn(M, K, device=cuda).to(dt)
     w = (torch.randn(K, N, device=cuda) / K ** 0.5).to(dt)
     b = torch.randn(N, device=cuda).to(dt)
     r = torch.randn(M, N, device=cuda).to(dt)
     pre = torch.empty(M, N, device=cuda, dtype=dt)
-    y = VK.linear_fwd(x, w, bias=b, act=VK.ACT_GELU, aux=pre)
+    y = VK.linear_fwd(x, w, bias=b, act=VK.ACT_GELU, aux=pre, cta_group=cg)
     z = x.float() @ w.float() + b.float()
     close(pre, z)
     close(y, torch.nn.functional.gelu(pre.float(), approximate="tanh"))
-    y2 = VK.linear_fwd(x, w, bias=b, residual=r)
+    y2 = VK.linear_fwd(x, w, bias=b, residual=r, cta_group=cg)
     close(y2, z + r.float())
     # GELU backward in the dgrad epilogue
     dh = torch.randn(M, N, device=cuda).to(dt)
     w2 = (torch.randn(K, N, device=cuda) / N ** 0.5).to(dt)
-    dz = VK.linear_dgrad(dh, w2)
+    dz = VK.linear_dgrad(dh, w2, cta_group=cg)
     close(dz, dh.float() @ w2.float().t())
     zin = torch.randn(M, K, device=cuda).to(dt)
-    dzg = VK.linear_dgrad(dh, w2, aux=zin)
+    dzg = VK.linear_dgrad(dh, w2, aux=zin, cta_group=cg)
     zz = zin.float().requires_grad_(True)
     torch.nn.functional.gelu(zz, approximate="tanh").backward(dh.float() @ w2.float().t())
     close(dzg, zz.grad, rel=2e-2)
     # alpha + f32 output
-    o = VK.gemm(x, w, M=M, N=N, K=K, lda=K, ldb=N, b_mn=True, alpha=0.125, out_dtype=torch.float32)
+    o = VK.gemm(x, w, M=M, N=N, K=K, lda=K, ldb=N, b_mn=True, alpha=0.125, out_dtype=torch.float32, cta_group=cg)
     close(o, 0.125 * (x.float() @ w.float()), rel=1e-3)
 
 
