@@ -165,6 +165,7 @@ typedef struct mpx_gemm_desc {
   int split_k; /* <= 1: none */
   void* workspace;
   int cta_group; /* 0 = auto, 1 = one CTA per 128-row tile, 2 = CTA pair per 256-row tile */
+  int tma_store; /* 0 = auto (16-bit C through smem + TMA stores), -1 = direct stores */
 } mpx_gemm_desc;
 
 int mpx_gemm(const mpx_gemm_desc* desc, void* stream);

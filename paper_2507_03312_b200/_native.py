@@ -57,7 +57,7 @@ class GemmDescC(ctypes.Structure):
         ("r_sb1", ctypes.c_int64), ("r_sb2", ctypes.c_int64),
         ("aux", ctypes.c_void_p), ("ld_aux", ctypes.c_int64),
         ("alpha", ctypes.c_float), ("act", ctypes.c_int), ("block_n", ctypes.c_int), ("split_k", ctypes.c_int),
-        ("workspace", ctypes.c_void_p), ("cta_group", ctypes.c_int),
+        ("workspace", ctypes.c_void_p), ("cta_group", ctypes.c_int), ("tma_store", ctypes.c_int),
     ]
 
 

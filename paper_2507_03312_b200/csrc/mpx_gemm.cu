@@ -40,7 +40,7 @@ constexpr int kATileBytes = kBM * kBK * 2;       // 16 KB
 constexpr int kBTileBytes = kBNMax * kBK * 2;    // 32 KB
 constexpr int kGemmThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps
 constexpr int kGroupM = 16;
-constexpr size_t kGemmSmem = 1024 + kStages * (kATileBytes + kBTileBytes) + 256;
+constexpr size_t kGemmSmem = 1024 + kStages * (kATileBytes + kBTileBytes) + 8 * 4096 + 256;
 
 enum { ACT_NONE = 0, ACT_GELU = 1, ACT_GELU_BWD = 2 };
 
@@ -66,6 +66,7 @@ struct GemmParams {
   float alpha;
   int act;
   float* ws;  // split-K partials [split][M][N] (f32)
+  int tma_store;  // 16-bit C written through swizzled smem staging + TMA bulk stores
 };
 
 __device__ __forceinline__ float half_to_f32(uint16_t h, int fmt) {
@@ -117,14 +118,15 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, long long t
 template <int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ GemmParams P) {
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ GemmParams P) {
   constexpr int S = CG == 1 ? kStages : 6;     // smem ring depth
   constexpr int BT = kBTileBytes / CG;         // B bytes per stage per CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * kATileBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * BT);
+  uint8_t* stage_epi = sB + S * BT;  // 8 epilogue warps x 4 KB output staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_epi + 8 * 4096);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -139,6 +141,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (P.tma_store) tma_prefetch(&tmC);
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -257,46 +260,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     // -------------------------------------------------- epilogue (256 thr)
-    // two warps per TMEM lane quarter (warp % 4), interleaving 16-column chunks
+    // two warps per TMEM lane quarter (warp % 4); warp half h owns 64-column
+    // groups h, h+2, ... (TMA-store path) or 16-column chunks h, h+2, ...
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int chunk0 = ((warp - 2) >> 2) * 16;
+    const int h = (warp - 2) >> 2;
+    uint8_t* stg = stage_epi + (warp - 2) * 4096;  // 32 rows x 128 B, 128B-swizzled
     int acc = 0;
     uint32_t acc_phase = 0;
     for (long long t = t_first; t < P.total_tiles; t += t_step) {
       const TileCoord tc = tile_coord(P, t);
       const int b1 = tc.z % P.nb1, b2 = tc.z / P.nb1;
-      const int row = tc.m_blk * (kBM * CG) + (int)rank * kBM + q * 32 + lane;
+      const int row0 = tc.m_blk * (kBM * CG) + (int)rank * kBM + q * 32;
+      const int row = row0 + lane;
       const int n0 = tc.n_blk * P.BN;
       const bool row_ok = row < P.M;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
-      uint32_t r[16];
-      if (chunk0 < P.BN) tmem_ld16(taddr + chunk0, r);
-      for (int c = chunk0; c < P.BN; c += 32) {
-        tmem_ld_wait();
-        float v[16];
+
+      // bias / activation / residual on 16 consecutive columns of this row
+      auto load8 = [&](const void* base, long long idx, float* o) {
+        const uint4 w = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(base) + idx);
+        const uint32_t u[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]) * P.alpha;
-        if (c + 32 < P.BN) tmem_ld16(taddr + c + 32, r);  // next chunk in flight while this one is processed
-        const int col = n0 + c;
-        if (col >= P.N_store || !row_ok) continue;
-        const int ncols = min(16, P.N_store - col);  // 8 or 16
-        if (P.split > 1) {
-          float* w = P.ws + ((long long)tc.s * P.M + row) * P.N + col;
-          for (int i = 0; i < ncols; i += 4) *reinterpret_cast<float4*>(w + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          continue;
+        for (int e = 0; e < 4; ++e) {
+          o[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), P.ab_fmt);
+          o[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), P.ab_fmt);
         }
-        // epilogue operands: 16-byte vector loads (8 halves), never scalar
-        auto load8 = [&](const void* base, long long idx, float* o) {
-          const uint4 w = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(base) + idx);
-          const uint32_t u[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            o[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), P.ab_fmt);
-            o[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), P.ab_fmt);
-          }
-        };
+      };
+      auto epi = [&](float* v, int col, int ncols) {
         if (P.bias) {
           float bb[16];
           if (col + 16 <= P.N) {
@@ -342,19 +334,96 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += rr[i];
         }
-        const long long off = b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ldc + col;
-        if (P.c_dtype == MPX_F32) {
-          float* o = static_cast<float*>(P.C) + off;
-          for (int i = 0; i < ncols; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else {
-          const int f = P.c_dtype == MPX_BF16 ? 1 : 0;
-          uint32_t pk[8];
+      };
+
+      if (P.tma_store) {
+        // groups of 128 bytes per row: 64 half columns or 32 f32 columns
+        const bool f32out = P.split > 1 || P.c_dtype == MPX_F32;
+        const int GW = f32out ? 32 : 64;
+        const int cf = P.c_dtype == MPX_BF16 ? 1 : 0;
+        for (int g = h; g * GW < P.BN; g += 2) {
+          const int nch = min(GW / 16, (P.BN - g * GW) / 16);
+          if (lane == 0) bulk_wait_read0();  // the previous TMA store has read the staging buffer
+          __syncwarp();
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            pk[i] = (uint32_t)f32_to_half(v[2 * i], f) | ((uint32_t)f32_to_half(v[2 * i + 1], f) << 16);
-          uint16_t* o = static_cast<uint16_t*>(P.C) + off;
-          *reinterpret_cast<uint4*>(o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          if (ncols == 16) *reinterpret_cast<uint4*>(o + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          for (int pair = 0; pair < 2; ++pair) {  // two 16-column chunks per TMEM round trip
+            if (pair * 2 >= nch) break;
+            uint32_t r[2][16];
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+              if (pair * 2 + k < nch) tmem_ld16(taddr + g * GW + (pair * 2 + k) * 16, r[k]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int cc = pair * 2 + k;
+              if (cc >= nch) break;
+              float v[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[k][i]) * P.alpha;
+              const int col = n0 + g * GW + cc * 16;
+              uint8_t* rowp = stg + lane * 128;
+              const int sw = lane & 7;
+              if (f32out) {  // raw (split-K partial) or f32 output: 4 x 16 B per chunk
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  *reinterpret_cast<float4*>(rowp + (((4 * cc + j) ^ sw) << 4)) =
+                      make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              } else {
+                if (row_ok && col < P.N_store) epi(v, col, min(16, P.N_store - col));
+                uint32_t pk[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  pk[i] = (uint32_t)f32_to_half(v[2 * i], cf) | ((uint32_t)f32_to_half(v[2 * i + 1], cf) << 16);
+                *reinterpret_cast<uint4*>(rowp + (((2 * cc) ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                *reinterpret_cast<uint4*>(rowp + (((2 * cc + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+              }
+            }
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (P.split > 1)
+              tma_store_4d(&tmC, stg, n0 + g * GW, row0, tc.s, 0);
+            else
+              tma_store_4d(&tmC, stg, n0 + g * GW, row0, b1, b2);
+            bulk_commit();
+          }
+        }
+      } else {
+        uint32_t r[16];
+        const int chunk0 = h * 16;
+        if (chunk0 < P.BN) tmem_ld16(taddr + chunk0, r);
+        for (int c = chunk0; c < P.BN; c += 32) {
+          tmem_ld_wait();
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]) * P.alpha;
+          if (c + 32 < P.BN) tmem_ld16(taddr + c + 32, r);  // next chunk in flight while this one is processed
+          const int col = n0 + c;
+          if (col >= P.N_store || !row_ok) continue;
+          const int ncols = min(16, P.N_store - col);  // 8 or 16
+          if (P.split > 1) {
+            float* w = P.ws + ((long long)tc.s * P.M + row) * P.N + col;
+            for (int i = 0; i < ncols; i += 4)
+              *reinterpret_cast<float4*>(w + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            continue;
+          }
+          epi(v, col, ncols);
+          const long long off = b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ldc + col;
+          if (P.c_dtype == MPX_F32) {
+            float* o = static_cast<float*>(P.C) + off;
+            for (int i = 0; i < ncols; i += 4)
+              *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else {
+            const int f = P.c_dtype == MPX_BF16 ? 1 : 0;
+            uint32_t pk[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              pk[i] = (uint32_t)f32_to_half(v[2 * i], f) | ((uint32_t)f32_to_half(v[2 * i + 1], f) << 16);
+            uint16_t* o = static_cast<uint16_t*>(P.C) + off;
+            *reinterpret_cast<uint4*>(o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            if (ncols == 16) *reinterpret_cast<uint4*>(o + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
         }
       }
       tc_fence_before();
@@ -365,6 +434,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (P.tma_store && lane == 0) bulk_wait0();
   }
   __syncthreads();
   if (CG == 2) cluster_sync();  // no CTA leaves while its peer may still signal it
@@ -428,6 +498,21 @@ static int make_map(CUtensorMap* m, const void* ptr, int ab_fmt, uint64_t inner,
 
 // a zero batch stride means "shared across that batch dim": the map gets
 // extent 1 there (TMA strides must be non-zero) and the kernel uses coordinate 0
+static int make_map_dt(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
+                       uint64_t nb1, uint64_t nb2, uint64_t s_outer, uint64_t s_b1, uint64_t s_b2, uint32_t box_inner,
+                       uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return fail(MPX_EINVAL, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {inner, outer, nb1, nb2};
+  cuuint64_t strides[3] = {s_outer, s_b1, s_b2};
+  cuuint32_t box[4] = {box_inner, box_outer, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, dt, 4, const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MPX_EINVAL, "cuTensorMapEncodeTiled (C) failed (" + std::to_string((int)r) + ")");
+  return 0;
+}
+
 static uint64_t nz_stride(int64_t s, uint64_t fallback) { return s > 0 ? (uint64_t)s : fallback; }
 static uint64_t ext(int64_t s, int n) { return s > 0 ? (uint64_t)n : 1u; }
 
@@ -454,7 +539,7 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   // CTA pair (M = 256 tiles) for the large problems; single CTA otherwise
   int CG = g->cta_group;
   const bool pair_ok = (BN == 256 || BN == 128) && (!g->b_mn_major || BN % 128 == 0);
-  if (CG == 0) CG = (pair_ok && g->M >= 1024) ? 2 : 1;
+  if (CG == 0) CG = (pair_ok && g->M >= 512) ? 2 : 1;
   if (CG != 1 && CG != 2) return fail(MPX_EINVAL, "mpx_gemm: cta_group must be 0, 1 or 2");
   if (CG == 2 && !pair_ok) return fail(MPX_EINVAL, "mpx_gemm: cta_group 2 needs BN 128/256");
 
@@ -518,6 +603,37 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   if (split > 1 && (long long)(split - 1) * P.kb_per_split >= P.k_blocks)
     return fail(MPX_EINVAL, "mpx_gemm: split_k too large for K");
 
+  // outputs go through swizzled smem staging + TMA stores when the layout
+  // allows: 16-bit / f32 C, and the f32 split-K partials ws[split][M][N]
+  CUtensorMap tc = tb;
+  if (g->tma_store >= 0) {
+    if (split > 1) {
+      const uint64_t s_m = (uint64_t)g->N * 4;
+      if (g->N % 4 == 0 && reinterpret_cast<uintptr_t>(g->workspace) % 16 == 0 && (BN % 32 == 0)) {
+        rc = make_map_dt(&tc, g->workspace, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, g->N, g->M, split, 1, s_m,
+                         s_m * g->M, s_m * g->M * split, 32, 32);
+        if (rc) return rc;
+        P.tma_store = 1;
+      }
+    } else {
+      const int es_c = g->c_dtype == MPX_F32 ? 4 : 2;
+      const bool c_aligned = (reinterpret_cast<uintptr_t>(g->C) % 16 == 0) && (g->ldc * es_c) % 16 == 0 &&
+                             (nb1 == 1 || (g->c_sb1 > 0 && (g->c_sb1 * es_c) % 16 == 0)) &&
+                             (nb2 == 1 || (g->c_sb2 > 0 && (g->c_sb2 * es_c) % 16 == 0));
+      const int gw = es_c == 4 ? 32 : 64;
+      if (c_aligned && (BN % gw == 0 || P.n_blocks == 1) && (es_c == 2 || g->act == ACT_NONE && !g->bias && !g->residual)) {
+        const uint64_t s_m = (uint64_t)g->ldc * es_c;
+        const CUtensorMapDataType dt = g->c_dtype == MPX_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                       : g->c_dtype == MPX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                                : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+        rc = make_map_dt(&tc, g->C, dt, g->N, g->M, nb1, nb2, s_m, nb1 > 1 ? (uint64_t)g->c_sb1 * es_c : s_m * g->M,
+                         nb2 > 1 ? (uint64_t)g->c_sb2 * es_c : s_m * g->M, es_c == 4 ? 32 : 64, 32);
+        if (rc) return rc;
+        P.tma_store = 1;
+      }
+    }
+  }
+
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
@@ -529,7 +645,7 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (CG == 1) {
     const long long grid = std::min<long long>(P.total_tiles, current_num_sms());
-    gemm_kernel<1><<<(unsigned)grid, kGemmThreads, kGemmSmem, st>>>(ta, tb, P);
+    gemm_kernel<1><<<(unsigned)grid, kGemmThreads, kGemmSmem, st>>>(ta, tb, tc, P);
   } else {
     const long long pairs = std::min<long long>(P.total_tiles, current_num_sms() / 2);
     cudaLaunchConfig_t cfg{};
@@ -544,7 +660,7 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    MPX_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_kernel<2>, ta, tb, P));
+    MPX_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_kernel<2>, ta, tb, tc, P));
   }
   MPX_LAUNCH_CHECK("gemm_kernel");
   if (split > 1) {

@@ -20,7 +20,8 @@ def _ptr(t):
 
 def gemm(A, B, *, M, N, K, lda, ldb, a_mn=False, b_mn=False, out=None, ldc=None, out_dtype=None, bias=None,
          residual=None, ldr=None, aux=None, ld_aux=None, act=ACT_NONE, alpha=1.0, nb=(1, 1), a_sb=(0, 0),
-         b_sb=(0, 0), c_sb=(0, 0), r_sb=(0, 0), split_k=1, workspace=None, block_n=0, cta_group=0):
+         b_sb=(0, 0), c_sb=(0, 0), r_sb=(0, 0), split_k=1, workspace=None, block_n=0, cta_group=0,
+         tma_store=0):
     """C = epi(alpha * A @ B) on the tcgen05 GEMM (see mpx_gemm_desc)."""
     require_cuda([A, B], "gemm")
     if A.dtype != B.dtype or A.dtype not in (torch.float16, torch.bfloat16):
@@ -50,6 +51,7 @@ def gemm(A, B, *, M, N, K, lda, ldb, a_mn=False, b_mn=False, out=None, ldc=None,
     d.split_k = split_k
     d.workspace = _ptr(workspace)
     d.cta_group = cta_group
+    d.tma_store = tma_store
     _nat.check(_nat.load().mpx_gemm(ctypes.byref(d), stream_handle(A.device)), "mpx_gemm")
     return out
 
@@ -73,13 +75,50 @@ def linear_dgrad(dy, w, aux=None, out=None, cta_group=0):
                 cta_group=cta_group)
 
 
+_SMS: dict = {}
+
+
+def _num_sms(device) -> int:
+    n = _SMS.get(device)
+    if n is None:
+        n = _SMS[device] = torch.cuda.get_device_properties(device).multi_processor_count
+    return n
+
+
+def auto_cta_group(M: int, N: int, b_mn: bool) -> int:
+    """Mirror of mpx_gemm's automatic choice (csrc/mpx_gemm.cu)."""
+    bn = 256 if N >= 256 else -(-N // 16) * 16
+    if b_mn:
+        bn = -(-bn // 64) * 64
+    pair_ok = bn in (128, 256) and (not b_mn or bn % 128 == 0)
+    return 2 if pair_ok and M >= 512 else 1
+
+
+def auto_split_k(M: int, N: int, K: int, cg: int, sms: int) -> int:
+    """Split-K factor that fills the machine in whole waves (wgrad: M, N are
+    the weight dims, K the token count)."""
+    bn = 256 if N >= 256 else -(-N // 16) * 16
+    tiles = -(-M // (128 * cg)) * -(-N // bn)
+    slots = sms // cg
+    kb = -(-K // 64)
+    best, best_s = -1.0, 1
+    for s in range(1, 17):
+        if kb // s < 8:
+            break
+        units = tiles * s
+        util = units / (-(-units // slots) * slots)
+        score = util - 0.004 * s
+        if score > best:
+            best, best_s = score, s
+    return best_s
+
+
 def linear_wgrad(x, dy, out=None, split_k=None, cta_group=0):
     """dw[K,N] = x[M,K]^T @ dy[M,N] (reduction over the M tokens)."""
     M, K = x.shape
     N_ = dy.shape[1]
     if split_k is None:
-        tiles = -(-K // 128) * -(-N_ // 256)
-        sms = torch.cuda.get_device_properties(x.device).multi_processor_count
-        split_k = max(1, min(8, sms // max(tiles, 1), M // 2048))
+        cg = cta_group or auto_cta_group(K, N_, True)
+        split_k = auto_split_k(K, N_, M, cg, _num_sms(x.device))
     return gemm(x, dy, M=K, N=N_, K=M, lda=K, ldb=N_, a_mn=True, b_mn=True, out=out,
                 ldc=N_ if out is not None else None, split_k=split_k, cta_group=cta_group)
