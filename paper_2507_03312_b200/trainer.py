@@ -19,40 +19,12 @@ from __future__ import annotations
 import torch
 
 from . import kernels as K
+from .dp import GradBuckets, GradExchange
 from .dtypes import F16, as_dtype
 from .precision import DynamicLossScaling
 from .step import FusedMPStep
 from .vit import ViTEngine, init_params
 from .vit_config import ViTConfig
-
-
-class GradBuckets:
-    """Contiguous gradient-arena slices, one per transformer block (plus the
-    head and the embedding), in the order the backward finishes them."""
-
-    def __init__(self, paths: list[str], offsets: list[int], numels: list[int], arena: torch.Tensor):
-        groups: dict[str, list[int]] = {}
-        for i, p in enumerate(paths):
-            key = p.split(".")[0] + ("." + p.split(".")[1] if p.startswith("blocks.") else "")
-            if p in ("ln_f.g", "ln_f.b", "head.w", "head.b"):
-                key = "head"
-            elif p in ("patch.w", "patch.b", "cls", "pos"):
-                key = "embed"
-            groups.setdefault(key, []).append(i)
-        self.views: dict[str, torch.Tensor] = {}
-        for key, idx in groups.items():
-            lo = min(offsets[i] for i in idx)
-            hi = max(offsets[i] + numels[i] for i in idx)
-            hi = -(-hi // 8) * 8
-            self.views[key] = arena[lo:hi]
-        for a in self.views.values():
-            for b in self.views.values():
-                if a is not b:
-                    assert a.data_ptr() + a.numel() * a.element_size() <= b.data_ptr() or \
-                        b.data_ptr() + b.numel() * b.element_size() <= a.data_ptr(), "buckets overlap"
-
-    def order(self, depth: int) -> list[str]:
-        return ["head"] + [f"blocks.{i}" for i in reversed(range(depth))] + ["embed"]
 
 
 class ViTTrainer:
@@ -79,15 +51,9 @@ class ViTTrainer:
         self.inv_w = torch.full((), 1.0 / world_size, dtype=torch.float32, device=self.dev)
         numels = [v.numel() for v in self.mp.grad.views]
         self.buckets = GradBuckets(self.paths, self.mp.grad.offsets, numels, self.mp.grad.buf)
-        self._pending = []
+        self.exchange = GradExchange(self.buckets, group)
 
     # ------------------------------------------------------------------
-    def _on_grads_ready(self, key: str):
-        if self.group is None:
-            return
-        work = torch.distributed.all_reduce(self.buckets.views[key], group=self.group, async_op=True)
-        self._pending.append(work)
-
     def forward_backward(self, images: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
         """images: [B, H, W, C] f32 (or already half) on the device."""
         if images.dtype != self.half.torch:
@@ -99,14 +65,12 @@ class ViTTrainer:
         # loss cotangent f32(scale) * (1/W): the scaled, DP-averaged seed
         K.cast_into([self.inv_w], [self.dloss], d_scale=self.mp.scaling.d_scale)
         self.engine.backward(self.P, self.G, dloss_f32=self.dloss,
-                             on_grads_ready=self._on_grads_ready if self.group is not None else None)
+                             on_grads_ready=self.exchange.ready if self.group is not None else None)
         return loss
 
     def step(self, images: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
         loss = self.forward_backward(images, labels)
-        for w in self._pending:
-            w.wait()
-        self._pending.clear()
+        self.exchange.wait()
         self.mp.step()
         return loss
 
