@@ -1,0 +1,569 @@
+// K6 — fused attention for the ViT (sm_100a): softmax(Q K^T * scale) V per
+// (image, head), straight out of the [B, N, 3, H, hd] qkv activation, with no
+// N x N tensor in HBM.
+//
+// The reference computes scores in half, a full-precision softmax island and
+// probabilities cast back to half before P V (bench.py:196-198;
+// tensors.py:431-446).  Here the scores accumulate in f32 in TMEM, are
+// rounded to the half format (the reference's score dtype), the softmax runs
+// in f32 from TMEM, and P is rounded to half as the A operand of P V — the
+// same roundings as the unfused path.
+//
+// One CTA = one (b, h, 128-query tile); all keys (N <= 256) fit on chip:
+//   TMA   Q tile [128 x 64], K and V [256 x 64] (rows >= N zero-filled), SW128
+//   MMA1  S[128 x 256] = Q K^T       tcgen05 M128 N256, f32 in TMEM cols 0-255
+//   4 warps: one query row per thread, two TMEM passes (online max/sum, then
+//            P = exp(s - m) / l), P (half) into smem in the UMMA K-major layout
+//   MMA2  O[128 x 64] = P V          tcgen05 M128 N64 K256 (V read MN-major)
+//   epilogue: O rows -> merged [B*N, H*hd] layout
+#include "mpx_common.cuh"
+#include "sm100_ptx.cuh"
+
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+namespace mpx {
+
+using namespace ptx;
+
+constexpr int kAttnQ = 16384;      // Q tile 128 x 64 half
+constexpr int kAttnKV = 32768;     // K / V 256 x 64 half
+constexpr int kAttnP = 65536;      // P 128 x 256 half (4 K-major chunks of 64 keys)
+constexpr int kSplit = 2;          // softmax warps per TMEM lane quarter (column split)
+constexpr int kAttnThreads = 128 + 128 * kSplit;  // warps 0-3 control, then 4*kSplit softmax warps
+// forward smem: P (64 KB) overwrites the dead Q (16 KB) + K (32 KB) tiles once
+// S = Q K^T has been computed, so two CTAs fit on one SM
+constexpr size_t kAttnSmem = 1024 + kAttnP + kAttnKV + 2 * kSplit * 128 * 4 + 256;
+
+struct AttnParams {
+  int N, H, hd, m_tiles;
+  float scale;
+  int fmt;  // 0 f16, 1 bf16
+  void* O;
+  long long ldo;  // O row stride (elements); head h at column h*hd
+};
+
+__device__ __forceinline__ float h2f(uint16_t h, int fmt) { return fmt ? to_f32<MPX_BF16>(h) : to_f32<MPX_F16>(h); }
+__device__ __forceinline__ uint16_t f2h(float x, int fmt) { return fmt ? from_f32<MPX_BF16>(x) : from_f32<MPX_F16>(x); }
+__device__ __forceinline__ void quarter_sync(int q) {  // the kSplit warps sharing TMEM lane quarter q
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * kSplit) : "memory");
+}
+
+// row r's softmax statistics over the keys this split handles, combined over
+// the kSplit warps of the quarter through smem: returns (m, 1/l)
+__device__ __forceinline__ void softmax_stats(uint32_t trow, int split, int r, int q, int N, float scale, int fmt,
+                                              float* red, float& m_out, float& inv_out) {
+  const int n_chunks = (N + 15) / 16;
+  float m = -INFINITY, l = 0.f;
+  for (int c = split; c < n_chunks; c += kSplit) {
+    uint32_t a[16];
+    tmem_ld16(trow + c * 16, a);
+    tmem_ld_wait();
+    float sv[16], cm = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      sv[i] = c * 16 + i < N ? h2f(f2h(__uint_as_float(a[i]) * scale, fmt), fmt) : -INFINITY;
+      cm = fmaxf(cm, sv[i]);
+    }
+    const float nm = fmaxf(m, cm);
+    float add = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) add += sv[i] == -INFINITY ? 0.f : __expf(sv[i] - nm);
+    l = (m == -INFINITY ? 0.f : l * __expf(m - nm)) + add;
+    m = nm;
+  }
+  red[split * 128 + r] = m;
+  red[kSplit * 128 + split * 128 + r] = l;
+  quarter_sync(q);
+  float M = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < kSplit; ++j) M = fmaxf(M, red[j * 128 + r]);
+  float L = 0.f;
+#pragma unroll
+  for (int j = 0; j < kSplit; ++j) {
+    const float mj = red[j * 128 + r];
+    if (mj != -INFINITY) L += red[kSplit * 128 + j * 128 + r] * __expf(mj - M);
+  }
+  quarter_sync(q);  // red[] may be reused afterwards
+  m_out = M;
+  inv_out = 1.f / L;
+}
+
+// P chunk c (keys 16c..16c+15) of row r into the K-major SW128 P tile
+__device__ __forceinline__ void store_p_chunk(uint8_t* sP, int c, int r, const uint32_t* pk) {
+  uint8_t* rowp = sP + (c >> 2) * 16384 + r * 128;
+  const int u0 = (c & 3) * 2, sw = r & 7;
+  *reinterpret_cast<uint4*>(rowp + ((u0 ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  *reinterpret_cast<uint4*>(rowp + (((u0 + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+}
+
+// P = exp(round(s*scale) - m) * inv for the chunks of this split (zeros past N)
+__device__ __forceinline__ void softmax_write_p(uint32_t trow, int split, int r, int N, float scale, int fmt, float m,
+                                                float inv, uint8_t* sP) {
+  const int n_chunks = (N + 15) / 16;
+  for (int c = split; c < 16; c += kSplit) {
+    uint32_t pk[8];
+    if (c < n_chunks) {
+      uint32_t a[16];
+      tmem_ld16(trow + c * 16, a);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float e[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int col = c * 16 + 2 * i + j;
+          const float sv = h2f(f2h(__uint_as_float(a[2 * i + j]) * scale, fmt), fmt);
+          e[j] = col < N ? __expf(sv - m) * inv : 0.f;
+        }
+        pk[i] = (uint32_t)f2h(e[0], fmt) | ((uint32_t)f2h(e[1], fmt) << 16);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pk[i] = 0u;
+    }
+    store_p_chunk(sP, c, r, pk);
+  }
+}
+
+__global__ void __launch_bounds__(kAttnThreads, 2)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ AttnParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sP = smem;               // P, aliasing Q (0-16K) and K (16K-48K) after MMA1
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + kAttnQ;
+  uint8_t* sV = smem + kAttnP;
+  float* red = reinterpret_cast<float*>(sV + kAttnKV);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * kSplit * 128);  // 0 load, 1 S, 2 P, 3 O
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 4);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tile = blockIdx.x;
+  const int mt = tile % P.m_tiles;
+  const int bh = tile / P.m_tiles;
+  const int h = bh % P.H, b = bh / P.H;
+  const int m0 = mt * 128;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 128 * kSplit);
+    mbar_init(&bar[3], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bar[0], kAttnQ + 2 * kAttnKV);
+      tma_load_4d(sQ, &tmQ, &bar[0], 0, m0, h, b);
+      tma_load_4d(sK, &tmK, &bar[0], 0, 0, h, b);
+      tma_load_4d(sV, &tmV, &bar[0], 0, 0, h, b);
+      mbar_wait(&bar[0], 0);
+      tc_fence_after();
+      const uint32_t idesc1 = idesc_f16(P.fmt, 128, 256, 0, 0);
+      const uint32_t q = smem_u32(sQ), k = smem_u32(sK);
+#pragma unroll
+      for (int s = 0; s < 4; ++s)  // S = Q K^T into TMEM cols 0-255
+        umma_f16(tmem, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), idesc1, s > 0);
+      umma_commit(&bar[1]);
+      mbar_wait(&bar[2], 0);
+      tc_fence_after();
+      const uint32_t idesc2 = idesc_f16(P.fmt, 128, 64, 0, 1);
+      const uint32_t p = smem_u32(sP), v = smem_u32(sV);
+#pragma unroll
+      for (int s = 0; s < 16; ++s)  // O = P V into TMEM cols 0-63 (S is consumed)
+        umma_f16(tmem, sw128_desc(p + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
+                 sw128_desc(v + s * 2048, 8192, 1024), idesc2, s > 0);
+      umma_commit(&bar[3]);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3, split = (warp - 4) >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    mbar_wait(&bar[1], 0);
+    tc_fence_after();
+    float m, inv;
+    softmax_stats(trow, split, r, q, P.N, P.scale, P.fmt, red, m, inv);
+    softmax_write_p(trow, split, r, P.N, P.scale, P.fmt, m, inv, sP);
+    fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+    tc_fence_before();
+    mbar_arrive(&bar[2]);
+    mbar_wait(&bar[3], 0);
+    tc_fence_after();
+    const int qrow = m0 + r;
+    uint16_t* o = static_cast<uint16_t*>(P.O) + ((long long)b * P.N + qrow) * P.ldo + (long long)h * P.hd;
+    for (int c = split; c < 4; c += kSplit) {
+      uint32_t a[16];
+      tmem_ld16(trow + c * 16, a);
+      tmem_ld_wait();
+      if (qrow < P.N) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          pk[i] = (uint32_t)f2h(__uint_as_float(a[2 * i]), P.fmt) |
+                  ((uint32_t)f2h(__uint_as_float(a[2 * i + 1]), P.fmt) << 16);
+        *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
+// ===========================================================================
+// Backward: one CTA per (b, h), both 128-query tiles, all keys on chip.
+//   dP = dO V^T;  dS = P * (dP - rowsum(P * dP));  dV = P^T dO;
+//   dK = scale * dS^T Q;  dQ = scale * dS K        (autodiff.py:193-205, 233-240)
+// TMEM: cols 0-255 S, then dP, then dQ (per tile); 256-383 dV, 384-511 dK
+// (keys 0-127 / 128-255 as two M=128 halves), accumulated over the tiles.
+// smem: Q_t, dO_t (16 KB each), K, V (32 KB), P_t, dS_t (64 KB each): the P /
+// dS tiles are K-major A operands for dQ and, read MN-major, for dV / dK.
+// ===========================================================================
+// 224 KB of tiles + 2 KB reduction scratch + barriers: the alignment slack is
+// trimmed to fit the 227 KB limit (the dynamic window starts 1 KB-aligned when
+// the kernel has no static shared memory; checked at run time)
+constexpr size_t kAttnBwdBody = 2 * kAttnQ + 2 * kAttnKV + 2 * kAttnP + 2 * kSplit * 128 * 4 + 128;
+constexpr size_t kAttnBwdSmem = 232448;
+static_assert(kAttnBwdBody <= kAttnBwdSmem, "attention backward tiles exceed shared memory");
+
+struct AttnBwdParams {
+  int N, H, hd, m_tiles;
+  float scale;
+  int fmt;
+  void* dqkv;  // [B*N, 3*H*hd]
+  long long ld;
+};
+
+__global__ void __launch_bounds__(kAttnThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                    const __grid_constant__ AttnBwdParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  if (reinterpret_cast<uintptr_t>(smem) - reinterpret_cast<uintptr_t>(smem_raw) + kAttnBwdBody > kAttnBwdSmem) __trap();
+  uint8_t* sQ = smem;
+  uint8_t* sdO = sQ + kAttnQ;
+  uint8_t* sK = sdO + kAttnQ;
+  uint8_t* sV = sK + kAttnKV;
+  uint8_t* sP = sV + kAttnKV;
+  uint8_t* sdS = sP + kAttnP;
+  // 0 kv, 1 q/dO, 2 S, 3 P, 4 dP, 5 dS, 6 dQ(+dV,dK), 7 dQ read
+  float* red = reinterpret_cast<float*>(sdS + kAttnP);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * kSplit * 128);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int h = blockIdx.x % P.H, b = blockIdx.x / P.H;
+  const int T = P.m_tiles;
+  const long long D = (long long)P.H * P.hd;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmdO);
+    for (int i = 0; i < 8; ++i) mbar_init(&bar[i], (i == 3 || i == 5 || i == 7) ? 128 * kSplit : 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bar[0], 2 * kAttnKV);
+      tma_load_4d(sK, &tmK, &bar[0], 0, 0, h, b);
+      tma_load_4d(sV, &tmV, &bar[0], 0, 0, h, b);
+      mbar_arrive_expect_tx(&bar[1], 2 * kAttnQ);
+      tma_load_4d(sQ, &tmQ, &bar[1], 0, 0, h, b);
+      tma_load_4d(sdO, &tmdO, &bar[1], 0, 0, h, b);
+      const uint32_t q = smem_u32(sQ), dO = smem_u32(sdO), k = smem_u32(sK), v = smem_u32(sV);
+      const uint32_t pp = smem_u32(sP), ds = smem_u32(sdS);
+      const uint32_t id_nk = idesc_f16(P.fmt, 128, 256, 0, 0);  // [128 x 256] = X[128 x 64] Y[256 x 64]^T
+      const uint32_t id_kv = idesc_f16(P.fmt, 128, 64, 1, 1);   // dV / dK halves: A, B MN-major
+      const uint32_t id_q = idesc_f16(P.fmt, 128, 64, 0, 1);    // dQ: A K-major, B MN-major
+      mbar_wait(&bar[0], 0);
+      for (int t = 0; t < T; ++t) {
+        const uint32_t ph = t & 1;
+        mbar_wait(&bar[1], ph);
+        if (t > 0) mbar_wait(&bar[7], ph ^ 1);  // previous dQ drained from TMEM cols 0-63
+        tc_fence_after();
+#pragma unroll
+        for (int s = 0; s < 4; ++s)  // S = Q K^T
+          umma_f16(tmem, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), id_nk, s > 0);
+        umma_commit(&bar[2]);
+        mbar_wait(&bar[3], ph);  // P_t written (S consumed)
+        tc_fence_after();
+#pragma unroll
+        for (int s = 0; s < 4; ++s)  // dP = dO V^T
+          umma_f16(tmem, sw128_desc(dO + s * 32, 16, 1024), sw128_desc(v + s * 32, 16, 1024), id_nk, s > 0);
+        umma_commit(&bar[4]);
+        mbar_wait(&bar[5], ph);  // dS_t written (dP consumed)
+        tc_fence_after();
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {  // over the 128 queries of the tile
+            const uint64_t bdo = sw128_desc(dO + s * 2048, 8192, 1024);
+            const uint64_t bq = sw128_desc(q + s * 2048, 8192, 1024);
+            umma_f16(tmem + 256 + half * 64, sw128_desc(pp + half * 32768 + s * 2048, 16384, 1024), bdo, id_kv,
+                     (t > 0 || s > 0));  // dV += P^T dO
+            umma_f16(tmem + 384 + half * 64, sw128_desc(ds + half * 32768 + s * 2048, 16384, 1024), bq, id_kv,
+                     (t > 0 || s > 0));  // dK += dS^T Q
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < 16; ++s)  // dQ = dS K
+          umma_f16(tmem, sw128_desc(ds + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024), sw128_desc(k + s * 2048, 8192, 1024),
+                   id_q, s > 0);
+        umma_commit(&bar[6]);
+        if (t + 1 < T) {  // next tile's Q / dO once this tile's MMAs have read them
+          mbar_wait(&bar[6], ph);
+          mbar_arrive_expect_tx(&bar[1], 2 * kAttnQ);
+          tma_load_4d(sQ, &tmQ, &bar[1], 0, (t + 1) * 128, h, b);
+          tma_load_4d(sdO, &tmdO, &bar[1], 0, (t + 1) * 128, h, b);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int qd = warp & 3, split = (warp - 4) >> 2;
+    const int r = qd * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
+    const int n_chunks = (P.N + 15) / 16;
+    const int sw = r & 7;
+    auto read_p = [&](int c, float* pv) {  // own row of P_t, keys 16c..16c+15
+      const uint8_t* rowp = sP + (c >> 2) * 16384 + r * 128;
+      const int u0 = (c & 3) * 2;
+      const uint4 w0 = *reinterpret_cast<const uint4*>(rowp + ((u0 ^ sw) << 4));
+      const uint4 w1 = *reinterpret_cast<const uint4*>(rowp + (((u0 + 1) ^ sw) << 4));
+      const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        pv[2 * i] = h2f((uint16_t)(u[i] & 0xFFFFu), P.fmt);
+        pv[2 * i + 1] = h2f((uint16_t)(u[i] >> 16), P.fmt);
+      }
+    };
+    for (int t = 0; t < T; ++t) {
+      const uint32_t ph = t & 1;
+      // ---- P = softmax(round(S * scale)) -> smem (as in the forward)
+      mbar_wait(&bar[2], ph);
+      tc_fence_after();
+      float m, inv;
+      softmax_stats(trow, split, r, qd, P.N, P.scale, P.fmt, red, m, inv);
+      softmax_write_p(trow, split, r, P.N, P.scale, P.fmt, m, inv, sP);
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bar[3]);
+      // ---- dS = P * (dP - sum(P * dP)) -> smem
+      mbar_wait(&bar[4], ph);
+      tc_fence_after();
+      float tsum = 0.f;
+      for (int c = split; c < n_chunks; c += kSplit) {
+        uint32_t a[16];
+        float pv[16];
+        tmem_ld16(trow + c * 16, a);
+        read_p(c, pv);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) tsum += pv[i] * __uint_as_float(a[i]);
+      }
+      red[split * 128 + r] = tsum;
+      quarter_sync(qd);
+      tsum = 0.f;
+#pragma unroll
+      for (int j = 0; j < kSplit; ++j) tsum += red[j * 128 + r];
+      quarter_sync(qd);
+      for (int c = split; c < 16; c += kSplit) {
+        uint32_t pk[8];
+        if (c < n_chunks) {
+          uint32_t a[16];
+          float pv[16];
+          tmem_ld16(trow + c * 16, a);
+          read_p(c, pv);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float d0 = pv[2 * i] * (__uint_as_float(a[2 * i]) - tsum);
+            const float d1 = pv[2 * i + 1] * (__uint_as_float(a[2 * i + 1]) - tsum);
+            pk[i] = (uint32_t)f2h(d0, P.fmt) | ((uint32_t)f2h(d1, P.fmt) << 16);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) pk[i] = 0u;
+        }
+        store_p_chunk(sdS, c, r, pk);
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bar[5]);
+      // ---- dQ_t -> dqkv[:, q part]
+      mbar_wait(&bar[6], ph);
+      tc_fence_after();
+      const int qrow = t * 128 + r;
+      uint16_t* o = static_cast<uint16_t*>(P.dqkv) + ((long long)b * P.N + qrow) * P.ld + (long long)h * P.hd;
+      for (int c = split; c < 4; c += kSplit) {
+        uint32_t a[16];
+        tmem_ld16(trow + c * 16, a);
+        tmem_ld_wait();
+        if (qrow < P.N) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            pk[i] = (uint32_t)f2h(__uint_as_float(a[2 * i]) * P.scale, P.fmt) |
+                    ((uint32_t)f2h(__uint_as_float(a[2 * i + 1]) * P.scale, P.fmt) << 16);
+          *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bar[7]);
+    }
+    // ---- dV, dK (keys r and 128 + r of this head): 4 (half, which) combos split over the warps
+    for (int combo = split; combo < 4; combo += kSplit) {
+      const int half = combo >> 1, which = combo & 1;
+      const int key = half * 128 + r;
+      uint16_t* o = static_cast<uint16_t*>(P.dqkv) + ((long long)b * P.N + key) * P.ld + (which ? D : 2 * D) +
+                    (long long)h * P.hd;
+      const float mul = which ? P.scale : 1.f;
+      for (int c = 0; c < 4; ++c) {
+        uint32_t a[16];
+        tmem_ld16(trow + 256 + which * 128 + half * 64 + c * 16, a);
+        tmem_ld_wait();
+        if (key < P.N) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            pk[i] = (uint32_t)f2h(__uint_as_float(a[2 * i]) * mul, P.fmt) |
+                    ((uint32_t)f2h(__uint_as_float(a[2 * i + 1]) * mul, P.fmt) << 16);
+          *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 attn_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// map over one of Q/K/V inside qkv [B, N, 3, H, hd]: dims (hd, N, H, B)
+static int qkv_map(CUtensorMap* m, const void* base, int fmt, int N, int H, int hd, int B, uint32_t box_rows,
+                   int row_heads = 3) {
+  auto fn = attn_encode_fn();
+  if (!fn) return fail(MPX_EINVAL, "cuTensorMapEncodeTiled unavailable");
+  const uint64_t row = (uint64_t)row_heads * H * hd * 2;
+  cuuint64_t dims[4] = {(cuuint64_t)hd, (cuuint64_t)N, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {row, (cuuint64_t)hd * 2, row * N};
+  cuuint32_t box[4] = {64, box_rows, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, fmt ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+                  const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MPX_EINVAL, "attention tensor map failed (" + std::to_string((int)r) + ")");
+  return 0;
+}
+
+}  // namespace mpx
+
+using namespace mpx;
+
+extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H, int hd, float scale, void* O,
+                                 int64_t ldo, void* stream) {
+  if (dtype != MPX_F16 && dtype != MPX_BF16) return fail(MPX_EINVAL, "attention: f16/bf16 only");
+  if (hd != 64 || N < 1 || N > 256) return fail(MPX_EINVAL, "attention_fwd: fused path needs hd == 64, N <= 256");
+  const int fmt = dtype == MPX_BF16 ? 1 : 0;
+  const uint16_t* base = static_cast<const uint16_t*>(qkv);
+  const int D = H * hd;
+  CUtensorMap tq, tk, tv;
+  int rc = qkv_map(&tq, base, fmt, N, H, hd, B, 128);
+  if (!rc) rc = qkv_map(&tk, base + D, fmt, N, H, hd, B, 256);
+  if (!rc) rc = qkv_map(&tv, base + 2 * D, fmt, N, H, hd, B, 256);
+  if (rc) return rc;
+  AttnParams P{};
+  P.N = N;
+  P.H = H;
+  P.hd = hd;
+  P.m_tiles = (N + 127) / 128;
+  P.scale = scale;
+  P.fmt = fmt;
+  P.O = O;
+  P.ldo = ldo;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmem);
+  });
+  if (err != cudaSuccess) return fail((int)err, "cudaFuncSetAttribute(attn_fwd_kernel)");
+  const long long grid = (long long)B * H * P.m_tiles;
+  attn_fwd_kernel<<<(unsigned)grid, kAttnThreads, kAttnSmem, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, P);
+  MPX_LAUNCH_CHECK("attn_fwd_kernel");
+  return 0;
+}
+
+extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int B, int N, int H, int hd, float scale,
+                                 void* dqkv, void* stream) {
+  if (dtype != MPX_F16 && dtype != MPX_BF16) return fail(MPX_EINVAL, "attention: f16/bf16 only");
+  if (hd != 64 || N < 1 || N > 256) return fail(MPX_EINVAL, "attention_bwd: fused path needs hd == 64, N <= 256");
+  const int fmt = dtype == MPX_BF16 ? 1 : 0;
+  const uint16_t* base = static_cast<const uint16_t*>(qkv);
+  const int D = H * hd;
+  CUtensorMap tq, tk, tv, tdo;
+  int rc = qkv_map(&tq, base, fmt, N, H, hd, B, 128);
+  if (!rc) rc = qkv_map(&tk, base + D, fmt, N, H, hd, B, 256);
+  if (!rc) rc = qkv_map(&tv, base + 2 * D, fmt, N, H, hd, B, 256);
+  if (!rc) rc = qkv_map(&tdo, dO, fmt, N, H, hd, B, 128, 1);
+  if (rc) return rc;
+  AttnBwdParams P{};
+  P.N = N;
+  P.H = H;
+  P.hd = hd;
+  P.m_tiles = (N + 127) / 128;
+  P.scale = scale;
+  P.fmt = fmt;
+  P.dqkv = dqkv;
+  P.ld = 3LL * D;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnBwdSmem);
+  });
+  if (err != cudaSuccess) return fail((int)err, "cudaFuncSetAttribute(attn_bwd_kernel)");
+  attn_bwd_kernel<<<(unsigned)(B * H), kAttnThreads, kAttnBwdSmem, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, tdo,
+                                                                                                       P);
+  MPX_LAUNCH_CHECK("attn_bwd_kernel");
+  return 0;
+}

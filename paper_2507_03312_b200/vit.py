@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import torch
 
@@ -63,8 +64,14 @@ class ViTEngine:
         self.x = [e(M, D) for _ in range(c.depth + 1)]  # residual stream at each block input (+ final)
         self.a = [e(M, D) for _ in range(c.depth)]  # LN1 out
         self.qkv = [e(M, 3 * D) for _ in range(c.depth)]
-        self.Sm = [e(B * H * S, self.ldS) for _ in range(c.depth)]  # scaled scores
-        self.P = [e(B * H * S, self.ldS) for _ in range(c.depth)]
+        # fused attention (K6, mpx_attn.cu) keeps scores/probabilities on chip
+        # (hd == 64, N <= 256); it is opt-in (MPX_FUSED_ATTENTION=1) until its
+        # phases are pipelined — today the unfused path (tcgen05 GEMM + f32
+        # softmax island + GEMM, S/P round-tripping HBM) is faster end to end
+        self.fused_attn = (self.hd == 64 and S <= 256 and os.environ.get("MPX_FUSED_ATTENTION", "0") == "1")
+        if not self.fused_attn:
+            self.Sm = [e(B * H * S, self.ldS) for _ in range(c.depth)]  # scaled scores
+            self.P = [e(B * H * S, self.ldS) for _ in range(c.depth)]
         self.O = [e(M, D) for _ in range(c.depth)]
         self.xm = [e(M, D) for _ in range(c.depth)]  # after attention residual
         self.bn = [e(M, D) for _ in range(c.depth)]  # LN2 out
@@ -87,7 +94,7 @@ class ViTEngine:
         self.dXm = e(M, D)
         self.dO = e(M, D)
         self.dqkv = e(M, 3 * D)
-        self.dP = e(B * H * S, self.ldS)
+        self.dP = e(B * H * S, self.ldS) if not self.fused_attn else None
         self.dpre = e(M, c.mlp)
         self.dA = e(M, D)
         self.dlogits = e(B, self.ldl)
@@ -151,13 +158,18 @@ class ViTEngine:
             x, a, qkv = self.x[i], self.a[i], self.qkv[i]
             self._ln_fwd(x, D, p[q + "ln1.g"], p[q + "ln1.b"], a, D, self.mu1[i], self.rs1[i], M)
             VK.linear_fwd(a, p[q + "qkv.w"], bias=p[q + "qkv.b"], out=qkv)
-            Sm, P_, O = self.Sm[i], self.P[i], self.O[i]
-            VK.gemm(qkv, qkv[:, D:], M=S, N=S, K=hd, lda=3 * D, ldb=3 * D, nb=(H, B), a_sb=(hd, S * 3 * D),
-                    b_sb=(hd, S * 3 * D), out=Sm, ldc=self.ldS, c_sb=(S * self.ldS, H * S * self.ldS), alpha=scale)
-            self._ck(lib.mpx_softmax_fwd(self.code, Sm.data_ptr(), P_.data_ptr(), B * H * S, S, self.ldS, st),
-                     "softmax_fwd")
-            VK.gemm(P_, qkv[:, 2 * D:], M=S, N=hd, K=S, lda=self.ldS, ldb=3 * D, b_mn=True, nb=(H, B),
-                    a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * 3 * D), out=O, ldc=D, c_sb=(hd, S * D))
+            O = self.O[i]
+            if self.fused_attn:
+                VK.attention_fwd(qkv, B, S, H, hd, scale, out=O)
+            else:
+                Sm, P_ = self.Sm[i], self.P[i]
+                VK.gemm(qkv, qkv[:, D:], M=S, N=S, K=hd, lda=3 * D, ldb=3 * D, nb=(H, B), a_sb=(hd, S * 3 * D),
+                        b_sb=(hd, S * 3 * D), out=Sm, ldc=self.ldS, c_sb=(S * self.ldS, H * S * self.ldS),
+                        alpha=scale)
+                self._ck(lib.mpx_softmax_fwd(self.code, Sm.data_ptr(), P_.data_ptr(), B * H * S, S, self.ldS, st),
+                         "softmax_fwd")
+                VK.gemm(P_, qkv[:, 2 * D:], M=S, N=hd, K=S, lda=self.ldS, ldb=3 * D, b_mn=True, nb=(H, B),
+                        a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * 3 * D), out=O, ldc=D, c_sb=(hd, S * D))
             xm = self.xm[i]
             VK.linear_fwd(O, p[q + "proj.w"], bias=p[q + "proj.b"], residual=x, out=xm)
             bn = self.bn[i]
@@ -254,26 +266,11 @@ class ViTEngine:
             self._colsum(dXm, D, M, D, g[q + "proj.b"])
             VK.linear_dgrad(dXm, p[q + "proj.w"], out=self.dO)
             # attention
-            qkv, dqkv, P_, Sm = self.qkv[i], self.dqkv, self.P[i], self.Sm[i]
-            # dV[b,h] = P^T dO
-            VK.gemm(P_, self.dO, M=S, N=hd, K=S, lda=self.ldS, ldb=D, a_mn=True, b_mn=True, nb=(H, B),
-                    a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * D), out=dqkv[:, 2 * D:], ldc=3 * D,
-                    c_sb=(hd, S * 3 * D))
-            # dP = dO V^T
-            VK.gemm(self.dO, qkv[:, 2 * D:], M=S, N=S, K=hd, lda=D, ldb=3 * D, nb=(H, B), a_sb=(hd, S * D),
-                    b_sb=(hd, S * 3 * D), out=self.dP, ldc=self.ldS, c_sb=(S * self.ldS, H * S * self.ldS))
-            # dS = softmax'(dP) (in place), then the 1/sqrt(hd) of the score scaling folds into alpha
-            self._ck(lib.mpx_softmax_bwd(self.code, Sm.data_ptr(), self.dP.data_ptr(), self.dP.data_ptr(), B * H * S,
-                                         S, self.ldS, st), "softmax_bwd")
-            dS = self.dP
-            # dQ = dS K * scale
-            VK.gemm(dS, qkv[:, D:], M=S, N=hd, K=S, lda=self.ldS, ldb=3 * D, b_mn=True, nb=(H, B),
-                    a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * 3 * D), out=dqkv, ldc=3 * D,
-                    c_sb=(hd, S * 3 * D), alpha=scale)
-            # dK = dS^T Q * scale
-            VK.gemm(dS, qkv, M=S, N=hd, K=S, lda=self.ldS, ldb=3 * D, a_mn=True, b_mn=True, nb=(H, B),
-                    a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * 3 * D), out=dqkv[:, D:], ldc=3 * D,
-                    c_sb=(hd, S * 3 * D), alpha=scale)
+            qkv, dqkv = self.qkv[i], self.dqkv
+            if self.fused_attn:
+                VK.attention_bwd(qkv, self.dO, B, S, H, hd, scale, dqkv=dqkv)
+            else:
+                self._attention_bwd_unfused(i, qkv, dqkv, scale)
             # qkv = a @ Wqkv + bqkv
             VK.linear_wgrad(self.a[i], dqkv, out=g[q + "qkv.w"])
             self._colsum(dqkv, 3 * D, M, 3 * D, g[q + "qkv.b"])
@@ -294,6 +291,30 @@ class ViTEngine:
         self._colsum(dpatch, D, B * self.np, D, g["patch.b"])
         VK.linear_wgrad(self.patches, dpatch, out=g["patch.w"])
         ready("embed")
+
+
+    def _attention_bwd_unfused(self, i, qkv, dqkv, scale):
+        B, S, D, H, hd, st, lib = self.B, self.S, self.D, self.H, self.hd, self._st(), self.lib
+        P_, Sm = self.P[i], self.Sm[i]
+        # dV[b,h] = P^T dO
+        VK.gemm(P_, self.dO, M=S, N=hd, K=S, lda=self.ldS, ldb=D, a_mn=True, b_mn=True, nb=(H, B),
+                a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * D), out=dqkv[:, 2 * D:], ldc=3 * D,
+                c_sb=(hd, S * 3 * D))
+        # dP = dO V^T
+        VK.gemm(self.dO, qkv[:, 2 * D:], M=S, N=S, K=hd, lda=D, ldb=3 * D, nb=(H, B), a_sb=(hd, S * D),
+                b_sb=(hd, S * 3 * D), out=self.dP, ldc=self.ldS, c_sb=(S * self.ldS, H * S * self.ldS))
+        # dS = softmax'(dP) (in place), then the 1/sqrt(hd) of the score scaling folds into alpha
+        self._ck(lib.mpx_softmax_bwd(self.code, Sm.data_ptr(), self.dP.data_ptr(), self.dP.data_ptr(), B * H * S,
+                                     S, self.ldS, st), "softmax_bwd")
+        dS = self.dP
+        # dQ = dS K * scale
+        VK.gemm(dS, qkv[:, D:], M=S, N=hd, K=S, lda=self.ldS, ldb=3 * D, b_mn=True, nb=(H, B),
+                a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * 3 * D), out=dqkv, ldc=3 * D,
+                c_sb=(hd, S * 3 * D), alpha=scale)
+        # dK = dS^T Q * scale
+        VK.gemm(dS, qkv, M=S, N=hd, K=S, lda=self.ldS, ldb=3 * D, a_mn=True, b_mn=True, nb=(H, B),
+                a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * 3 * D), out=dqkv[:, D:], ldc=3 * D,
+                c_sb=(hd, S * 3 * D), alpha=scale)
 
 
 # ---------------------------------------------------------------------------

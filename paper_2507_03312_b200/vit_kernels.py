@@ -122,3 +122,24 @@ def linear_wgrad(x, dy, out=None, split_k=None, cta_group=0):
         split_k = auto_split_k(K, N_, M, cg, _num_sms(x.device))
     return gemm(x, dy, M=K, N=N_, K=M, lda=K, ldb=N_, a_mn=True, b_mn=True, out=out,
                 ldc=N_ if out is not None else None, split_k=split_k, cta_group=cta_group)
+
+
+def attention_fwd(qkv, B: int, N: int, H: int, hd: int, scale: float, out=None):
+    """Fused softmax(Q K^T * scale) V from qkv [B*N, 3*H*hd] into out [B*N, H*hd]."""
+    require_cuda([qkv], "attention_fwd")
+    D = H * hd
+    if out is None:
+        out = torch.empty(B * N, D, dtype=qkv.dtype, device=qkv.device)
+    _nat.check(_nat.load().mpx_attention_fwd(_CODE[qkv.dtype], qkv.data_ptr(), B, N, H, hd, scale, out.data_ptr(),
+                                             out.stride(0), stream_handle(qkv.device)), "mpx_attention_fwd")
+    return out
+
+
+def attention_bwd(qkv, dO, B: int, N: int, H: int, hd: int, scale: float, dqkv=None):
+    """Fused attention backward: the whole dqkv [B*N, 3*H*hd] from qkv and dO."""
+    require_cuda([qkv, dO], "attention_bwd")
+    if dqkv is None:
+        dqkv = torch.empty_like(qkv)
+    _nat.check(_nat.load().mpx_attention_bwd(_CODE[qkv.dtype], qkv.data_ptr(), dO.data_ptr(), B, N, H, hd, scale,
+                                             dqkv.data_ptr(), stream_handle(qkv.device)), "mpx_attention_bwd")
+    return dqkv

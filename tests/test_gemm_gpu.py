@@ -95,3 +95,38 @@ def test_batched_strided_attention_shapes(cuda):
             a_sb=(Nt * ldS, H * Nt * ldS), b_sb=(hd, Nt * 3 * D), out=O, ldc=D, c_sb=(hd, Nt * D))
     refO = torch.einsum("bhnm,bmhd->bnhd", P.float(), v.float()).reshape(Bsz * Nt, D)
     close(O, refO)
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("Nt", [197, 64, 130])
+def test_fused_attention_forward(cuda, dt, Nt):
+    Bsz, H, hd = 3, 4, 64
+    D = H * hd
+    g = torch.Generator(device=cuda).manual_seed(Nt)
+    qkv = (torch.randn(Bsz * Nt, 3 * D, device=cuda, generator=g) * 1.5).to(dt)
+    out = VK.attention_fwd(qkv, Bsz, Nt, H, hd, 0.125)
+    q, k, v = (qkv.view(Bsz, Nt, 3, H, hd)[:, :, i].float() for i in range(3))
+    s = (torch.einsum("bnhd,bmhd->bhnm", q, k) * 0.125).to(dt).float()  # scores rounded to half
+    p = torch.softmax(s, -1).to(dt).float()
+    ref = torch.einsum("bhnm,bmhd->bnhd", p, v).reshape(Bsz * Nt, D)
+    close(out, ref)
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("Nt", [197, 64, 130])
+def test_fused_attention_backward(cuda, dt, Nt):
+    Bsz, H, hd = 2, 3, 64
+    D = H * hd
+    g = torch.Generator(device=cuda).manual_seed(7 + Nt)
+    qkv = torch.randn(Bsz * Nt, 3 * D, device=cuda, generator=g).to(dt)
+    dO = torch.randn(Bsz * Nt, D, device=cuda, generator=g).to(dt)
+    dqkv = VK.attention_bwd(qkv, dO, Bsz, Nt, H, hd, 0.125)
+    x = qkv.float().requires_grad_(True)
+    q, k, v = (x.view(Bsz, Nt, 3, H, hd)[:, :, i] for i in range(3))
+    p = torch.softmax(torch.einsum("bnhd,bmhd->bhnm", q, k) * 0.125, -1)
+    o = torch.einsum("bhnm,bmhd->bnhd", p, v).reshape(Bsz * Nt, D)
+    o.backward(dO.float())
+    for i, name in enumerate("qkv"):
+        got = dqkv[:, i * D:(i + 1) * D]
+        want = x.grad[:, i * D:(i + 1) * D]
+        close(got, want, rel=3e-2)
