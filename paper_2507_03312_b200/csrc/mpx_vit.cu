@@ -656,7 +656,7 @@ int mpx_layernorm_bwd(int dtype, const void* x, int64_t ldx, const void* gain, c
   if (vec && D == 768)
     ln_bwd_vec_kernel<3><<<nb, 256, sh, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace,
                                               rows, D, f);
-  else if (vec && D == 1024)
+  else if (vec && D == 1024)  // (v2 would spill at 4 vectors per lane)
     ln_bwd_vec_kernel<4><<<nb, 256, sh, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace,
                                               rows, D, f);
   else if (vec && D == 256)
