@@ -117,7 +117,7 @@ __device__ __forceinline__ void softmax_write_p(uint32_t trow, int split, int r,
           const float sv = h2f(f2h(__uint_as_float(a[2 * i + j]) * scale, fmt), fmt);
           e[j] = col < N ? __expf(sv - m) * inv : 0.f;
         }
-        pk[i] = (uint32_t)f2h(e[0], fmt) | ((uint32_t)f2h(e[1], fmt) << 16);
+        pk[i] = pack2_fmt(e[0], e[1], fmt);
       }
     } else {
 #pragma unroll
@@ -211,8 +211,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         uint32_t pk[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          pk[i] = (uint32_t)f2h(__uint_as_float(a[2 * i]), P.fmt) |
-                  ((uint32_t)f2h(__uint_as_float(a[2 * i + 1]), P.fmt) << 16);
+          pk[i] = pack2_fmt(__uint_as_float(a[2 * i]), __uint_as_float(a[2 * i + 1]), P.fmt);
         *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
       }
@@ -403,7 +402,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           for (int i = 0; i < 8; ++i) {
             const float d0 = pv[2 * i] * (__uint_as_float(a[2 * i]) - tsum);
             const float d1 = pv[2 * i + 1] * (__uint_as_float(a[2 * i + 1]) - tsum);
-            pk[i] = (uint32_t)f2h(d0, P.fmt) | ((uint32_t)f2h(d1, P.fmt) << 16);
+            pk[i] = pack2_fmt(d0, d1, P.fmt);
           }
         } else {
 #pragma unroll
@@ -427,8 +426,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           uint32_t pk[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            pk[i] = (uint32_t)f2h(__uint_as_float(a[2 * i]) * P.scale, P.fmt) |
-                    ((uint32_t)f2h(__uint_as_float(a[2 * i + 1]) * P.scale, P.fmt) << 16);
+            pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * P.scale, __uint_as_float(a[2 * i + 1]) * P.scale, P.fmt);
           *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
@@ -451,8 +449,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           uint32_t pk[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            pk[i] = (uint32_t)f2h(__uint_as_float(a[2 * i]) * mul, P.fmt) |
-                    ((uint32_t)f2h(__uint_as_float(a[2 * i + 1]) * mul, P.fmt) << 16);
+            pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * mul, __uint_as_float(a[2 * i + 1]) * mul, P.fmt);
           *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }

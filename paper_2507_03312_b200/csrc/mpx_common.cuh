@@ -65,6 +65,21 @@ template <> __device__ __forceinline__ uint16_t from_f32<MPX_BF16>(float x) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(x));
 }
 
+// two f32 -> one packed pair (low half = a), RNE: a single cvt.rn.{f16,bf16}x2.f32
+// on the ALU pipe instead of two F2F conversions — bit-identical to from_f32
+template <int DT> __device__ __forceinline__ uint32_t pack2(float a, float b);
+template <> __device__ __forceinline__ uint32_t pack2<MPX_F16>(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+template <> __device__ __forceinline__ uint32_t pack2<MPX_BF16>(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ uint32_t pack2_fmt(float a, float b, int bf16) {
+  return bf16 ? pack2<MPX_BF16>(a, b) : pack2<MPX_F16>(a, b);
+}
+
 // round an f32 onto DT's grid, staying in f32 (quantize_array semantics)
 template <int DT> __device__ __forceinline__ float quantize_f32(float x) {
   return to_f32<DT>(from_f32<DT>(x));
@@ -109,8 +124,8 @@ template <int DT> struct Vec4Half {
   }
   __device__ __forceinline__ static uint2 pack(const float* x) {
     uint2 w;
-    w.x = (uint32_t)from_f32<DT>(x[0]) | ((uint32_t)from_f32<DT>(x[1]) << 16);
-    w.y = (uint32_t)from_f32<DT>(x[2]) | ((uint32_t)from_f32<DT>(x[3]) << 16);
+    w.x = pack2<DT>(x[0], x[1]);
+    w.y = pack2<DT>(x[2], x[3]);
     return w;
   }
   __device__ __forceinline__ static void load(const void* base, int64_t i, float* o) {

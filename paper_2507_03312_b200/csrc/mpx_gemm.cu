@@ -308,8 +308,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint32_t pk[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              const uint16_t lo = f32_to_half(v[2 * i], P.ab_fmt), hi = f32_to_half(v[2 * i + 1], P.ab_fmt);
-              pk[i] = (uint32_t)lo | ((uint32_t)hi << 16);
+              pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], P.ab_fmt);
+              const uint16_t lo = (uint16_t)(pk[i] & 0xFFFFu), hi = (uint16_t)(pk[i] >> 16);
               v[2 * i] = half_to_f32(lo, P.ab_fmt);  // GELU of the rounded pre-activation
               v[2 * i + 1] = half_to_f32(hi, P.ab_fmt);
             }
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 uint32_t pk[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
-                  pk[i] = (uint32_t)f32_to_half(v[2 * i], cf) | ((uint32_t)f32_to_half(v[2 * i + 1], cf) << 16);
+                  pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], cf);
                 *reinterpret_cast<uint4*>(rowp + (((2 * cc) ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 *reinterpret_cast<uint4*>(rowp + (((2 * cc + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
               }
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint32_t pk[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              pk[i] = (uint32_t)f32_to_half(v[2 * i], f) | ((uint32_t)f32_to_half(v[2 * i + 1], f) << 16);
+              pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], f);
             uint16_t* o = static_cast<uint16_t*>(P.C) + off;
             *reinterpret_cast<uint4*>(o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             if (ncols == 16) *reinterpret_cast<uint4*>(o + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);

@@ -32,14 +32,8 @@ __device__ __forceinline__ void unpack8(uint4 w, float* o, int fmt) {
   }
 }
 __device__ __forceinline__ uint4 pack8(const float* x, int fmt) {
-  uint32_t u[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint16_t lo = fmt ? from_f32<MPX_BF16>(x[2 * i]) : from_f32<MPX_F16>(x[2 * i]);
-    const uint16_t hi = fmt ? from_f32<MPX_BF16>(x[2 * i + 1]) : from_f32<MPX_F16>(x[2 * i + 1]);
-    u[i] = (uint32_t)lo | ((uint32_t)hi << 16);
-  }
-  return make_uint4(u[0], u[1], u[2], u[3]);
+  return make_uint4(pack2_fmt(x[0], x[1], fmt), pack2_fmt(x[2], x[3], fmt), pack2_fmt(x[4], x[5], fmt),
+                    pack2_fmt(x[6], x[7], fmt));
 }
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
