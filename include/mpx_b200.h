@@ -182,6 +182,14 @@ int mpx_layernorm_bwd_blocks(int rows);
 int mpx_layernorm_bwd(int dtype, const void* x, int64_t ldx, const void* gain, const float* mean, const float* rstd,
                       const void* dy, int64_t lddy, const void* dres, int64_t ldres, void* dx, int64_t lddx,
                       void* dgain, void* dbias, float* workspace, int rows, int D, void* stream);
+/* K7 backward, occupancy-split form: dx as above, then one coalesced pass
+ * for dgain, dbias and (dxsum != NULL) the column sum of dx itself — the
+ * gradient of the bias that produced this residual stream (proj.b / fc2.b).
+ * workspace >= 3 * splits * D floats (splits <= 4 * SMs). */
+int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, const float* mean, const float* rstd,
+                       const void* dy, int64_t lddy, const void* dres, int64_t ldres, void* dx, int64_t lddx,
+                       void* dgain, void* dbias, void* dxsum, float* workspace, int64_t workspace_floats, int rows,
+                       int D, void* stream);
 /* out[z][c] = alpha * sum_r x[z][r][c]: bias / position gradients
  * (_unbroadcast, autodiff.py:88-99) and the mean-pool island; deterministic
  * two passes through workspace (>= splits*cols*batches f32). */

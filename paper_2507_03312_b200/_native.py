@@ -81,6 +81,9 @@ SIGNATURES = {
     "mpx_layernorm_bwd": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, _P, _P, _P, _P, ctypes.c_int64, _P,
                                          ctypes.c_int64, _P, ctypes.c_int64, _P, _P, _P, ctypes.c_int, ctypes.c_int,
                                          _P]),
+    "mpx_layernorm_bwd2": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, _P, _P, _P, _P, ctypes.c_int64, _P,
+                                          ctypes.c_int64, _P, ctypes.c_int64, _P, _P, _P, _P, ctypes.c_int64,
+                                          ctypes.c_int, ctypes.c_int, _P]),
     "mpx_colsum": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                   ctypes.c_int, _P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_float,
                                   _P]),

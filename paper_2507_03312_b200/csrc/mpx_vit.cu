@@ -163,6 +163,138 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const void* __restrict__ x,
   }
 }
 
+// ===========================================================================
+// K7 LayerNorm backward, split for occupancy (v3):
+//   ln_dx_kernel        dx = rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)) + dres,
+//                       one warp per row, 16-byte vectors, no column state
+//   ln_colsum_kernel    column partials of dy*xhat (dgain), dy (dbias) and,
+//                       optionally, of dx itself (the bias gradient of the layer
+//                       that produced the residual stream) — one coalesced pass
+// ===========================================================================
+template <int V>
+__global__ void __launch_bounds__(256) ln_dx_kernel(const void* __restrict__ x, long long ldx,
+                                                    const void* __restrict__ g, const float* __restrict__ mean,
+                                                    const float* __restrict__ rstd, const void* __restrict__ dy,
+                                                    long long lddy, const void* __restrict__ dres, long long ldres,
+                                                    void* __restrict__ dx, long long lddx, int rows, int D, int fmt) {
+  const int lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  uint4 wx[V], wd[V], wr[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int c0 = (j * 32 + lane) * 8;
+    wx[j] = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + row * ldx + c0);
+    wd[j] = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dy) + row * lddy + c0);
+    if (dres) wr[j] = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dres) + row * ldres + c0);
+  }
+  const float mu = mean[row], rs = rstd[row];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int c0 = (j * 32 + lane) * 8;
+    float xv[8], dv[8], gg[8];
+    unpack8(wx[j], xv, fmt);
+    unpack8(wd[j], dv, fmt);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g) + c0)), gg, fmt);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float dg = dv[e] * gg[e];
+      s1 += dg;
+      s2 += dg * (xv[e] - mu) * rs;
+    }
+  }
+  s1 = warp_sum(s1) / (float)D;
+  s2 = warp_sum(s2) / (float)D;
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int c0 = (j * 32 + lane) * 8;
+    float xv[8], dv[8], gg[8], rv[8], o[8];
+    unpack8(wx[j], xv, fmt);
+    unpack8(wd[j], dv, fmt);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g) + c0)), gg, fmt);
+    if (dres) unpack8(wr[j], rv, fmt);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = rs * (dv[e] * gg[e] - s1 - (xv[e] - mu) * rs * s2) + (dres ? rv[e] : 0.f);
+    *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dx) + row * lddx + c0) = pack8(o, fmt);
+  }
+}
+
+// block = 32 column vectors of 8 (256 columns) x 8 row lanes; ws layout
+// [nsum][split][D] with nsum = 2 (dgain, dbias) or 3 (+ colsum(dx))
+__global__ void __launch_bounds__(256) ln_colsum_kernel(const void* __restrict__ x, long long ldx,
+                                                        const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                        const void* __restrict__ dy, long long lddy,
+                                                        const void* __restrict__ dx, long long lddx, int rows, int D,
+                                                        int rows_per_split, float* __restrict__ ws, int fmt) {
+  __shared__ float sh[3][8][257];
+  const int cv = threadIdx.x & 31, rl = threadIdx.x >> 5;
+  const int c0 = blockIdx.x * 256 + cv * 8;
+  const int split = blockIdx.y, nsplit = gridDim.y;
+  const int r0 = split * rows_per_split, r1 = min(rows, r0 + rows_per_split);
+  float ag[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ax[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const bool live = c0 < D;
+  if (live) {
+    for (int r = r0 + rl; r < r1; r += 8) {
+      float xv[8], dv[8];
+      unpack8(*reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + (long long)r * ldx + c0), xv, fmt);
+      unpack8(*reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dy) + (long long)r * lddy + c0), dv, fmt);
+      const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        ag[e] += dv[e] * (xv[e] - mu) * rs;
+        ab[e] += dv[e];
+      }
+      if (dx) {
+        float ov[8];
+        unpack8(*reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dx) + (long long)r * lddx + c0), ov,
+                fmt);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ax[e] += ov[e];
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    sh[0][rl][cv * 8 + e] = ag[e];
+    sh[1][rl][cv * 8 + e] = ab[e];
+    sh[2][rl][cv * 8 + e] = ax[e];
+  }
+  __syncthreads();
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c < D) {
+    const int nsum = dx ? 3 : 2;
+    for (int k = 0; k < nsum; ++k) {
+      float t = 0.f;
+      for (int l = 0; l < 8; ++l) t += sh[k][l][threadIdx.x];
+      ws[((long long)k * nsplit + split) * D + c] = t;
+    }
+  }
+}
+
+// ws [nsum][nb][D] -> outputs; block = 32 columns x 8 partial lanes
+__global__ void __launch_bounds__(256) partials_reduce3_kernel(const float* __restrict__ ws, int nb, int D,
+                                                               void* out0, void* out1, void* out2, int fmt) {
+  __shared__ float sm[3][8][33];
+  const int cl = threadIdx.x & 31, kl = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
+  void* outs[3] = {out0, out1, out2};
+  const int nsum = out2 ? 3 : 2;
+  for (int q = 0; q < nsum; ++q) {
+    float a = 0.f;
+    if (c < D)
+      for (int k = kl; k < nb; k += 8) a += ws[((long long)q * nb + k) * D + c];
+    sm[q][kl][cl] = a;
+  }
+  __syncthreads();
+  if (kl == 0 && c < D)
+    for (int q = 0; q < nsum; ++q) {
+      float t = 0.f;
+      for (int k = 0; k < 8; ++k) t += sm[q][k][cl];
+      if (outs[q]) st_h(outs[q], c, t, fmt);
+    }
+}
+
 // sum ws partials over blocks -> half outputs (ws[0..nb) -> out0, ws[nb..2nb) -> out1)
 // block = 32 columns x 8 partial lanes (coalesced 128-byte reads), fixed order
 __global__ void __launch_bounds__(256) partials_reduce_kernel(const float* __restrict__ ws, int nb, int D, void* out0,
@@ -228,13 +360,23 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const void* __restr
   }
 }
 
-__global__ void colsum_final_kernel(const float* __restrict__ ws, int splits, int cols, int batches, void* out,
-                                    long long ld_out, int out_dtype, float alpha) {
+// block = 32 columns x 8 split lanes (coalesced), fixed summation order
+__global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restrict__ ws, int splits, int cols,
+                                                           int batches, void* out, long long ld_out, int out_dtype,
+                                                           float alpha) {
+  __shared__ float sm[8][33];
+  const int cl = threadIdx.x & 31, kl = threadIdx.x >> 5;
+  const long long i = (long long)blockIdx.x * 32 + cl;  // flat (z, c)
   const long long n = (long long)cols * batches;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const long long z = i / cols, c = i - z * cols;
+  const long long z = i / cols, c = i - z * cols;
+  float a = 0.f;
+  if (i < n)
+    for (int k = kl; k < splits; k += 8) a += ws[(z * splits + k) * cols + c];
+  sm[kl][cl] = a;
+  __syncthreads();
+  if (kl == 0 && i < n) {
     float s = 0.f;
-    for (int k = 0; k < splits; ++k) s += ws[(z * splits + k) * cols + c];
+    for (int k = 0; k < 8; ++k) s += sm[k][cl];
     s *= alpha;
     if (out_dtype == MPX_F32)
       static_cast<float*>(out)[z * ld_out + c] = s;
@@ -665,6 +807,45 @@ int mpx_layernorm_bwd(int dtype, const void* x, int64_t ldx, const void* gain, c
   return 0;
 }
 
+int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, const float* mean, const float* rstd,
+                       const void* dy, int64_t lddy, const void* dres, int64_t ldres, void* dx, int64_t lddx,
+                       void* dgain, void* dbias, void* dxsum, float* workspace, int64_t workspace_floats, int rows,
+                       int D, void* stream) {
+  if (!half_dtype(dtype)) return fail(MPX_EINVAL, "layernorm_bwd2: f16/bf16 only");
+  if (rows <= 0) return 0;
+  const bool vec = D % 256 == 0 && D <= 1024 && ldx % 8 == 0 && lddy % 8 == 0 && lddx % 8 == 0 &&
+                   (!dres || ldres % 8 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx) |
+                     reinterpret_cast<uintptr_t>(gain) | reinterpret_cast<uintptr_t>(dres)) % 16 == 0);
+  if (!vec) {  // generic shapes: the fused single-kernel path (+ a separate dx colsum)
+    int rc = mpx_layernorm_bwd(dtype, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, dgain, dbias,
+                               workspace, rows, D, stream);
+    if (rc || !dxsum) return rc;
+    return mpx_colsum(dtype, dx, lddx, 0, rows, D, 1, workspace, workspace_floats, dxsum, D, dtype, 1.f, stream);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int f = fmt_of(dtype);
+  const unsigned g1 = (unsigned)((rows + 7) / 8);
+  switch (D / 256) {
+    case 1: ln_dx_kernel<1><<<g1, 256, 0, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f); break;
+    case 2: ln_dx_kernel<2><<<g1, 256, 0, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f); break;
+    case 3: ln_dx_kernel<3><<<g1, 256, 0, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f); break;
+    default: ln_dx_kernel<4><<<g1, 256, 0, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f); break;
+  }
+  MPX_LAUNCH_CHECK("ln_dx_kernel");
+  const int cblocks = D / 256;
+  const int nsum = dxsum ? 3 : 2;
+  int splits = std::max(1, std::min(rows / 64, current_num_sms() * 4 / cblocks));
+  while ((long long)nsum * splits * D > workspace_floats && splits > 1) splits /= 2;
+  const int rps = (rows + splits - 1) / splits;
+  ln_colsum_kernel<<<dim3(cblocks, splits), 256, 0, st>>>(x, ldx, mean, rstd, dy, lddy, dxsum ? dx : nullptr, lddx, rows,
+                                                         D, rps, workspace, f);
+  MPX_LAUNCH_CHECK("ln_colsum_kernel");
+  partials_reduce3_kernel<<<(D + 31) / 32, 256, 0, st>>>(workspace, splits, D, dgain, dbias, dxsum, f);
+  MPX_LAUNCH_CHECK("partials_reduce3_kernel");
+  return 0;
+}
+
 int mpx_colsum(int dtype, const void* x, int64_t ldx, int64_t sbx, int rows, int cols, int batches, float* workspace,
                int64_t workspace_floats, void* out, int64_t ld_out, int out_dtype, float alpha, void* stream) {
   if (!half_dtype(dtype)) return fail(MPX_EINVAL, "colsum: f16/bf16 input only");
@@ -680,8 +861,8 @@ int mpx_colsum(int dtype, const void* x, int64_t ldx, int64_t sbx, int rows, int
   dim3 grid(cblocks, splits, batches);
   colsum_partial_kernel<<<grid, 256, 0, st>>>(x, ldx, sbx, rows, cols, rps, workspace, fmt_of(dtype));
   MPX_LAUNCH_CHECK("colsum_partial_kernel");
-  colsum_final_kernel<<<ew_grid((long long)cols * batches), 256, 0, st>>>(workspace, splits, cols, batches, out, ld_out,
-                                                                         out_dtype, alpha);
+  colsum_final_kernel<<<(unsigned)(((long long)cols * batches + 31) / 32), 256, 0, st>>>(workspace, splits, cols, batches,
+                                                                                      out, ld_out, out_dtype, alpha);
   MPX_LAUNCH_CHECK("colsum_final_kernel");
   return 0;
 }

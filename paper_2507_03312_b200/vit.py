@@ -130,6 +130,15 @@ class ViTEngine:
                                             db.data_ptr(), self.ws.data_ptr(), rows, self.D, self._st()),
                  "layernorm_bwd")
 
+    def _ln_bwd2(self, x, ldx, g, mu, rs, dy, lddy, dres, dx, lddx, dg, db, dxsum, rows):
+        """LN backward + fused column sums; dxsum (or None) = colsum of dx."""
+        self._ck(self.lib.mpx_layernorm_bwd2(self.code, x.data_ptr(), ldx, g.data_ptr(), mu.data_ptr(), rs.data_ptr(),
+                                             dy.data_ptr(), lddy, dres.data_ptr() if dres is not None else None,
+                                             self.D if dres is not None else 0, dx.data_ptr(), lddx, dg.data_ptr(),
+                                             db.data_ptr(), dxsum.data_ptr() if dxsum is not None else None,
+                                             self.ws.data_ptr(), self.ws_floats, rows, self.D, self._st()),
+                 "layernorm_bwd2")
+
     def _colsum(self, x, ldx, rows, cols, out, sbx=0, batches=1, ld_out=0, alpha=1.0, out_dtype=None):
         self._ck(self.lib.mpx_colsum(self.code, x.data_ptr(), ldx, sbx, rows, cols, batches, self.ws.data_ptr(),
                                      self.ws_floats, out.data_ptr(), ld_out or cols,
@@ -236,34 +245,34 @@ class ViTEngine:
         VK.gemm(self.dlogits, hw, M=B, N=D, K=c.classes, lda=self.ldl, ldb=ldhw, out=dfeat, ldc=D)
         dX = self.dX
         xl = self.x[c.depth]
+        top_fc2b = g[f"blocks.{c.depth - 1}.fc2.b"] if c.depth else None
         if cls:
             dX.zero_()
-            self._ln_bwd(xl, S * D, p["ln_f.g"], self.muf, self.rsf, dfeat, D, None, dX, S * D, g["ln_f.g"],
-                         g["ln_f.b"], B)
+            # only the cls rows carry gradient: colsum over them = colsum(dX) = the top fc2.b grad
+            self._ln_bwd2(xl, S * D, p["ln_f.g"], self.muf, self.rsf, dfeat, D, None, dX, S * D, g["ln_f.g"],
+                          g["ln_f.b"], top_fc2b, B)
         else:
             self._ck(lib.mpx_bcast_rows(self.code, dfeat.data_ptr(), D, self.dfin.data_ptr(), D, S * D, S, B, D,
                                         1.0 / S, st), "bcast_rows")
-            self._ln_bwd(xl, D, p["ln_f.g"], self.muf, self.rsf, self.dfin, D, None, dX, D, g["ln_f.g"], g["ln_f.b"],
-                         M)
+            self._ln_bwd2(xl, D, p["ln_f.g"], self.muf, self.rsf, self.dfin, D, None, dX, D, g["ln_f.g"],
+                          g["ln_f.b"], top_fc2b, M)
         ready("head")
         scale = 1.0 / math.sqrt(hd)
         for i in reversed(range(c.depth)):
             q = f"blocks.{i}."
             # fc2: x_{i+1} = h @ W2 + b2 + xm
-            VK.linear_wgrad(self.h[i], dX, out=g[q + "fc2.w"])
-            self._colsum(dX, D, M, D, g[q + "fc2.b"])
+            VK.linear_wgrad(self.h[i], dX, out=g[q + "fc2.w"])  # fc2.b came with the LN backward above
             VK.linear_dgrad(dX, p[q + "fc2.w"], aux=self.pre[i], out=self.dpre)  # dpre = (dX W2^T) * gelu'(pre)
             # fc1: pre = bn @ W1 + b1
             VK.linear_wgrad(self.bn[i], self.dpre, out=g[q + "fc1.w"])
             self._colsum(self.dpre, c.mlp, M, c.mlp, g[q + "fc1.b"])
             VK.linear_dgrad(self.dpre, p[q + "fc1.w"], out=self.dA)
-            # LN2 (+ residual): dxm = LN2'(dA) + dX
-            self._ln_bwd(self.xm[i], D, p[q + "ln2.g"], self.mu2[i], self.rs2[i], self.dA, D, dX, self.dXm, D,
-                         g[q + "ln2.g"], g[q + "ln2.b"], M)
+            # LN2 (+ residual): dxm = LN2'(dA) + dX; colsum(dxm) = proj.b grad
+            self._ln_bwd2(self.xm[i], D, p[q + "ln2.g"], self.mu2[i], self.rs2[i], self.dA, D, dX, self.dXm, D,
+                          g[q + "ln2.g"], g[q + "ln2.b"], g[q + "proj.b"], M)
             dXm = self.dXm
             # proj: xm = O @ Wp + bp + x
             VK.linear_wgrad(self.O[i], dXm, out=g[q + "proj.w"])
-            self._colsum(dXm, D, M, D, g[q + "proj.b"])
             VK.linear_dgrad(dXm, p[q + "proj.w"], out=self.dO)
             # attention
             qkv, dqkv = self.qkv[i], self.dqkv
@@ -275,9 +284,9 @@ class ViTEngine:
             VK.linear_wgrad(self.a[i], dqkv, out=g[q + "qkv.w"])
             self._colsum(dqkv, 3 * D, M, 3 * D, g[q + "qkv.b"])
             VK.linear_dgrad(dqkv, p[q + "qkv.w"], out=self.dA)
-            # LN1 (+ residual): dX = LN1'(dA) + dXm
-            self._ln_bwd(self.x[i], D, p[q + "ln1.g"], self.mu1[i], self.rs1[i], self.dA, D, dXm, dX, D,
-                         g[q + "ln1.g"], g[q + "ln1.b"], M)
+            # LN1 (+ residual): dX = LN1'(dA) + dXm; colsum(dX) = fc2.b grad of the block below
+            self._ln_bwd2(self.x[i], D, p[q + "ln1.g"], self.mu1[i], self.rs1[i], self.dA, D, dXm, dX, D,
+                          g[q + "ln1.g"], g[q + "ln1.b"], g[f"blocks.{i - 1}.fc2.b"] if i > 0 else None, M)
             ready(f"blocks.{i}")
         # embedding: tokens = patches @ Wp + bp + pos (+ cls row)
         self._colsum(dX, S * D, B, S * D, g["pos"])  # sum over the batch
