@@ -30,11 +30,13 @@ using namespace ptx;
 constexpr int kAttnQ = 16384;      // Q tile 128 x 64 half
 constexpr int kAttnKV = 32768;     // K / V 256 x 64 half
 constexpr int kAttnP = 65536;      // P 128 x 256 half (4 K-major chunks of 64 keys)
-constexpr int kSplit = 2;          // softmax warps per TMEM lane quarter (column split)
+constexpr int kSplit = 2;          // backward: softmax warps per TMEM lane quarter (column split)
+constexpr int kSplitF = 4;         // forward (40 registers: 2 CTAs x 640 threads per SM)
 constexpr int kAttnThreads = 128 + 128 * kSplit;  // warps 0-3 control, then 4*kSplit softmax warps
+constexpr int kAttnThreadsF = 128 + 128 * kSplitF;
 // forward smem: P (64 KB) overwrites the dead Q (16 KB) + K (32 KB) tiles once
 // S = Q K^T has been computed, so two CTAs fit on one SM
-constexpr size_t kAttnSmem = 1024 + kAttnP + kAttnKV + 2 * kSplit * 128 * 4 + 256;
+constexpr size_t kAttnSmem = 1024 + kAttnP + kAttnKV + 2 * kSplitF * 128 * 4 + 256;
 
 struct AttnParams {
   int N, H, hd, m_tiles;
@@ -46,17 +48,19 @@ struct AttnParams {
 
 __device__ __forceinline__ float h2f(uint16_t h, int fmt) { return fmt ? to_f32<MPX_BF16>(h) : to_f32<MPX_F16>(h); }
 __device__ __forceinline__ uint16_t f2h(float x, int fmt) { return fmt ? from_f32<MPX_BF16>(x) : from_f32<MPX_F16>(x); }
-__device__ __forceinline__ void quarter_sync(int q) {  // the kSplit warps sharing TMEM lane quarter q
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * kSplit) : "memory");
+template <int NS>
+__device__ __forceinline__ void quarter_sync(int q) {  // the NS warps sharing TMEM lane quarter q
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * NS) : "memory");
 }
 
 // row r's softmax statistics over the keys this split handles, combined over
 // the kSplit warps of the quarter through smem: returns (m, 1/l)
+template <int NS>
 __device__ __forceinline__ void softmax_stats(uint32_t trow, int split, int r, int q, int N, float scale, int fmt,
                                               float* red, float& m_out, float& inv_out) {
   const int n_chunks = (N + 15) / 16;
   float m = -INFINITY, l = 0.f;
-  for (int c = split; c < n_chunks; c += kSplit) {
+  for (int c = split; c < n_chunks; c += NS) {
     uint32_t a[16];
     tmem_ld16(trow + c * 16, a);
     tmem_ld_wait();
@@ -74,18 +78,18 @@ __device__ __forceinline__ void softmax_stats(uint32_t trow, int split, int r, i
     m = nm;
   }
   red[split * 128 + r] = m;
-  red[kSplit * 128 + split * 128 + r] = l;
-  quarter_sync(q);
+  red[NS * 128 + split * 128 + r] = l;
+  quarter_sync<NS>(q);
   float M = -INFINITY;
 #pragma unroll
-  for (int j = 0; j < kSplit; ++j) M = fmaxf(M, red[j * 128 + r]);
+  for (int j = 0; j < NS; ++j) M = fmaxf(M, red[j * 128 + r]);
   float L = 0.f;
 #pragma unroll
-  for (int j = 0; j < kSplit; ++j) {
+  for (int j = 0; j < NS; ++j) {
     const float mj = red[j * 128 + r];
-    if (mj != -INFINITY) L += red[kSplit * 128 + j * 128 + r] * __expf(mj - M);
+    if (mj != -INFINITY) L += red[NS * 128 + j * 128 + r] * __expf(mj - M);
   }
-  quarter_sync(q);  // red[] may be reused afterwards
+  quarter_sync<NS>(q);  // red[] may be reused afterwards
   m_out = M;
   inv_out = 1.f / L;
 }
@@ -99,10 +103,11 @@ __device__ __forceinline__ void store_p_chunk(uint8_t* sP, int c, int r, const u
 }
 
 // P = exp(round(s*scale) - m) * inv for the chunks of this split (zeros past N)
+template <int NS>
 __device__ __forceinline__ void softmax_write_p(uint32_t trow, int split, int r, int N, float scale, int fmt, float m,
                                                 float inv, uint8_t* sP) {
   const int n_chunks = (N + 15) / 16;
-  for (int c = split; c < 16; c += kSplit) {
+  for (int c = split; c < 16; c += NS) {
     uint32_t pk[8];
     if (c < n_chunks) {
       uint32_t a[16];
@@ -127,7 +132,7 @@ __device__ __forceinline__ void softmax_write_p(uint32_t trow, int split, int r,
   }
 }
 
-__global__ void __launch_bounds__(kAttnThreads, 2)
+__global__ void __launch_bounds__(kAttnThreadsF, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ AttnParams P) {
   extern __shared__ uint8_t smem_raw[];
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   uint8_t* sK = smem + kAttnQ;
   uint8_t* sV = smem + kAttnP;
   float* red = reinterpret_cast<float*>(sV + kAttnKV);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * kSplit * 128);  // 0 load, 1 S, 2 P, 3 O
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * kSplitF * 128);  // 0 load, 1 S, 2 P, 3 O
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 4);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -153,7 +158,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     tma_prefetch(&tmV);
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
-    mbar_init(&bar[2], 128 * kSplit);
+    mbar_init(&bar[2], 128 * kSplitF);
     mbar_init(&bar[3], 1);
     fence_barrier_init();
   }
@@ -194,8 +199,8 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     mbar_wait(&bar[1], 0);
     tc_fence_after();
     float m, inv;
-    softmax_stats(trow, split, r, q, P.N, P.scale, P.fmt, red, m, inv);
-    softmax_write_p(trow, split, r, P.N, P.scale, P.fmt, m, inv, sP);
+    softmax_stats<kSplitF>(trow, split, r, q, P.N, P.scale, P.fmt, red, m, inv);
+    softmax_write_p<kSplitF>(trow, split, r, P.N, P.scale, P.fmt, m, inv, sP);
     fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
     tc_fence_before();
     mbar_arrive(&bar[2]);
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     tc_fence_after();
     const int qrow = m0 + r;
     uint16_t* o = static_cast<uint16_t*>(P.O) + ((long long)b * P.N + qrow) * P.ldo + (long long)h * P.hd;
-    for (int c = split; c < 4; c += kSplit) {
+    for (int c = split; c < 4; c += kSplitF) {
       uint32_t a[16];
       tmem_ld16(trow + c * 16, a);
       tmem_ld_wait();
@@ -366,8 +371,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_wait(&bar[2], ph);
       tc_fence_after();
       float m, inv;
-      softmax_stats(trow, split, r, qd, P.N, P.scale, P.fmt, red, m, inv);
-      softmax_write_p(trow, split, r, P.N, P.scale, P.fmt, m, inv, sP);
+      softmax_stats<kSplit>(trow, split, r, qd, P.N, P.scale, P.fmt, red, m, inv);
+      softmax_write_p<kSplit>(trow, split, r, P.N, P.scale, P.fmt, m, inv, sP);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&bar[3]);
@@ -385,11 +390,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int i = 0; i < 16; ++i) tsum += pv[i] * __uint_as_float(a[i]);
       }
       red[split * 128 + r] = tsum;
-      quarter_sync(qd);
+      quarter_sync<kSplit>(qd);
       tsum = 0.f;
 #pragma unroll
       for (int j = 0; j < kSplit; ++j) tsum += red[j * 128 + r];
-      quarter_sync(qd);
+      quarter_sync<kSplit>(qd);
       for (int c = split; c < 16; c += kSplit) {
         uint32_t pk[8];
         if (c < n_chunks) {
@@ -526,7 +531,7 @@ extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H
   });
   if (err != cudaSuccess) return fail((int)err, "cudaFuncSetAttribute(attn_fwd_kernel)");
   const long long grid = (long long)B * H * P.m_tiles;
-  attn_fwd_kernel<<<(unsigned)grid, kAttnThreads, kAttnSmem, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, P);
+  attn_fwd_kernel<<<(unsigned)grid, kAttnThreadsF, kAttnSmem, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, P);
   MPX_LAUNCH_CHECK("attn_fwd_kernel");
   return 0;
 }
