@@ -158,15 +158,21 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
     images = torch.randn(B, cfg.img, cfg.img, cfg.chans, generator=g, device=dev)
     labels = torch.randint(0, cfg.classes, (B,), generator=g, device=dev).to(torch.int32)
     stream = torch.cuda.current_stream(dev)
-    for _ in range(args.vit_warmup):
-        tr.step(images, labels)
+    use_graph = ws == 1 and not args.no_graph
+    if use_graph:  # the whole step as one CUDA graph (warm-up steps run inside capture())
+        tr.capture(images, labels, warmup=args.vit_warmup)
+        step = tr.replay
+    else:
+        for _ in range(args.vit_warmup):
+            tr.step(images, labels)
+        step = lambda: tr.step(images, labels)  # noqa: E731
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     K = args.vit_steps
     e0.record(stream)
     for _ in range(K):
-        loss = tr.step(images, labels)
+        loss = step()
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -179,8 +185,10 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
     h_img.copy_(images)
     h_lab = torch.empty(labels.shape, dtype=torch.int32, pin_memory=True)
     h_lab.copy_(labels)
-    d_img = [torch.empty_like(images), torch.empty_like(images)]
-    d_lab = [torch.empty_like(labels), torch.empty_like(labels)]
+    # the graph reads `images`/`labels`: land the host copies there (single
+    # buffer, the copy of step j+1 waits for step j's cast/patchify)
+    d_img = [images, images] if use_graph else [torch.empty_like(images), torch.empty_like(images)]
+    d_lab = [labels, labels] if use_graph else [torch.empty_like(labels), torch.empty_like(labels)]
     out_loss = torch.empty(K, dtype=torch.float32, pin_memory=True)
     cs = torch.cuda.Stream(dev)
     copied = [torch.cuda.Event(), torch.cuda.Event()]
@@ -193,13 +201,13 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
     for j in range(K):
         b = j % 2
         with torch.cuda.stream(cs):
-            if j >= 2:
-                cs.wait_event(consumed[b])
+            if j >= 2 or (use_graph and j >= 1):
+                cs.wait_event(consumed[(j - 1) % 2] if use_graph else consumed[b])
             d_img[b].copy_(h_img, non_blocking=True)
             d_lab[b].copy_(h_lab, non_blocking=True)
             copied[b].record(cs)
         stream.wait_event(copied[b])
-        l2 = tr.step(d_img[b], d_lab[b])
+        l2 = tr.replay() if use_graph else tr.step(d_img[b], d_lab[b])
         consumed[b].record(stream)
         out_loss[j].copy_(l2, non_blocking=True)
     s1.record(stream)
@@ -219,7 +227,8 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
                    "global_batch": B * ws, "half": args.vit_half, "loss_scaling": "dynamic, init 2^15",
                    "optimizer": "Adam lr 1e-3 (fused K4, f32 master)", "data": "synthetic N(0,1) images",
                    "parallelism": f"dp{ws}" + (" (per-block NCCL grad all-reduce overlapped with backward)"
-                                               if ws > 1 else "")},
+                                               if ws > 1 else ""),
+                   "execution": "one CUDA graph per step" if use_graph else "eager stream-ordered launches"},
         "roofline": {"bound": "tensor", "achieved": round(tflops, 1), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(tflops / peak, 4), "flops_per_image": cfg.flops_per_image(),
                      "note": "whole-step training FLOPs (3x forward GEMM+attention) / step time vs measured "
@@ -475,6 +484,7 @@ def main():
     ap.add_argument("--vit-steps", type=int, default=10)
     ap.add_argument("--vit-warmup", type=int, default=3)
     ap.add_argument("--vit-half", choices=["f16", "bf16"], default="bf16")
+    ap.add_argument("--no-graph", action="store_true", help="ViT section: eager launches instead of a CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -74,6 +74,32 @@ class ViTTrainer:
         self.mp.step()
         return loss
 
+    # ------------------------------------------------------------------
+    # CUDA graph: the step has no host sync and every scalar it branches on
+    # (finite flag, loss scale, step counter) lives on the device, so it is
+    # captured once and replayed — one launch per step instead of ~470
+    # Python/ctypes launches (and their host-side tensor-map encodes).
+    def capture(self, images: torch.Tensor, labels: torch.Tensor, warmup: int = 2):
+        """Capture step() reading from the given (static) device buffers."""
+        if self.group is not None:
+            raise RuntimeError("graph capture is single-process only (NCCL exchange runs eagerly)")
+        s = torch.cuda.Stream(self.dev)
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(s):
+            for _ in range(warmup):  # allocations (split-K workspaces) happen outside the capture
+                self.step(images, labels)
+        torch.cuda.current_stream(self.dev).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(images, labels)
+        self._graph = g
+        self._graph_inputs = (images, labels)
+        return g
+
+    def replay(self) -> torch.Tensor:
+        self._graph.replay()
+        return self.engine.loss
+
     @property
     def grads_finite(self):
         return self.mp.grads_finite
