@@ -160,7 +160,10 @@ typedef struct mpx_gemm_desc {
   void* aux;
   int64_t ld_aux;
   float alpha; /* 0 means 1 */
-  int act;     /* 0 none, 1 GELU, 2 GELU backward */
+  int act;     /* 0 none, 1 GELU, 2 GELU backward, 3 row softmax of round_half(alpha*acc)
+                  (whole rows: N <= 256 in one tile), 4 softmax backward: C = P*(alpha*acc -
+                  rowsum(P*alpha*acc)) with aux = P (ld_aux >= round_up(N, 16)); aux is
+                  addressed with C's batch strides */
   int block_n; /* 0 = auto */
   int split_k; /* <= 1: none */
   void* workspace;

@@ -42,7 +42,11 @@ constexpr int kGemmThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps
 constexpr int kGroupM = 16;
 constexpr size_t kGemmSmem = 1024 + kStages * (kATileBytes + kBTileBytes) + 8 * 4096 + 256;
 
-enum { ACT_NONE = 0, ACT_GELU = 1, ACT_GELU_BWD = 2 };
+// ACT_SOFTMAX: the tile holds whole rows (one N block, N <= 256): C = softmax
+//   over the row of round_half(alpha * acc) (f32 island, tensors.py:431-446)
+// ACT_SOFTMAX_BWD: aux = P (same layout as C); C = P * (acc - sum_row(P * acc))
+//   with acc = dP (autodiff.py:233-240)
+enum { ACT_NONE = 0, ACT_GELU = 1, ACT_GELU_BWD = 2, ACT_SOFTMAX = 3, ACT_SOFTMAX_BWD = 4 };
 
 struct GemmParams {
   int M, N, K, BN;
@@ -288,7 +292,82 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           o[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), P.ab_fmt);
         }
       };
+      // ---- softmax modes: row statistics over this warp's column groups,
+      // combined with the partner warp (same TMEM lane quarter) through smem
+      float row_m = 0.f, row_inv = 1.f, row_t = 0.f;
+      const bool smx = P.act == ACT_SOFTMAX || P.act == ACT_SOFTMAX_BWD;
+      auto round_half = [&](float x) { return half_to_f32(f32_to_half(x, P.ab_fmt), P.ab_fmt); };
+      if (smx) {
+        float m = -INFINITY, l = 0.f, tacc = 0.f;
+        for (int g = h; g * 64 < P.BN; g += 2) {
+          for (int cc = 0; cc < 4 && g * 64 + cc * 16 < P.BN; ++cc) {
+            uint32_t r[16];
+            tmem_ld16(taddr + g * 64 + cc * 16, r);
+            tmem_ld_wait();
+            const int col = n0 + g * 64 + cc * 16;
+            if (P.act == ACT_SOFTMAX) {
+              float sv[16], cm = -INFINITY;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                sv[i] = col + i < P.N ? round_half(__uint_as_float(r[i]) * P.alpha) : -INFINITY;
+                cm = fmaxf(cm, sv[i]);
+              }
+              const float nm = fmaxf(m, cm);
+              float add = 0.f;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) add += sv[i] == -INFINITY ? 0.f : __expf(sv[i] - nm);
+              l = (m == -INFINITY ? 0.f : l * __expf(m - nm)) + add;
+              m = nm;
+            } else if (row_ok && col < P.N) {
+              float pv[16];
+              const long long ai = b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ld_aux + col;
+              const uint4 w0 = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(P.aux) + ai);
+              const uint4 w1 = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(P.aux) + ai + 8);
+              const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                pv[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), P.ab_fmt);
+                pv[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), P.ab_fmt);
+              }
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (col + i < P.N) tacc += pv[i] * __uint_as_float(r[i]) * P.alpha;
+            }
+          }
+        }
+        // exchange with the partner warp through the (idle) staging buffers
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+        float* mine = reinterpret_cast<float*>(stg);
+        const float* other = reinterpret_cast<const float*>(stage_epi + ((((warp - 2) + 4) & 7) * 4096));
+        mine[lane] = m;
+        mine[32 + lane] = l;
+        mine[64 + lane] = tacc;
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+        const float om = other[lane], ol = other[32 + lane], ot = other[64 + lane];
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+        const float M = fmaxf(m, om);
+        const float L = (m == -INFINITY ? 0.f : l * __expf(m - M)) + (om == -INFINITY ? 0.f : ol * __expf(om - M));
+        row_m = M;
+        row_inv = 1.f / L;
+        row_t = tacc + ot;
+      }
+
       auto epi = [&](float* v, int col, int ncols) {
+        if (P.act == ACT_SOFTMAX) {  // v = alpha*acc: P = exp(round(v) - M) / L, 0 past N
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            v[i] = col + i < P.N ? __expf(round_half(v[i]) - row_m) * row_inv : 0.f;
+          return;
+        }
+        if (P.act == ACT_SOFTMAX_BWD) {  // v = alpha*dP: dS = P * (v - t)
+          float pv[16];
+          load8(P.aux, b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ld_aux + col, pv);
+          load8(P.aux, b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ld_aux + col + 8, pv + 8);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = col + i < P.N ? pv[i] * (v[i] - row_t) : 0.f;
+          return;
+        }
         if (P.bias) {
           float bb[16];
           if (col + 16 <= P.N) {
@@ -304,7 +383,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         if (P.act == ACT_GELU) {
           if (P.aux) {
-            uint16_t* ax = static_cast<uint16_t*>(P.aux) + (long long)row * P.ld_aux + col;
+            uint16_t* ax = static_cast<uint16_t*>(P.aux) + b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ld_aux + col;
             uint32_t pk[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -320,7 +399,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int i = 0; i < 16; ++i) v[i] = gelu_f(v[i]);
         } else if (P.act == ACT_GELU_BWD) {
           float z[16];
-          const long long ai = (long long)row * P.ld_aux + col;
+          const long long ai = b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ld_aux + col;
           load8(P.aux, ai, z);
           if (ncols == 16) load8(P.aux, ai + 8, z + 8);
 #pragma unroll
@@ -536,6 +615,13 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   const int split = g->split_k > 1 ? g->split_k : 1;
   if (split > 1 && (nb1 * nb2 != 1 || !g->workspace)) return fail(MPX_EINVAL, "mpx_gemm: split-K needs batch 1 + workspace");
   if (split > 1 && g->act != ACT_NONE) return fail(MPX_EINVAL, "mpx_gemm: split-K supports no activation");
+  if (g->act == ACT_SOFTMAX || g->act == ACT_SOFTMAX_BWD) {
+    // the epilogue needs whole rows: one N block, and 16-element aux reads
+    if (g->N > BN || split > 1 || (g->c_dtype != MPX_F16 && g->c_dtype != MPX_BF16))
+      return fail(MPX_EINVAL, "mpx_gemm: softmax epilogues need N <= 256 in one tile, 16-bit C, no split-K");
+    if (g->act == ACT_SOFTMAX_BWD && (!g->aux || g->ld_aux < (g->N + 15) / 16 * 16 || g->ld_aux % 8))
+      return fail(MPX_EINVAL, "mpx_gemm: softmax backward needs aux = P with ld_aux >= round_up(N, 16)");
+  }
   // CTA pair (M = 256 tiles) for the large problems; single CTA otherwise
   int CG = g->cta_group;
   const bool pair_ok = (BN == 256 || BN == 128) && (!g->b_mn_major || BN % 128 == 0);

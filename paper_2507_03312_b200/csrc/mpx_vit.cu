@@ -386,6 +386,98 @@ __global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restri
 }
 
 // ===========================================================================
+// K6 softmax, short rows (ld <= 256, ld % 8 == 0): R rows per warp, every
+// 16-byte load of all R rows issued before any arithmetic (memory-level
+// parallelism), one lane per 8-column chunk.
+// ===========================================================================
+template <int R>
+__global__ void __launch_bounds__(256) softmax_fwd_rows_kernel(const void* __restrict__ S, void* __restrict__ P,
+                                                               long long rows, int L, long long ld, int fmt) {
+  const int lane = threadIdx.x & 31;
+  const long long row0 = ((long long)blockIdx.x * 8 + (threadIdx.x >> 5)) * R;
+  const int c0 = lane * 8;
+  const bool act = c0 < ld;
+  uint4 w[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+    w[k] = (act && row0 + k < rows) ? *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(S) + (row0 + k) * ld + c0)
+                                    : make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (row0 + k >= rows) break;
+    float v[8];
+    unpack8(w[k], v, fmt);
+    float m = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      if (!act || c0 + e >= L) v[e] = -INFINITY;
+      m = fmaxf(m, v[e]);
+    }
+    m = warp_max(m);
+    float sum = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      v[e] = v[e] == -INFINITY ? 0.f : __expf(v[e] - m);
+      sum += v[e];
+    }
+    const float inv = 1.f / warp_sum(sum);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] *= inv;
+    if (act) *reinterpret_cast<uint4*>(static_cast<uint16_t*>(P) + (row0 + k) * ld + c0) = pack8(v, fmt);
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) softmax_bwd_rows_kernel(const void* __restrict__ S, const void* __restrict__ dP,
+                                                               void* __restrict__ dS, long long rows, int L,
+                                                               long long ld, int fmt) {
+  const int lane = threadIdx.x & 31;
+  const long long row0 = ((long long)blockIdx.x * 8 + (threadIdx.x >> 5)) * R;
+  const int c0 = lane * 8;
+  const bool act = c0 < ld;
+  uint4 ws_[R], wg[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const bool ok = act && row0 + k < rows;
+    ws_[k] = ok ? *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(S) + (row0 + k) * ld + c0)
+                : make_uint4(0, 0, 0, 0);
+    wg[k] = ok ? *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dP) + (row0 + k) * ld + c0)
+               : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (row0 + k >= rows) break;
+    float y[8], g[8];
+    unpack8(ws_[k], y, fmt);
+    unpack8(wg[k], g, fmt);
+    float m = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      if (!act || c0 + e >= L) y[e] = -INFINITY;
+      m = fmaxf(m, y[e]);
+    }
+    m = warp_max(m);
+    float sum = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      y[e] = y[e] == -INFINITY ? 0.f : __expf(y[e] - m);
+      sum += y[e];
+    }
+    const float inv = 1.f / warp_sum(sum);
+    float t = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      y[e] *= inv;
+      t += g[e] * y[e];
+    }
+    t = warp_sum(t);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) g[e] = y[e] * (g[e] - t);
+    if (act) *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dS) + (row0 + k) * ld + c0) = pack8(g, fmt);
+  }
+}
+
+// ===========================================================================
 // K6 attention softmax, register-resident rows (ld % 8 == 0, ld <= 256*CH):
 // each lane holds CH 8-element chunks; one 16-byte load and store per chunk.
 // ===========================================================================
@@ -874,7 +966,7 @@ int mpx_softmax_fwd(int dtype, const void* S, void* P, int64_t rows, int L, int6
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool vec = ld % 8 == 0 && ((reinterpret_cast<uintptr_t>(S) | reinterpret_cast<uintptr_t>(P)) % 16 == 0);
   if (vec && ld <= 256)
-    softmax_fwd_vec_kernel<1><<<grid, 256, 0, st>>>(S, P, rows, L, ld, fmt_of(dtype));
+    softmax_fwd_rows_kernel<4><<<(unsigned)((rows + 31) / 32), 256, 0, st>>>(S, P, rows, L, ld, fmt_of(dtype));
   else if (vec && ld <= 512)
     softmax_fwd_vec_kernel<2><<<grid, 256, 0, st>>>(S, P, rows, L, ld, fmt_of(dtype));
   else
@@ -891,7 +983,7 @@ int mpx_softmax_bwd(int dtype, const void* S, const void* dP, void* dS, int64_t 
   const bool vec = ld % 8 == 0 && ((reinterpret_cast<uintptr_t>(S) | reinterpret_cast<uintptr_t>(dP) |
                                     reinterpret_cast<uintptr_t>(dS)) % 16 == 0);
   if (vec && ld <= 256)
-    softmax_bwd_vec_kernel<1><<<grid, 256, 0, st>>>(S, dP, dS, rows, L, ld, fmt_of(dtype));
+    softmax_bwd_rows_kernel<4><<<(unsigned)((rows + 31) / 32), 256, 0, st>>>(S, dP, dS, rows, L, ld, fmt_of(dtype));
   else if (vec && ld <= 512)
     softmax_bwd_vec_kernel<2><<<grid, 256, 0, st>>>(S, dP, dS, rows, L, ld, fmt_of(dtype));
   else

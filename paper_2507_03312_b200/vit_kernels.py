@@ -11,7 +11,7 @@ from . import _native as _nat
 from .kernels import require_cuda, stream_handle
 
 _CODE = {torch.float32: _nat.MPX_F32, torch.float16: _nat.MPX_F16, torch.bfloat16: _nat.MPX_BF16}
-ACT_NONE, ACT_GELU, ACT_GELU_BWD = 0, 1, 2
+ACT_NONE, ACT_GELU, ACT_GELU_BWD, ACT_SOFTMAX, ACT_SOFTMAX_BWD = 0, 1, 2, 3, 4
 
 
 def _ptr(t):

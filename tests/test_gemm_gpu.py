@@ -130,3 +130,31 @@ def test_fused_attention_backward(cuda, dt, Nt):
         got = dqkv[:, i * D:(i + 1) * D]
         want = x.grad[:, i * D:(i + 1) * D]
         close(got, want, rel=3e-2)
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("Nt", [197, 64])
+def test_softmax_epilogues(cuda, dt, Nt):
+    """Q K^T with the softmax island in the epilogue, and dP = dO V^T with the
+    softmax backward in the epilogue (aux = P), batched over (head, image)."""
+    Bsz, H, hd = 2, 3, 64
+    D = H * hd
+    ld = -(-Nt // 16) * 16
+    g = torch.Generator(device=cuda).manual_seed(Nt + 3)
+    qkv = torch.randn(Bsz * Nt, 3 * D, device=cuda, generator=g).to(dt)
+    dO = torch.randn(Bsz * Nt, D, device=cuda, generator=g).to(dt)
+    P = torch.zeros(Bsz, H, Nt, ld, device=cuda, dtype=dt)
+    VK.gemm(qkv, qkv[:, D:], M=Nt, N=Nt, K=hd, lda=3 * D, ldb=3 * D, nb=(H, Bsz), a_sb=(hd, Nt * 3 * D),
+            b_sb=(hd, Nt * 3 * D), out=P, ldc=ld, c_sb=(Nt * ld, H * Nt * ld), alpha=0.125, act=VK.ACT_SOFTMAX)
+    q, k, v = (qkv.view(Bsz, Nt, 3, H, hd)[:, :, i].float() for i in range(3))
+    s = (torch.einsum("bnhd,bmhd->bhnm", q, k) * 0.125).to(dt).float()
+    p = torch.softmax(s, -1)
+    close(P[..., :Nt], p)
+    dS = torch.zeros_like(P)
+    VK.gemm(dO, qkv[:, 2 * D:], M=Nt, N=Nt, K=hd, lda=D, ldb=3 * D, nb=(H, Bsz), a_sb=(hd, Nt * D),
+            b_sb=(hd, Nt * 3 * D), out=dS, ldc=ld, c_sb=(Nt * ld, H * Nt * ld), act=VK.ACT_SOFTMAX_BWD, aux=P,
+            ld_aux=ld)
+    dp = torch.einsum("bnhd,bmhd->bhnm", dO.float().view(Bsz, Nt, H, hd), v)
+    ph = P[..., :Nt].float()
+    want = ph * (dp - (ph * dp).sum(-1, keepdim=True))
+    close(dS[..., :Nt], want, rel=2e-2)
