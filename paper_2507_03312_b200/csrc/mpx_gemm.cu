@@ -26,6 +26,7 @@
 
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 namespace mpx {
@@ -71,7 +72,9 @@ struct GemmParams {
   int act;
   float* ws;  // split-K partials [split][M][N] (f32)
   int tma_store;  // 16-bit C written through swizzled smem staging + TMA bulk stores
+  int xop;        // epilogue operand through TMA (tmX): 0 none, 1 residual in, 2 aux in (GELU'), 3 aux out (GELU)
 };
+enum { XOP_NONE = 0, XOP_RES_IN = 1, XOP_AUX_IN = 2, XOP_AUX_OUT = 3 };
 
 __device__ __forceinline__ float half_to_f32(uint16_t h, int fmt) {
   return fmt ? to_f32<MPX_BF16>(h) : to_f32<MPX_F16>(h);
@@ -119,10 +122,11 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, long long t
 // per 256-row tile: each CTA stages its 128 A rows and half of the BN B
 // columns, the leader issues tcgen05.mma.cta_group::2 (M = 256), so each SM
 // streams 2/3 of the bytes per FLOP of the 1-CTA tile.
-template <int CG>
+template <int CG, int XO>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ GemmParams P) {
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
+                const __grid_constant__ GemmParams P) {
   constexpr int S = CG == 1 ? kStages : 6;     // smem ring depth
   constexpr int BT = kBTileBytes / CG;         // B bytes per stage per CTA
   extern __shared__ uint8_t smem_raw[];
@@ -134,7 +138,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ebar = tempty + 2;  // per epilogue warp: its operand tile has landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 8);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -146,6 +151,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if (P.tma_store) tma_prefetch(&tmC);
+    if (XO != XOP_NONE) tma_prefetch(&tmX);
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -154,6 +160,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 256 * CG);
     }
+    for (int i = 0; i < 8; ++i) mbar_init(&ebar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -269,6 +276,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int h = (warp - 2) >> 2;
     uint8_t* stg = stage_epi + (warp - 2) * 4096;  // 32 rows x 128 B, 128B-swizzled
+    uint32_t eph = 0;  // phase of this warp's operand barrier
     int acc = 0;
     uint32_t acc_phase = 0;
     for (long long t = t_first; t < P.total_tiles; t += t_step) {
@@ -353,7 +361,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         row_t = tacc + ot;
       }
 
-      auto epi = [&](float* v, int col, int ncols) {
+      // xin: the 16 staged operand values of this chunk (TMA operand path) or unused
+      auto epi = [&](float* v, int col, int ncols, const float* xin) {
         if (P.act == ACT_SOFTMAX) {  // v = alpha*acc: P = exp(round(v) - M) / L, 0 past N
 #pragma unroll
           for (int i = 0; i < 16; ++i)
@@ -381,7 +390,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += bb[i];
         }
-        if (P.act == ACT_GELU) {
+        if (P.act == ACT_GELU && XO == XOP_AUX_OUT) {
+          // bias only here; the staged aux store and the GELU happen in the caller
+        } else if (P.act == ACT_GELU) {
           if (P.aux) {
             uint16_t* ax = static_cast<uint16_t*>(P.aux) + b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ld_aux + col;
             uint32_t pk[8];
@@ -399,13 +410,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int i = 0; i < 16; ++i) v[i] = gelu_f(v[i]);
         } else if (P.act == ACT_GELU_BWD) {
           float z[16];
-          const long long ai = b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ld_aux + col;
-          load8(P.aux, ai, z);
-          if (ncols == 16) load8(P.aux, ai + 8, z + 8);
+          if (XO == XOP_AUX_IN) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) z[i] = xin[i];
+          } else {
+            const long long ai = b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ld_aux + col;
+            load8(P.aux, ai, z);
+            if (ncols == 16) load8(P.aux, ai + 8, z + 8);
+          }
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] *= gelu_grad_f(z[i]);
         }
-        if (P.res) {
+        if (P.res && XO == XOP_RES_IN) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += xin[i];
+        } else if (P.res) {
           float rr[16];
           const long long ri = b1 * P.r_sb1 + b2 * P.r_sb2 + (long long)row * P.ldr + col;
           load8(P.res, ri, rr);
@@ -424,9 +443,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int nch = min(GW / 16, (P.BN - g * GW) / 16);
           if (lane == 0) bulk_wait_read0();  // the previous TMA store has read the staging buffer
           __syncwarp();
+          uint8_t* rowp = stg + lane * 128;
+          const int sw = lane & 7;
+          if (XO == XOP_RES_IN || XO == XOP_AUX_IN) {  // operand tile -> staging by TMA
+            if (lane == 0) {
+              mbar_arrive_expect_tx(&ebar[warp - 2], 4096);
+              const int xb1 = XO == XOP_RES_IN && P.r_sb1 == 0 ? 0 : b1;
+              const int xb2 = XO == XOP_RES_IN && P.r_sb2 == 0 ? 0 : b2;
+              tma_load_4d(stg, &tmX, &ebar[warp - 2], n0 + g * GW, row0, xb1, xb2);
+            }
+            mbar_wait(&ebar[warp - 2], eph);
+            eph ^= 1u;
+          }
 #pragma unroll
           for (int pair = 0; pair < 2; ++pair) {  // two 16-column chunks per TMEM round trip
-            if (pair * 2 >= nch) break;
+            if (pair * 2 >= nch) continue;
             uint32_t r[2][16];
 #pragma unroll
             for (int k = 0; k < 2; ++k)
@@ -435,24 +466,64 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const int cc = pair * 2 + k;
-              if (cc >= nch) break;
+              if (cc >= nch) continue;
               float v[16];
 #pragma unroll
               for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[k][i]) * P.alpha;
               const int col = n0 + g * GW + cc * 16;
-              uint8_t* rowp = stg + lane * 128;
-              const int sw = lane & 7;
               if (f32out) {  // raw (split-K partial) or f32 output: 4 x 16 B per chunk
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
                   *reinterpret_cast<float4*>(rowp + (((4 * cc + j) ^ sw) << 4)) =
                       make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
               } else {
-                if (row_ok && col < P.N_store) epi(v, col, min(16, P.N_store - col));
-                uint32_t pk[8];
+                float xv[16];
+                if (XO == XOP_RES_IN || XO == XOP_AUX_IN) {  // own row of the staged operand
+                  const uint4 w0 = *reinterpret_cast<const uint4*>(rowp + (((2 * cc) ^ sw) << 4));
+                  const uint4 w1 = *reinterpret_cast<const uint4*>(rowp + (((2 * cc + 1) ^ sw) << 4));
+                  const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                  pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], cf);
+                  for (int e = 0; e < 8; ++e) {
+                    xv[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), P.ab_fmt);
+                    xv[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), P.ab_fmt);
+                  }
+                }
+                if (row_ok && col < P.N_store) epi(v, col, min(16, P.N_store - col), xv);
+                uint32_t pk[8];
+                if (XO == XOP_AUX_OUT) {  // stage the rounded pre-activation (aux), keep it for GELU
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], P.ab_fmt);
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], cf);
+                }
+                *reinterpret_cast<uint4*>(rowp + (((2 * cc) ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                *reinterpret_cast<uint4*>(rowp + (((2 * cc + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+              }
+            }
+          }
+          if (XO == XOP_AUX_OUT) {  // store aux, then reuse the staging for GELU(pre)
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_4d(&tmX, stg, n0 + g * GW, row0, b1, b2);
+              bulk_commit();
+              bulk_wait_read0();
+            }
+            __syncwarp();
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              if (cc < nch) {
+                // the rounded pre-activations are still in this lane's staging row
+                const uint4 w0 = *reinterpret_cast<const uint4*>(rowp + (((2 * cc) ^ sw) << 4));
+                const uint4 w1 = *reinterpret_cast<const uint4*>(rowp + (((2 * cc + 1) ^ sw) << 4));
+                uint32_t pk[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const float a = half_to_f32((uint16_t)(pk[i] & 0xFFFFu), P.ab_fmt);
+                  const float b = half_to_f32((uint16_t)(pk[i] >> 16), P.ab_fmt);
+                  pk[i] = pack2_fmt(gelu_f(a), gelu_f(b), cf);
+                }
                 *reinterpret_cast<uint4*>(rowp + (((2 * cc) ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 *reinterpret_cast<uint4*>(rowp + (((2 * cc + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
               }
@@ -487,7 +558,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               *reinterpret_cast<float4*>(w + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
             continue;
           }
-          epi(v, col, ncols);
+          epi(v, col, ncols, v);  // (no staged operand on the direct path)
           const long long off = b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ldc + col;
           if (P.c_dtype == MPX_F32) {
             float* o = static_cast<float*>(P.C) + off;
@@ -720,18 +791,49 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
     }
   }
 
+  // epilogue operand (residual in / GELU aux in / GELU aux out) through TMA when possible
+  CUtensorMap tx = tb;
+  P.xop = XOP_NONE;
+  static const bool no_xop = getenv("MPX_GEMM_NO_XOP") != nullptr;  // debugging switch
+  if (P.tma_store && split == 1 && g->c_dtype != MPX_F32 && g->tma_store >= 0 && !no_xop) {
+    const uint64_t es2 = 2;
+    auto al16 = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+    if ((g->act == ACT_GELU || g->act == ACT_GELU_BWD) && g->aux && al16(g->aux) && g->ld_aux % 8 == 0 &&
+        (nb1 == 1 || (g->c_sb1 > 0 && g->c_sb1 % 8 == 0)) && (nb2 == 1 || (g->c_sb2 > 0 && g->c_sb2 % 8 == 0))) {
+      const uint64_t s_m = (uint64_t)g->ld_aux * es2;
+      rc = make_map(&tx, g->aux, fmt, g->N, g->M, nb1, nb2, s_m, nb1 > 1 ? (uint64_t)g->c_sb1 * es2 : s_m * g->M,
+                    nb2 > 1 ? (uint64_t)g->c_sb2 * es2 : s_m * g->M, 64, 32);
+      if (rc) return rc;
+      P.xop = g->act == ACT_GELU ? XOP_AUX_OUT : XOP_AUX_IN;
+    } else if (g->act == ACT_NONE && g->residual && al16(g->residual) && g->ldr % 8 == 0 &&
+               (nb1 == 1 || g->r_sb1 == 0 || g->r_sb1 % 8 == 0) && (nb2 == 1 || g->r_sb2 == 0 || g->r_sb2 % 8 == 0)) {
+      const uint64_t s_m = (uint64_t)g->ldr * es2;
+      rc = make_map(&tx, g->residual, fmt, g->N, g->M, ext(g->r_sb1, nb1), ext(g->r_sb2, nb2), s_m,
+                    g->r_sb1 > 0 ? (uint64_t)g->r_sb1 * es2 : s_m * g->M,
+                    g->r_sb2 > 0 ? (uint64_t)g->r_sb2 * es2 : s_m * g->M, 64, 32);
+      if (rc) return rc;
+      P.xop = XOP_RES_IN;
+    }
+  }
+
+  using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                           const GemmParams);
+  static const KernelFn kernels[2][4] = {
+      {gemm_kernel<1, XOP_NONE>, gemm_kernel<1, XOP_RES_IN>, gemm_kernel<1, XOP_AUX_IN>, gemm_kernel<1, XOP_AUX_OUT>},
+      {gemm_kernel<2, XOP_NONE>, gemm_kernel<2, XOP_RES_IN>, gemm_kernel<2, XOP_AUX_IN>, gemm_kernel<2, XOP_AUX_OUT>}};
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+    for (int c = 0; c < 2 && attr_err == cudaSuccess; ++c)
+      for (int x = 0; x < 4 && attr_err == cudaSuccess; ++x)
+        attr_err = cudaFuncSetAttribute(kernels[c][x], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
   });
   if (attr_err != cudaSuccess) return fail((int)attr_err, "cudaFuncSetAttribute(gemm_kernel)");
+  const KernelFn kern = kernels[CG - 1][P.xop];
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (CG == 1) {
     const long long grid = std::min<long long>(P.total_tiles, current_num_sms());
-    gemm_kernel<1><<<(unsigned)grid, kGemmThreads, kGemmSmem, st>>>(ta, tb, tc, P);
+    kern<<<(unsigned)grid, kGemmThreads, kGemmSmem, st>>>(ta, tb, tc, tx, P);
   } else {
     const long long pairs = std::min<long long>(P.total_tiles, current_num_sms() / 2);
     cudaLaunchConfig_t cfg{};
@@ -746,7 +848,7 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    MPX_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_kernel<2>, ta, tb, tc, P));
+    MPX_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, P));
   }
   MPX_LAUNCH_CHECK("gemm_kernel");
   if (split > 1) {
