@@ -214,14 +214,17 @@ int mpx_cross_entropy_bwd(int dtype, const void* logits, int64_t ld, const int32
  * O[b*N + n, h*hd + :] = softmax(round(Q K^T * scale)) V for every image b and
  * head h, reading Q/K/V straight from qkv [B, N, 3, H, hd]; scores live in
  * TMEM, probabilities in shared memory — nothing N x N reaches HBM.
- * Requires hd == 64 and N <= 256 (ViT-B/16, ViT-L/16: N = 197). */
+ * Requires hd == 64 and N <= 256 (ViT-B/16, ViT-L/16: N = 197).  row_stats
+ * (nullable, f32 [B*H*ceil(N/128)*128*2]) receives each query row's softmax
+ * (max, 1/sum) for mpx_attention_bwd. */
 int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H, int hd, float scale, void* O, int64_t ldo,
-                      void* stream);
+                      float* row_stats, void* stream);
 /* K6 fused attention backward: given qkv and dO [B*N, H*hd], writes the whole
  * dqkv [B*N, 3*H*hd] (dQ = scale dS K, dK = scale dS^T Q, dV = P^T dO with
- * dS = P (dP - rowsum(P dP)), dP = dO V^T, P recomputed on chip). */
+ * dS = P (dP - rowsum(P dP)), dP = dO V^T, P recomputed on chip — from the
+ * forward's row_stats when given, else from the scores here; same P bits). */
 int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int B, int N, int H, int hd, float scale,
-                      void* dqkv, void* stream);
+                      void* dqkv, const float* row_stats, void* stream);
 /* image [B,H,W,C] -> patch rows [B*(H/P)*(W/P), P*P*C], order (py, px, c) */
 int mpx_patchify(int dtype, const void* img, void* patches, int B, int H, int W, int C, int P, void* stream);
 /* strided row copy dst[b][r][c] = src[b][r][c] */

@@ -30,7 +30,7 @@ using namespace ptx;
 constexpr int kAttnQ = 16384;      // Q tile 128 x 64 half
 constexpr int kAttnKV = 32768;     // K / V 256 x 64 half
 constexpr int kAttnP = 65536;      // P 128 x 256 half (4 K-major chunks of 64 keys)
-constexpr int kSplit = 2;          // backward: softmax warps per TMEM lane quarter (column split)
+constexpr int kSplit = 4;          // backward: softmax warps per TMEM lane quarter (column split)
 constexpr int kSplitF = 4;         // forward (40 registers: 2 CTAs x 640 threads per SM)
 constexpr int kAttnThreads = 128 + 128 * kSplit;  // warps 0-3 control, then 4*kSplit softmax warps
 constexpr int kAttnThreadsF = 128 + 128 * kSplitF;
@@ -44,6 +44,7 @@ struct AttnParams {
   int fmt;  // 0 f16, 1 bf16
   void* O;
   long long ldo;  // O row stride (elements); head h at column h*hd
+  float2* stats;  // optional [(b*H + h)*m_tiles*128 + row] = (row max, 1 / row sum) for the backward
 };
 
 __device__ __forceinline__ float h2f(uint16_t h, int fmt) { return fmt ? to_f32<MPX_BF16>(h) : to_f32<MPX_F16>(h); }
@@ -132,6 +133,164 @@ __device__ __forceinline__ void softmax_write_p(uint32_t trow, int split, int r,
   }
 }
 
+__device__ __forceinline__ void unpack2(uint32_t pk, int fmt, float& lo, float& hi) {
+  if (fmt) {
+    lo = __uint_as_float(pk << 16);
+    hi = __uint_as_float(pk & 0xFFFF0000u);
+  } else {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&pk));
+    lo = f.x;
+    hi = f.y;
+  }
+}
+// the 16 scores of a TMEM chunk, scaled and rounded to the half format (the
+// reference's score dtype) with paired conversions
+__device__ __forceinline__ void round_scores16(const uint32_t* a, float scale, int fmt, float* sv) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    unpack2(pack2_fmt(__uint_as_float(a[2 * i]) * scale, __uint_as_float(a[2 * i + 1]) * scale, fmt), fmt,
+            sv[2 * i], sv[2 * i + 1]);
+}
+
+// Forward softmax of row r over the chunks c = split, split + NS, ... < n_chunks:
+//   pass 1  row max of the rounded scores (no exponentials)
+//   pass 2  e = exp(s - M), row sum; e goes back into the same TMEM columns
+//   pass 3  P = e / L rounded to half, into the K-major P tile
+// One exponential per score; the masked tail (keys >= N) only in the last chunk.
+template <int NS>
+__device__ __forceinline__ void softmax_fwd_p(uint32_t trow, int split, int r, int q, int N, float scale, int fmt,
+                                              float* red, uint8_t* sP, float2* stats) {
+  constexpr float kLog2e = 1.4426950408889634f;
+  const int n_chunks = (N + 15) / 16;
+  const int tail = N - (n_chunks - 1) * 16;  // valid keys in the last chunk (1..16)
+  float m = -INFINITY;
+  for (int c = split; c < n_chunks; c += NS) {
+    uint32_t a[16];
+    tmem_ld16(trow + c * 16, a);
+    tmem_ld_wait();
+    float sv[16];
+    round_scores16(a, scale, fmt, sv);
+    if (c == n_chunks - 1) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (i >= tail) sv[i] = -INFINITY;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) m = fmaxf(m, sv[i]);
+  }
+  red[split * 128 + r] = m;
+  quarter_sync<NS>(q);
+  float M = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < NS; ++j) M = fmaxf(M, red[j * 128 + r]);
+  const float ml = M * kLog2e;
+  float l = 0.f;
+  for (int c = split; c < n_chunks; c += NS) {
+    uint32_t a[16];
+    tmem_ld16(trow + c * 16, a);
+    tmem_ld_wait();
+    float sv[16];
+    round_scores16(a, scale, fmt, sv);
+    const int lim = c == n_chunks - 1 ? tail : 16;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float e = i < lim ? ex2_approx(fmaf(sv[i], kLog2e, -ml)) : 0.f;
+      l += e;
+      a[i] = __float_as_uint(e);
+    }
+    tmem_st16(trow + c * 16, a);
+  }
+  red[NS * 128 + split * 128 + r] = l;
+  quarter_sync<NS>(q);
+  float L = 0.f;
+#pragma unroll
+  for (int j = 0; j < NS; ++j) L += red[NS * 128 + j * 128 + r];
+  const float inv = 1.f / L;
+  if (stats != nullptr && split == 0) *stats = make_float2(M, inv);
+  tmem_st_wait();
+  for (int c = split; c < n_chunks; c += NS) {
+    uint32_t a[16];
+    tmem_ld16(trow + c * 16, a);
+    tmem_ld_wait();
+    uint32_t pk[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * inv, __uint_as_float(a[2 * i + 1]) * inv, fmt);
+    store_p_chunk(sP, c, r, pk);
+  }
+}
+
+// Backward: P_t of row r recomputed exactly as the forward wrote it — from
+// the forward's (M, 1/L) when given, else from two statistics passes here.
+template <int NS>
+__device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, int q, int N, float scale, int fmt,
+                                              float* red, uint8_t* sP, const float2* stats) {
+  constexpr float kLog2e = 1.4426950408889634f;
+  const int n_chunks = (N + 15) / 16;
+  const int tail = N - (n_chunks - 1) * 16;
+  float M, inv;
+  if (stats != nullptr) {
+    const float2 st = *stats;
+    M = st.x;
+    inv = st.y;
+  } else {
+    float m = -INFINITY;
+    for (int c = split; c < n_chunks; c += NS) {
+      uint32_t a[16];
+      tmem_ld16(trow + c * 16, a);
+      tmem_ld_wait();
+      float sv[16];
+      round_scores16(a, scale, fmt, sv);
+      const int lim = c == n_chunks - 1 ? tail : 16;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (i < lim) m = fmaxf(m, sv[i]);
+    }
+    red[split * 128 + r] = m;
+    quarter_sync<NS>(q);
+    M = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) M = fmaxf(M, red[j * 128 + r]);
+    quarter_sync<NS>(q);  // one scratch row set (the backward's smem is full)
+    const float ml = M * kLog2e;
+    float l = 0.f;
+    for (int c = split; c < n_chunks; c += NS) {
+      uint32_t a[16];
+      tmem_ld16(trow + c * 16, a);
+      tmem_ld_wait();
+      float sv[16];
+      round_scores16(a, scale, fmt, sv);
+      const int lim = c == n_chunks - 1 ? tail : 16;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (i < lim) l += ex2_approx(fmaf(sv[i], kLog2e, -ml));
+    }
+    red[split * 128 + r] = l;
+    quarter_sync<NS>(q);
+    float L = 0.f;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) L += red[j * 128 + r];
+    quarter_sync<NS>(q);  // red[] is reused by the caller
+    inv = 1.f / L;
+  }
+  const float ml = M * kLog2e;
+  for (int c = split; c < n_chunks; c += NS) {
+    uint32_t a[16];
+    tmem_ld16(trow + c * 16, a);
+    tmem_ld_wait();
+    float sv[16];
+    round_scores16(a, scale, fmt, sv);
+    const int lim = c == n_chunks - 1 ? tail : 16;
+    uint32_t pk[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float e0 = 2 * i < lim ? ex2_approx(fmaf(sv[2 * i], kLog2e, -ml)) : 0.f;
+      const float e1 = 2 * i + 1 < lim ? ex2_approx(fmaf(sv[2 * i + 1], kLog2e, -ml)) : 0.f;
+      pk[i] = pack2_fmt(e0 * inv, e1 * inv, fmt);
+    }
+    store_p_chunk(sP, c, r, pk);
+  }
+}
+
 __global__ void __launch_bounds__(kAttnThreadsF, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ AttnParams P) {
@@ -176,7 +335,8 @@ __global__ void __launch_bounds__(kAttnThreadsF, 2)
       tma_load_4d(sV, &tmV, &bar[0], 0, 0, h, b);
       mbar_wait(&bar[0], 0);
       tc_fence_after();
-      const uint32_t idesc1 = idesc_f16(P.fmt, 128, 256, 0, 0);
+      const int n_chunks = (P.N + 15) / 16;
+      const uint32_t idesc1 = idesc_f16(P.fmt, 128, 16 * n_chunks, 0, 0);  // keys past N: never computed
       const uint32_t q = smem_u32(sQ), k = smem_u32(sK);
 #pragma unroll
       for (int s = 0; s < 4; ++s)  // S = Q K^T into TMEM cols 0-255
@@ -186,8 +346,7 @@ __global__ void __launch_bounds__(kAttnThreadsF, 2)
       tc_fence_after();
       const uint32_t idesc2 = idesc_f16(P.fmt, 128, 64, 0, 1);
       const uint32_t p = smem_u32(sP), v = smem_u32(sV);
-#pragma unroll
-      for (int s = 0; s < 16; ++s)  // O = P V into TMEM cols 0-63 (S is consumed)
+      for (int s = 0; s < n_chunks; ++s)  // O = P V into TMEM cols 0-63 (S is consumed)
         umma_f16(tmem, sw128_desc(p + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
                  sw128_desc(v + s * 2048, 8192, 1024), idesc2, s > 0);
       umma_commit(&bar[3]);
@@ -198,9 +357,8 @@ __global__ void __launch_bounds__(kAttnThreadsF, 2)
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     mbar_wait(&bar[1], 0);
     tc_fence_after();
-    float m, inv;
-    softmax_stats<kSplitF>(trow, split, r, q, P.N, P.scale, P.fmt, red, m, inv);
-    softmax_write_p<kSplitF>(trow, split, r, P.N, P.scale, P.fmt, m, inv, sP);
+    float2* st = P.stats ? P.stats + ((long long)bh * P.m_tiles + mt) * 128 + r : nullptr;
+    softmax_fwd_p<kSplitF>(trow, split, r, q, P.N, P.scale, P.fmt, red, sP, st);
     fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
     tc_fence_before();
     mbar_arrive(&bar[2]);
@@ -242,7 +400,7 @@ __global__ void __launch_bounds__(kAttnThreadsF, 2)
 // 224 KB of tiles + 2 KB reduction scratch + barriers: the alignment slack is
 // trimmed to fit the 227 KB limit (the dynamic window starts 1 KB-aligned when
 // the kernel has no static shared memory; checked at run time)
-constexpr size_t kAttnBwdBody = 2 * kAttnQ + 2 * kAttnKV + 2 * kAttnP + 2 * kSplit * 128 * 4 + 128;
+constexpr size_t kAttnBwdBody = 2 * kAttnQ + 2 * kAttnKV + 2 * kAttnP + kSplit * 128 * 4 + 128;
 constexpr size_t kAttnBwdSmem = 232448;
 static_assert(kAttnBwdBody <= kAttnBwdSmem, "attention backward tiles exceed shared memory");
 
@@ -252,6 +410,7 @@ struct AttnBwdParams {
   int fmt;
   void* dqkv;  // [B*N, 3*H*hd]
   long long ld;
+  const float2* stats;  // the forward's row statistics, or null (recomputed here)
 };
 
 __global__ void __launch_bounds__(kAttnThreads, 1)
@@ -269,7 +428,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* sdS = sP + kAttnP;
   // 0 kv, 1 q/dO, 2 S, 3 P, 4 dP, 5 dS, 6 dQ(+dV,dK), 7 dQ read
   float* red = reinterpret_cast<float*>(sdS + kAttnP);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * kSplit * 128);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + kSplit * 128);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -301,7 +460,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tma_load_4d(sdO, &tmdO, &bar[1], 0, 0, h, b);
       const uint32_t q = smem_u32(sQ), dO = smem_u32(sdO), k = smem_u32(sK), v = smem_u32(sV);
       const uint32_t pp = smem_u32(sP), ds = smem_u32(sdS);
-      const uint32_t id_nk = idesc_f16(P.fmt, 128, 256, 0, 0);  // [128 x 256] = X[128 x 64] Y[256 x 64]^T
+      const int n_chunks = (P.N + 15) / 16;
+      const int halves = P.N > 128 ? 2 : 1;
+      // [128 x 16 n_chunks] = X[128 x 64] Y[keys x 64]^T: keys past N are never computed
+      const uint32_t id_nk = idesc_f16(P.fmt, 128, 16 * n_chunks, 0, 0);
       const uint32_t id_kv = idesc_f16(P.fmt, 128, 64, 1, 1);   // dV / dK halves: A, B MN-major
       const uint32_t id_q = idesc_f16(P.fmt, 128, 64, 0, 1);    // dQ: A K-major, B MN-major
       mbar_wait(&bar[0], 0);
@@ -322,8 +484,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         umma_commit(&bar[4]);
         mbar_wait(&bar[5], ph);  // dS_t written (dP consumed)
         tc_fence_after();
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
+        for (int half = 0; half < halves; ++half) {
 #pragma unroll
           for (int s = 0; s < 8; ++s) {  // over the 128 queries of the tile
             const uint64_t bdo = sw128_desc(dO + s * 2048, 8192, 1024);
@@ -334,8 +495,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                      (t > 0 || s > 0));  // dK += dS^T Q
           }
         }
-#pragma unroll
-        for (int s = 0; s < 16; ++s)  // dQ = dS K
+        for (int s = 0; s < n_chunks; ++s)  // dQ = dS K
           umma_f16(tmem, sw128_desc(ds + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024), sw128_desc(k + s * 2048, 8192, 1024),
                    id_q, s > 0);
         umma_commit(&bar[6]);
@@ -360,43 +520,28 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint4 w1 = *reinterpret_cast<const uint4*>(rowp + (((u0 + 1) ^ sw) << 4));
       const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        pv[2 * i] = h2f((uint16_t)(u[i] & 0xFFFFu), P.fmt);
-        pv[2 * i + 1] = h2f((uint16_t)(u[i] >> 16), P.fmt);
-      }
+      for (int i = 0; i < 8; ++i) unpack2(u[i], P.fmt, pv[2 * i], pv[2 * i + 1]);
     };
+    constexpr int kMaxC = 16 / kSplit;  // chunks per thread
     for (int t = 0; t < T; ++t) {
       const uint32_t ph = t & 1;
       // ---- P = softmax(round(S * scale)) -> smem (as in the forward)
       mbar_wait(&bar[2], ph);
       tc_fence_after();
-      float m, inv;
-      softmax_stats<kSplit>(trow, split, r, qd, P.N, P.scale, P.fmt, red, m, inv);
-      softmax_write_p<kSplit>(trow, split, r, P.N, P.scale, P.fmt, m, inv, sP);
+      const float2* st = P.stats ? P.stats + ((long long)blockIdx.x * T + t) * 128 + r : nullptr;
+      softmax_bwd_p<kSplit>(trow, split, r, qd, P.N, P.scale, P.fmt, red, sP, st);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&bar[3]);
-      // ---- dS = P * (dP - sum(P * dP)) -> smem
+      // ---- dS = P * (dP - sum(P * dP)) -> smem; dP rounded to the half
+      // format first (the reference's dP is a half GEMM output), kept packed
       mbar_wait(&bar[4], ph);
       tc_fence_after();
+      uint32_t dpk[kMaxC][8];
       float tsum = 0.f;
-      for (int c = split; c < n_chunks; c += kSplit) {
-        uint32_t a[16];
-        float pv[16];
-        tmem_ld16(trow + c * 16, a);
-        read_p(c, pv);
-        tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) tsum += pv[i] * __uint_as_float(a[i]);
-      }
-      red[split * 128 + r] = tsum;
-      quarter_sync<kSplit>(qd);
-      tsum = 0.f;
-#pragma unroll
-      for (int j = 0; j < kSplit; ++j) tsum += red[j * 128 + r];
-      quarter_sync<kSplit>(qd);
-      for (int c = split; c < 16; c += kSplit) {
-        uint32_t pk[8];
+      for (int j = 0; j < kMaxC; ++j) {
+        const int c = split + j * kSplit;
         if (c < n_chunks) {
           uint32_t a[16];
           float pv[16];
@@ -405,15 +550,35 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float d0 = pv[2 * i] * (__uint_as_float(a[2 * i]) - tsum);
-            const float d1 = pv[2 * i + 1] * (__uint_as_float(a[2 * i + 1]) - tsum);
-            pk[i] = pack2_fmt(d0, d1, P.fmt);
+            dpk[j][i] = pack2_fmt(__uint_as_float(a[2 * i]), __uint_as_float(a[2 * i + 1]), P.fmt);
+            float d0, d1;
+            unpack2(dpk[j][i], P.fmt, d0, d1);
+            tsum += pv[2 * i] * d0;
+            tsum += pv[2 * i + 1] * d1;
           }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) pk[i] = 0u;
         }
-        store_p_chunk(sdS, c, r, pk);
+      }
+      red[split * 128 + r] = tsum;
+      quarter_sync<kSplit>(qd);
+      tsum = 0.f;
+#pragma unroll
+      for (int j = 0; j < kSplit; ++j) tsum += red[j * 128 + r];
+      quarter_sync<kSplit>(qd);
+#pragma unroll
+      for (int j = 0; j < kMaxC; ++j) {
+        const int c = split + j * kSplit;
+        if (c < n_chunks) {
+          float pv[16];
+          read_p(c, pv);
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float d0, d1;
+            unpack2(dpk[j][i], P.fmt, d0, d1);
+            pk[i] = pack2_fmt(pv[2 * i] * (d0 - tsum), pv[2 * i + 1] * (d1 - tsum), P.fmt);
+          }
+          store_p_chunk(sdS, c, r, pk);
+        }
       }
       fence_async_smem();
       tc_fence_before();
@@ -504,7 +669,7 @@ static int qkv_map(CUtensorMap* m, const void* base, int fmt, int N, int H, int 
 using namespace mpx;
 
 extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H, int hd, float scale, void* O,
-                                 int64_t ldo, void* stream) {
+                                 int64_t ldo, float* row_stats, void* stream) {
   if (dtype != MPX_F16 && dtype != MPX_BF16) return fail(MPX_EINVAL, "attention: f16/bf16 only");
   if (hd != 64 || N < 1 || N > 256) return fail(MPX_EINVAL, "attention_fwd: fused path needs hd == 64, N <= 256");
   const int fmt = dtype == MPX_BF16 ? 1 : 0;
@@ -524,6 +689,7 @@ extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H
   P.fmt = fmt;
   P.O = O;
   P.ldo = ldo;
+  P.stats = reinterpret_cast<float2*>(row_stats);
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
@@ -537,7 +703,7 @@ extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H
 }
 
 extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int B, int N, int H, int hd, float scale,
-                                 void* dqkv, void* stream) {
+                                 void* dqkv, const float* row_stats, void* stream) {
   if (dtype != MPX_F16 && dtype != MPX_BF16) return fail(MPX_EINVAL, "attention: f16/bf16 only");
   if (hd != 64 || N < 1 || N > 256) return fail(MPX_EINVAL, "attention_bwd: fused path needs hd == 64, N <= 256");
   const int fmt = dtype == MPX_BF16 ? 1 : 0;
@@ -558,6 +724,7 @@ extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int
   P.fmt = fmt;
   P.dqkv = dqkv;
   P.ld = 3LL * D;
+  P.stats = reinterpret_cast<const float2*>(row_stats);
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {

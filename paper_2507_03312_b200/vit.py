@@ -65,13 +65,15 @@ class ViTEngine:
         self.a = [e(M, D) for _ in range(c.depth)]  # LN1 out
         self.qkv = [e(M, 3 * D) for _ in range(c.depth)]
         # fused attention (K6, mpx_attn.cu) keeps scores/probabilities on chip
-        # (hd == 64, N <= 256); it is opt-in (MPX_FUSED_ATTENTION=1) until its
-        # phases are pipelined — today the unfused path (tcgen05 GEMM + f32
-        # softmax island + GEMM, S/P round-tripping HBM) is faster end to end
-        self.fused_attn = (self.hd == 64 and S <= 256 and os.environ.get("MPX_FUSED_ATTENTION", "0") == "1")
+        # (hd == 64, N <= 256); MPX_FUSED_ATTENTION=0 selects the unfused path
+        # (tcgen05 GEMM + f32 softmax island + GEMM, S/P round-tripping HBM)
+        self.fused_attn = (self.hd == 64 and S <= 256 and os.environ.get("MPX_FUSED_ATTENTION", "1") == "1")
         if not self.fused_attn:
             self.Sm = [e(B * H * S, self.ldS) for _ in range(c.depth)]  # scaled scores
             self.P = [e(B * H * S, self.ldS) for _ in range(c.depth)]
+        else:  # per-row softmax statistics saved by the forward for the backward
+            self.attn_stats = [torch.empty(VK.attention_stats_numel(B, S, H), dtype=torch.float32, device=self.dev)
+                               for _ in range(c.depth)]
         self.O = [e(M, D) for _ in range(c.depth)]
         self.xm = [e(M, D) for _ in range(c.depth)]  # after attention residual
         self.bn = [e(M, D) for _ in range(c.depth)]  # LN2 out
@@ -169,7 +171,7 @@ class ViTEngine:
             VK.linear_fwd(a, p[q + "qkv.w"], bias=p[q + "qkv.b"], out=qkv)
             O = self.O[i]
             if self.fused_attn:
-                VK.attention_fwd(qkv, B, S, H, hd, scale, out=O)
+                VK.attention_fwd(qkv, B, S, H, hd, scale, out=O, stats=self.attn_stats[i])
             else:
                 Sm, P_ = self.Sm[i], self.P[i]
                 VK.gemm(qkv, qkv[:, D:], M=S, N=S, K=hd, lda=3 * D, ldb=3 * D, nb=(H, B), a_sb=(hd, S * 3 * D),
@@ -277,7 +279,7 @@ class ViTEngine:
             # attention
             qkv, dqkv = self.qkv[i], self.dqkv
             if self.fused_attn:
-                VK.attention_bwd(qkv, self.dO, B, S, H, hd, scale, dqkv=dqkv)
+                VK.attention_bwd(qkv, self.dO, B, S, H, hd, scale, dqkv=dqkv, stats=self.attn_stats[i])
             else:
                 self._attention_bwd_unfused(i, qkv, dqkv, scale)
             # qkv = a @ Wqkv + bqkv

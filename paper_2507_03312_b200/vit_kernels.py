@@ -124,22 +124,35 @@ def linear_wgrad(x, dy, out=None, split_k=None, cta_group=0):
                 ldc=N_ if out is not None else None, split_k=split_k, cta_group=cta_group)
 
 
-def attention_fwd(qkv, B: int, N: int, H: int, hd: int, scale: float, out=None):
-    """Fused softmax(Q K^T * scale) V from qkv [B*N, 3*H*hd] into out [B*N, H*hd]."""
+def attention_stats_numel(B: int, N: int, H: int) -> int:
+    """f32 elements of the forward's per-row softmax statistics (max, 1/sum)."""
+    return B * H * ((N + 127) // 128) * 128 * 2
+
+
+def attention_fwd(qkv, B: int, N: int, H: int, hd: int, scale: float, out=None, stats=None):
+    """Fused softmax(Q K^T * scale) V from qkv [B*N, 3*H*hd] into out [B*N, H*hd];
+    `stats` (f32, attention_stats_numel) receives the row statistics for the backward."""
     require_cuda([qkv], "attention_fwd")
     D = H * hd
     if out is None:
         out = torch.empty(B * N, D, dtype=qkv.dtype, device=qkv.device)
+    if stats is not None:
+        assert stats.dtype == torch.float32 and stats.numel() >= attention_stats_numel(B, N, H)
     _nat.check(_nat.load().mpx_attention_fwd(_CODE[qkv.dtype], qkv.data_ptr(), B, N, H, hd, scale, out.data_ptr(),
-                                             out.stride(0), stream_handle(qkv.device)), "mpx_attention_fwd")
+                                             out.stride(0), stats.data_ptr() if stats is not None else None,
+                                             stream_handle(qkv.device)), "mpx_attention_fwd")
     return out
 
 
-def attention_bwd(qkv, dO, B: int, N: int, H: int, hd: int, scale: float, dqkv=None):
-    """Fused attention backward: the whole dqkv [B*N, 3*H*hd] from qkv and dO."""
+def attention_bwd(qkv, dO, B: int, N: int, H: int, hd: int, scale: float, dqkv=None, stats=None):
+    """Fused attention backward: the whole dqkv [B*N, 3*H*hd] from qkv and dO
+    (with the forward's `stats`, P is rebuilt without the statistics passes)."""
     require_cuda([qkv, dO], "attention_bwd")
     if dqkv is None:
         dqkv = torch.empty_like(qkv)
+    if stats is not None:
+        assert stats.dtype == torch.float32 and stats.numel() >= attention_stats_numel(B, N, H)
     _nat.check(_nat.load().mpx_attention_bwd(_CODE[qkv.dtype], qkv.data_ptr(), dO.data_ptr(), B, N, H, hd, scale,
-                                             dqkv.data_ptr(), stream_handle(qkv.device)), "mpx_attention_bwd")
+                                             dqkv.data_ptr(), stats.data_ptr() if stats is not None else None,
+                                             stream_handle(qkv.device)), "mpx_attention_bwd")
     return dqkv

@@ -121,6 +121,10 @@ def test_fused_attention_backward(cuda, dt, Nt):
     qkv = torch.randn(Bsz * Nt, 3 * D, device=cuda, generator=g).to(dt)
     dO = torch.randn(Bsz * Nt, D, device=cuda, generator=g).to(dt)
     dqkv = VK.attention_bwd(qkv, dO, Bsz, Nt, H, hd, 0.125)
+    # with the forward's row statistics P is rebuilt bit-identically
+    stats = torch.empty(VK.attention_stats_numel(Bsz, Nt, H), device=cuda)
+    VK.attention_fwd(qkv, Bsz, Nt, H, hd, 0.125, stats=stats)
+    assert torch.equal(VK.attention_bwd(qkv, dO, Bsz, Nt, H, hd, 0.125, stats=stats), dqkv)
     x = qkv.float().requires_grad_(True)
     q, k, v = (x.view(Bsz, Nt, 3, H, hd)[:, :, i] for i in range(3))
     p = torch.softmax(torch.einsum("bnhd,bmhd->bhnm", q, k) * 0.125, -1)

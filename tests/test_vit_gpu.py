@@ -58,7 +58,10 @@ CFGS = {
 
 @pytest.mark.parametrize("name", list(CFGS))
 @pytest.mark.parametrize("half", [torch.float16, torch.bfloat16])
-def test_engine_matches_fp32_reference(cuda, name, half):
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_engine_matches_fp32_reference(cuda, name, half, fused, monkeypatch):
+    """fused = K6 attention kernels; "0" = GEMM + softmax island + GEMM."""
+    monkeypatch.setenv("MPX_FUSED_ATTENTION", fused)
     cfg = CFGS[name]
     B = 4
     p32 = init_params(cfg, cuda, seed=3, std=0.05)
@@ -70,6 +73,7 @@ def test_engine_matches_fp32_reference(cuda, name, half):
     images = torch.randn(B, cfg.img, cfg.img, cfg.chans, device=cuda, generator=g).to(half)
     labels = torch.randint(0, cfg.classes, (B,), device=cuda, generator=g).to(torch.int32)
     eng = ViTEngine(cfg, B, mpx.as_dtype(half), cuda)
+    assert eng.fused_attn == (fused == "1" and cfg.dim // cfg.heads == 64)
     loss = eng.forward(ph, images, labels).item()
     scale = 1024.0
     grads = {k: torch.empty_like(v) for k, v in ph.items()}
