@@ -36,12 +36,12 @@ using namespace ptx;
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kBNMax = 256;
-constexpr int kStages = 4;
 constexpr int kATileBytes = kBM * kBK * 2;       // 16 KB
 constexpr int kBTileBytes = kBNMax * kBK * 2;    // 32 KB
 constexpr int kGemmThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps
 constexpr int kGroupM = 16;
-constexpr size_t kGemmSmem = 1024 + kStages * (kATileBytes + kBTileBytes) + 8 * 4096 + 256;
+constexpr size_t kGemmSmem = 1024 + 5 * (kATileBytes + kBTileBytes / 2) + 8 * 8192 + 256;
+static_assert(3 * (kATileBytes + kBTileBytes) <= 5 * (kATileBytes + kBTileBytes / 2), "CG=1 ring exceeds the CG=2 one");
 
 // ACT_SOFTMAX: the tile holds whole rows (one N block, N <= 256): C = softmax
 //   over the row of round_half(alpha * acc) (f32 island, tensors.py:431-446)
@@ -74,7 +74,10 @@ struct GemmParams {
   int tma_store;  // 16-bit C written through swizzled smem staging + TMA bulk stores
   int xop;        // epilogue operand through TMA (tmX): 0 none, 1 residual in, 2 aux in (GELU'), 3 aux out (GELU)
 };
-enum { XOP_NONE = 0, XOP_RES_IN = 1, XOP_AUX_IN = 2, XOP_AUX_OUT = 3 };
+// kernel variants by epilogue: XOP_NONE = generic (every act / operand at run
+// time, operands read from global); the others are lean staged-path variants
+// (bias optional): residual in, GELU' with aux in, GELU with aux out, plain
+enum { XOP_NONE = 0, XOP_RES_IN = 1, XOP_AUX_IN = 2, XOP_AUX_OUT = 3, XOP_PLAIN = 4 };
 
 __device__ __forceinline__ float half_to_f32(uint16_t h, int fmt) {
   return fmt ? to_f32<MPX_BF16>(h) : to_f32<MPX_F16>(h);
@@ -127,14 +130,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
                 const __grid_constant__ GemmParams P) {
-  constexpr int S = CG == 1 ? kStages : 6;     // smem ring depth
+  constexpr int S = CG == 1 ? 3 : 5;           // smem ring depth (48 / 32 KB stages)
   constexpr int BT = kBTileBytes / CG;         // B bytes per stage per CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * kATileBytes;
-  uint8_t* stage_epi = sB + S * BT;  // 8 epilogue warps x 4 KB output staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_epi + 8 * 4096);
+  uint8_t* stage_epi = sB + S * BT;  // 8 epilogue warps x 8 KB staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_epi + 8 * 8192);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -275,7 +278,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // groups h, h+2, ... (TMA-store path) or 16-column chunks h, h+2, ...
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int h = (warp - 2) >> 2;
-    uint8_t* stg = stage_epi + (warp - 2) * 4096;  // 32 rows x 128 B, 128B-swizzled
+    // two 4 KB staging buffers per warp (32 rows x 128 B, swizzled), used
+    // alternately by successive column groups
+    uint8_t* obuf = stage_epi + (warp - 2) * 8192;
+    uint8_t* stg = obuf;
+    uint32_t gcount = 0;  // staged column groups so far (selects the ping-pong buffer)
     uint32_t eph = 0;  // phase of this warp's operand barrier
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -347,7 +354,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) bulk_wait_read0();
         __syncwarp();
         float* mine = reinterpret_cast<float*>(stg);
-        const float* other = reinterpret_cast<const float*>(stage_epi + ((((warp - 2) + 4) & 7) * 4096));
+        const float* other = reinterpret_cast<const float*>(stage_epi + ((((warp - 2) + 4) & 7) * 8192));
         mine[lane] = m;
         mine[32 + lane] = l;
         mine[64 + lane] = tacc;
@@ -363,6 +370,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
       // xin: the 16 staged operand values of this chunk (TMA operand path) or unused
       auto epi = [&](float* v, int col, int ncols, const float* xin) {
+        if (XO != XOP_NONE) {  // lean variants: bias, then the staged operand
+          if (P.bias) {
+            float bb[16];
+            if (col + 16 <= P.N) {
+              load8(P.bias, col, bb);
+              load8(P.bias, col + 8, bb + 8);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                bb[i] = col + i < P.N ? half_to_f32(static_cast<const uint16_t*>(P.bias)[col + i], P.ab_fmt) : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += bb[i];
+          }
+          if (XO == XOP_RES_IN) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += xin[i];
+          } else if (XO == XOP_AUX_IN) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] *= gelu_grad_f(xin[i]);
+          }
+          return;  // XOP_AUX_OUT: the caller rounds (aux) and applies the GELU
+        }
         if (P.act == ACT_SOFTMAX) {  // v = alpha*acc: P = exp(round(v) - M) / L, 0 past N
 #pragma unroll
           for (int i = 0; i < 16; ++i)
@@ -434,109 +464,161 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       };
 
-      if (P.tma_store) {
-        // groups of 128 bytes per row: 64 half columns or 32 f32 columns
+      if (XO != XOP_NONE || P.tma_store) {  // (the lean variants are only launched staged)
+        // Column groups of GW: 64 half columns (128 B rows, SW128), or 32 f32
+        // columns, or — GELU with the aux written too — 32 half columns whose
+        // aux and C tiles (64 B rows, SW64) share one buffer.  Each warp
+        // ping-pongs its two 4 KB buffers over a running group count, so the
+        // TMA store of group gc overlaps the TMEM loads and math of gc + 1; a
+        // staged operand (residual / GELU aux in) lands in the group's buffer
+        // one group ahead and the output overwrites it in place, row by row.
+        constexpr bool kXin = XO == XOP_RES_IN || XO == XOP_AUX_IN;
+        constexpr bool kAuxOut = XO == XOP_AUX_OUT;
         const bool f32out = P.split > 1 || P.c_dtype == MPX_F32;
-        const int GW = f32out ? 32 : 64;
+        const int GW = (f32out || kAuxOut) ? 32 : 64;
         const int cf = P.c_dtype == MPX_BF16 ? 1 : 0;
-        for (int g = h; g * GW < P.BN; g += 2) {
-          const int nch = min(GW / 16, (P.BN - g * GW) / 16);
-          if (lane == 0) bulk_wait_read0();  // the previous TMA store has read the staging buffer
-          __syncwarp();
-          uint8_t* rowp = stg + lane * 128;
-          const int sw = lane & 7;
-          if (XO == XOP_RES_IN || XO == XOP_AUX_IN) {  // operand tile -> staging by TMA
-            if (lane == 0) {
-              mbar_arrive_expect_tx(&ebar[warp - 2], 4096);
-              const int xb1 = XO == XOP_RES_IN && P.r_sb1 == 0 ? 0 : b1;
-              const int xb2 = XO == XOP_RES_IN && P.r_sb2 == 0 ? 0 : b2;
-              tma_load_4d(stg, &tmX, &ebar[warp - 2], n0 + g * GW, row0, xb1, xb2);
-            }
-            mbar_wait(&ebar[warp - 2], eph);
-            eph ^= 1u;
-          }
+        const int n_groups = (P.BN + GW - 1) / GW;
+        const int my_groups = n_groups > h ? (n_groups - h + 1) / 2 : 0;
+        auto buf = [&](uint32_t c) { return obuf + (c & 1u) * 4096; };
+        auto x_load = [&](int g, uint32_t c) {  // operand tile of group g -> buffer of group count c
+          const int xb1 = XO == XOP_RES_IN && P.r_sb1 == 0 ? 0 : b1;
+          const int xb2 = XO == XOP_RES_IN && P.r_sb2 == 0 ? 0 : b2;
+          bulk_wait_read1();  // the store that last used this buffer (group c - 2) has read it
+          mbar_arrive_expect_tx(&ebar[warp - 2], 4096);
+          tma_load_4d(buf(c), &tmX, &ebar[warp - 2], n0 + g * GW, row0, xb1, xb2);
+        };
+        auto release_acc = [&]() {  // this warp is done with the accumulator: the MMA may reuse it
+          tc_fence_before();
+          if (CG == 2)
+            mbar_arrive_remote(&tempty[acc], 0);
+          else
+            mbar_arrive(&tempty[acc]);
+        };
+        // TMEM -> epilogue math -> the group's staging buffer (in place over a staged operand)
+        auto stage_group = [&](int g, int nch, uint8_t* bb, bool last) {
+          constexpr int kLd = XO == XOP_NONE ? 2 : 4;  // chunks in flight per TMEM wait
 #pragma unroll
-          for (int pair = 0; pair < 2; ++pair) {  // two 16-column chunks per TMEM round trip
-            if (pair * 2 >= nch) continue;
-            uint32_t r[2][16];
+          for (int pair = 0; pair < 4 / kLd; ++pair) {
+            if (pair * kLd >= nch) continue;
+            uint32_t r[kLd][16];
 #pragma unroll
-            for (int k = 0; k < 2; ++k)
-              if (pair * 2 + k < nch) tmem_ld16(taddr + g * GW + (pair * 2 + k) * 16, r[k]);
+            for (int k = 0; k < kLd; ++k)
+              if (pair * kLd + k < nch) tmem_ld16(taddr + g * GW + (pair * kLd + k) * 16, r[k]);
             tmem_ld_wait();
+            if (last && (pair == 4 / kLd - 1 || nch <= (pair + 1) * kLd)) release_acc();
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const int cc = pair * 2 + k;
-              if (cc >= nch) continue;
+            for (int kk = 0; kk < kLd; ++kk) {
+              const int k = pair * kLd + kk;
+              if (k >= nch) continue;
               float v[16];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[k][i]) * P.alpha;
-              const int col = n0 + g * GW + cc * 16;
-              if (f32out) {  // raw (split-K partial) or f32 output: 4 x 16 B per chunk
+              for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[kk][i]) * P.alpha;
+              if (f32out) {  // raw (split-K partial) or f32 output: 4 x 16 B, SW128
+                uint8_t* rowp = bb + lane * 128;
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                  *reinterpret_cast<float4*>(rowp + (((4 * cc + j) ^ sw) << 4)) =
-                      make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-              } else {
-                float xv[16];
-                if (XO == XOP_RES_IN || XO == XOP_AUX_IN) {  // own row of the staged operand
-                  const uint4 w0 = *reinterpret_cast<const uint4*>(rowp + (((2 * cc) ^ sw) << 4));
-                  const uint4 w1 = *reinterpret_cast<const uint4*>(rowp + (((2 * cc + 1) ^ sw) << 4));
-                  const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-                  for (int e = 0; e < 8; ++e) {
-                    xv[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), P.ab_fmt);
-                    xv[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), P.ab_fmt);
-                  }
-                }
-                if (row_ok && col < P.N_store) epi(v, col, min(16, P.N_store - col), xv);
-                uint32_t pk[8];
-                if (XO == XOP_AUX_OUT) {  // stage the rounded pre-activation (aux), keep it for GELU
-#pragma unroll
-                  for (int i = 0; i < 8; ++i) pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], P.ab_fmt);
-                } else {
-#pragma unroll
-                  for (int i = 0; i < 8; ++i) pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], cf);
-                }
-                *reinterpret_cast<uint4*>(rowp + (((2 * cc) ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                *reinterpret_cast<uint4*>(rowp + (((2 * cc + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                for (int u = 0; u < 4; ++u)
+                  *reinterpret_cast<float4*>(rowp + (((4 * k + u) ^ (lane & 7)) << 4)) =
+                      make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                continue;
               }
-            }
-          }
-          if (XO == XOP_AUX_OUT) {  // store aux, then reuse the staging for GELU(pre)
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_4d(&tmX, stg, n0 + g * GW, row0, b1, b2);
-              bulk_commit();
-              bulk_wait_read0();
-            }
-            __syncwarp();
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-              if (cc < nch) {
-                // the rounded pre-activations are still in this lane's staging row
-                const uint4 w0 = *reinterpret_cast<const uint4*>(rowp + (((2 * cc) ^ sw) << 4));
-                const uint4 w1 = *reinterpret_cast<const uint4*>(rowp + (((2 * cc + 1) ^ sw) << 4));
-                uint32_t pk[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+              const int col = n0 + g * GW + k * 16;
+              if (kAuxOut) {  // aux (rounded pre-activation) at bb, C = GELU(aux) at bb + 2 KB; SW64
+                if (row_ok && col < P.N_store) epi(v, col, min(16, P.N_store - col), v);
+                uint32_t pa[8], pc[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                  const float a = half_to_f32((uint16_t)(pk[i] & 0xFFFFu), P.ab_fmt);
-                  const float b = half_to_f32((uint16_t)(pk[i] >> 16), P.ab_fmt);
-                  pk[i] = pack2_fmt(gelu_f(a), gelu_f(b), cf);
+                  pa[i] = pack2_fmt(v[2 * i], v[2 * i + 1], P.ab_fmt);
+                  const float a = half_to_f32((uint16_t)(pa[i] & 0xFFFFu), P.ab_fmt);
+                  const float b = half_to_f32((uint16_t)(pa[i] >> 16), P.ab_fmt);
+                  pc[i] = pack2_fmt(gelu_f(a), gelu_f(b), cf);
                 }
-                *reinterpret_cast<uint4*>(rowp + (((2 * cc) ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                *reinterpret_cast<uint4*>(rowp + (((2 * cc + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                const int s64 = (lane >> 1) & 3;
+                uint8_t* ra = bb + lane * 64;
+                uint8_t* rc = ra + 2048;
+                *reinterpret_cast<uint4*>(ra + (((2 * k) ^ s64) << 4)) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+                *reinterpret_cast<uint4*>(ra + (((2 * k + 1) ^ s64) << 4)) = make_uint4(pa[4], pa[5], pa[6], pa[7]);
+                *reinterpret_cast<uint4*>(rc + (((2 * k) ^ s64) << 4)) = make_uint4(pc[0], pc[1], pc[2], pc[3]);
+                *reinterpret_cast<uint4*>(rc + (((2 * k + 1) ^ s64) << 4)) = make_uint4(pc[4], pc[5], pc[6], pc[7]);
+                continue;
               }
+              uint8_t* rowp = bb + lane * 128;
+              const int sw = lane & 7;
+              float xv[16];
+              if (kXin) {  // own row of the staged operand
+                const uint4 w0 = *reinterpret_cast<const uint4*>(rowp + (((2 * k) ^ sw) << 4));
+                const uint4 w1 = *reinterpret_cast<const uint4*>(rowp + (((2 * k + 1) ^ sw) << 4));
+                const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  xv[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), P.ab_fmt);
+                  xv[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), P.ab_fmt);
+                }
+              }
+              if (row_ok && col < P.N_store) epi(v, col, min(16, P.N_store - col), xv);
+              uint32_t pk[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], cf);
+              *reinterpret_cast<uint4*>(rowp + (((2 * k) ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              *reinterpret_cast<uint4*>(rowp + (((2 * k + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
             }
           }
+        };
+        auto store_group = [&](int g, uint8_t* bb) {  // lane 0
+          if (P.split > 1) {
+            tma_store_4d(&tmC, bb, n0 + g * GW, row0, tc.s, 0);
+          } else if (kAuxOut) {
+            tma_store_4d(&tmX, bb, n0 + g * GW, row0, b1, b2);
+            tma_store_4d(&tmC, bb + 2048, n0 + g * GW, row0, b1, b2);
+          } else {
+            tma_store_4d(&tmC, bb, n0 + g * GW, row0, b1, b2);
+          }
+        };
+        // batched: both of this warp's groups staged at once (one buffer each),
+        // one proxy fence and one bulk group per tile — the previous tile's
+        // stores had a whole tile of MMA time to drain.  Otherwise (f32 / GELU-
+        // aux-out groups, > 2 groups) ping-pong the buffers group by group.
+        const bool batched = !f32out && !kAuxOut && my_groups <= 2;
+        if (batched) {
+          if (lane == 0) {
+            bulk_wait_read0();
+            if (kXin && my_groups > 0) {
+              const int xb1 = XO == XOP_RES_IN && P.r_sb1 == 0 ? 0 : b1;
+              const int xb2 = XO == XOP_RES_IN && P.r_sb2 == 0 ? 0 : b2;
+              mbar_arrive_expect_tx(&ebar[warp - 2], 4096u * my_groups);
+              for (int j = 0; j < my_groups; ++j)
+                tma_load_4d(buf(j), &tmX, &ebar[warp - 2], n0 + (h + 2 * j) * GW, row0, xb1, xb2);
+            }
+          }
+          __syncwarp();
+        } else if (kXin && lane == 0 && my_groups > 0) {
+          x_load(h, gcount);
+        }
+        if (my_groups == 0) release_acc();
+        for (int j = 0; j < my_groups; ++j, ++gcount) {
+          const int g = h + 2 * j;
+          const int nch = min(GW / 16, (P.BN - g * GW) / 16);
+          uint8_t* bb = batched ? buf(j) : buf(gcount);
+          if (kXin) {
+            if (!batched || j == 0) {
+              mbar_wait(&ebar[warp - 2], eph);
+              eph ^= 1u;
+            }
+          } else if (!batched) {
+            if (lane == 0) bulk_wait_read1();  // group gcount - 2's store has read this buffer
+            __syncwarp();
+          }
+          stage_group(g, nch, bb, j == my_groups - 1);
+          if (batched && j + 1 < my_groups) continue;
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            if (P.split > 1)
-              tma_store_4d(&tmC, stg, n0 + g * GW, row0, tc.s, 0);
-            else
-              tma_store_4d(&tmC, stg, n0 + g * GW, row0, b1, b2);
+            if (batched) {
+              for (int jj = 0; jj < my_groups; ++jj) store_group(h + 2 * jj, buf(jj));
+            } else {
+              store_group(g, bb);
+            }
             bulk_commit();
+            if (!batched && kXin && j + 1 < my_groups) x_load(g + 2, gcount + 1);  // next group's operand
           }
         }
       } else {
@@ -576,11 +658,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
-      tc_fence_before();
-      if (CG == 2)
-        mbar_arrive_remote(&tempty[acc], 0);  // the leader's MMA reuses this accumulator
-      else
-        mbar_arrive(&tempty[acc]);
+      if (!P.tma_store) {  // (the staged path released it after its last TMEM load)
+        tc_fence_before();
+        if (CG == 2)
+          mbar_arrive_remote(&tempty[acc], 0);  // the leader's MMA reuses this accumulator
+        else
+          mbar_arrive(&tempty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -632,7 +716,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 4-D map: (inner, outer, b1, b2) with byte strides for dims 1..3
 static int make_map(CUtensorMap* m, const void* ptr, int ab_fmt, uint64_t inner, uint64_t outer, uint64_t nb1,
                     uint64_t nb2, uint64_t s_outer, uint64_t s_b1, uint64_t s_b2, uint32_t box_inner,
-                    uint32_t box_outer) {
+                    uint32_t box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return fail(MPX_EINVAL, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[4] = {inner, outer, nb1, nb2};
@@ -640,8 +724,8 @@ static int make_map(CUtensorMap* m, const void* ptr, int ab_fmt, uint64_t inner,
   cuuint32_t box[4] = {box_inner, box_outer, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = fn(m, ab_fmt ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
-                  const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(MPX_EINVAL, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return 0;
 }
@@ -650,15 +734,15 @@ static int make_map(CUtensorMap* m, const void* ptr, int ab_fmt, uint64_t inner,
 // extent 1 there (TMA strides must be non-zero) and the kernel uses coordinate 0
 static int make_map_dt(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
                        uint64_t nb1, uint64_t nb2, uint64_t s_outer, uint64_t s_b1, uint64_t s_b2, uint32_t box_inner,
-                       uint32_t box_outer) {
+                       uint32_t box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return fail(MPX_EINVAL, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[4] = {inner, outer, nb1, nb2};
   cuuint64_t strides[3] = {s_outer, s_b1, s_b2};
   cuuint32_t box[4] = {box_inner, box_outer, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
-  CUresult r = fn(m, dt, 4, const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = fn(m, dt, 4, const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(MPX_EINVAL, "cuTensorMapEncodeTiled (C) failed (" + std::to_string((int)r) + ")");
   return 0;
 }
@@ -798,13 +882,23 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   if (P.tma_store && split == 1 && g->c_dtype != MPX_F32 && g->tma_store >= 0 && !no_xop) {
     const uint64_t es2 = 2;
     auto al16 = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
-    if ((g->act == ACT_GELU || g->act == ACT_GELU_BWD) && g->aux && al16(g->aux) && g->ld_aux % 8 == 0 &&
+    if ((g->act == ACT_GELU || g->act == ACT_GELU_BWD) && !g->residual && g->aux && al16(g->aux) && g->ld_aux % 8 == 0 &&
         (nb1 == 1 || (g->c_sb1 > 0 && g->c_sb1 % 8 == 0)) && (nb2 == 1 || (g->c_sb2 > 0 && g->c_sb2 % 8 == 0))) {
       const uint64_t s_m = (uint64_t)g->ld_aux * es2;
-      rc = make_map(&tx, g->aux, fmt, g->N, g->M, nb1, nb2, s_m, nb1 > 1 ? (uint64_t)g->c_sb1 * es2 : s_m * g->M,
-                    nb2 > 1 ? (uint64_t)g->c_sb2 * es2 : s_m * g->M, 64, 32);
-      if (rc) return rc;
       P.xop = g->act == ACT_GELU ? XOP_AUX_OUT : XOP_AUX_IN;
+      // GELU out: aux and C leave as 32-column SW64 tiles sharing one staging buffer
+      const bool out2 = P.xop == XOP_AUX_OUT;
+      const CUtensorMapSwizzle swz = out2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+      rc = make_map(&tx, g->aux, fmt, g->N, g->M, nb1, nb2, s_m, nb1 > 1 ? (uint64_t)g->c_sb1 * es2 : s_m * g->M,
+                    nb2 > 1 ? (uint64_t)g->c_sb2 * es2 : s_m * g->M, out2 ? 32 : 64, 32, swz);
+      if (rc) return rc;
+      if (out2) {
+        const uint64_t s_c = (uint64_t)g->ldc * es2;
+        rc = make_map(&tc, g->C, g->c_dtype == MPX_BF16 ? 1 : 0, g->N, g->M, nb1, nb2, s_c,
+                      nb1 > 1 ? (uint64_t)g->c_sb1 * es2 : s_c * g->M, nb2 > 1 ? (uint64_t)g->c_sb2 * es2 : s_c * g->M,
+                      32, 32, swz);
+        if (rc) return rc;
+      }
     } else if (g->act == ACT_NONE && g->residual && al16(g->residual) && g->ldr % 8 == 0 &&
                (nb1 == 1 || g->r_sb1 == 0 || g->r_sb1 % 8 == 0) && (nb2 == 1 || g->r_sb2 == 0 || g->r_sb2 % 8 == 0)) {
       const uint64_t s_m = (uint64_t)g->ldr * es2;
@@ -815,17 +909,20 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
       P.xop = XOP_RES_IN;
     }
   }
+  if (P.tma_store && P.xop == XOP_NONE && g->act == ACT_NONE && !g->residual && !no_xop) P.xop = XOP_PLAIN;
 
   using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
                            const GemmParams);
-  static const KernelFn kernels[2][4] = {
-      {gemm_kernel<1, XOP_NONE>, gemm_kernel<1, XOP_RES_IN>, gemm_kernel<1, XOP_AUX_IN>, gemm_kernel<1, XOP_AUX_OUT>},
-      {gemm_kernel<2, XOP_NONE>, gemm_kernel<2, XOP_RES_IN>, gemm_kernel<2, XOP_AUX_IN>, gemm_kernel<2, XOP_AUX_OUT>}};
+  static const KernelFn kernels[2][5] = {
+      {gemm_kernel<1, XOP_NONE>, gemm_kernel<1, XOP_RES_IN>, gemm_kernel<1, XOP_AUX_IN>, gemm_kernel<1, XOP_AUX_OUT>,
+       gemm_kernel<1, XOP_PLAIN>},
+      {gemm_kernel<2, XOP_NONE>, gemm_kernel<2, XOP_RES_IN>, gemm_kernel<2, XOP_AUX_IN>, gemm_kernel<2, XOP_AUX_OUT>,
+       gemm_kernel<2, XOP_PLAIN>}};
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
     for (int c = 0; c < 2 && attr_err == cudaSuccess; ++c)
-      for (int x = 0; x < 4 && attr_err == cudaSuccess; ++x)
+      for (int x = 0; x < 5 && attr_err == cudaSuccess; ++x)
         attr_err = cudaFuncSetAttribute(kernels[c][x], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
   });
   if (attr_err != cudaSuccess) return fail((int)attr_err, "cudaFuncSetAttribute(gemm_kernel)");
