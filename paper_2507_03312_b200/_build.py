@@ -52,18 +52,23 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    OBJ.mkdir(parents=True, exist_ok=True)
-    LIB.parent.mkdir(parents=True, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines: tuple = (), out: Path | None = None) -> Path:
+    """defines: extra -D macros for an instrumented variant (objects in
+    build/obj-<tag>, library at `out`); the product build has none."""
+    obj_dir = OBJ if not defines else OBJ.parent / ("obj-" + "-".join(d.lower() for d in defines))
+    lib = LIB if out is None else Path(out)
+    obj_dir.mkdir(parents=True, exist_ok=True)
+    lib.parent.mkdir(parents=True, exist_ok=True)
+    flags = NVCC_FLAGS + [f"-D{d}" for d in defines]
     headers = _headers()
     cc = nvcc()
     jobs = []
     objs = []
     for src in _sources():
-        obj = OBJ / (src.stem + ".o")
+        obj = obj_dir / (src.stem + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            jobs.append([cc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)])
+            jobs.append([cc, *flags, "-c", str(src), "-o", str(obj)])
 
     def run(cmd):
         if verbose:
@@ -75,10 +80,13 @@ def build(verbose: bool = False, force: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         list(ex.map(run, jobs))
-    if force or jobs or _stale(LIB, objs):
-        run([cc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs)])
-    return LIB
+    if force or jobs or _stale(lib, objs):
+        run([cc, *ARCH, "-shared", "-o", str(lib), *map(str, objs)])
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    # python _build.py [-v] [-f] [-DNAME ... -o out.so]   (instrumented variants)
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    out = sys.argv[sys.argv.index("-o") + 1] if "-o" in sys.argv else None
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, defines=defs, out=out))

@@ -27,6 +27,21 @@ namespace mpx {
 
 using namespace ptx;
 
+// -DMPX_TRACE builds (tools only): per-CTA clock64 timestamps of the backward's
+// phases for the first kTraceCtas CTAs, read back with mpx_debug_attn_trace
+#ifdef MPX_TRACE
+constexpr int kTraceCtas = 64, kTraceSlots = 32;
+__device__ long long g_attn_trace[kTraceCtas * kTraceSlots];
+#define ATRACE(slot)                                                            \
+  do {                                                                          \
+    if (blockIdx.x < kTraceCtas) g_attn_trace[blockIdx.x * kTraceSlots + (slot)] = clock64(); \
+  } while (0)
+#else
+#define ATRACE(slot) \
+  do {               \
+  } while (0)
+#endif
+
 constexpr int kAttnQ = 16384;      // Q tile 128 x 64 half
 constexpr int kAttnKV = 32768;     // K / V 256 x 64 half
 constexpr int kAttnP = 65536;      // P 128 x 256 half (4 K-major chunks of 64 keys)
@@ -426,10 +441,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* sV = sK + kAttnKV;
   uint8_t* sP = sV + kAttnKV;
   uint8_t* sdS = sP + kAttnP;
-  // 0 kv, 1 q/dO, 2 S, 3 P, 4 dP, 5 dS, 6 dQ(+dV,dK), 7 dQ read
+  // 0 kv, 1 q/dO, 2 S, 3 P, 4 dP, 5 dS, 6 dQ(+dV,dK), 7 dQ read, 8 Q free (dK), 9 dO free (dV)
   float* red = reinterpret_cast<float*>(sdS + kAttnP);
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + kSplit * 128);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int h = blockIdx.x % P.H, b = blockIdx.x / P.H;
@@ -441,7 +456,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     tma_prefetch(&tmdO);
-    for (int i = 0; i < 8; ++i) mbar_init(&bar[i], (i == 3 || i == 5 || i == 7) ? 128 * kSplit : 1);
+    for (int i = 0; i < 10; ++i) mbar_init(&bar[i], (i == 3 || i == 5 || i == 7) ? 128 * kSplit : 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -466,10 +481,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t id_nk = idesc_f16(P.fmt, 128, 16 * n_chunks, 0, 0);
       const uint32_t id_kv = idesc_f16(P.fmt, 128, 64, 1, 1);   // dV / dK halves: A, B MN-major
       const uint32_t id_q = idesc_f16(P.fmt, 128, 64, 0, 1);    // dQ: A K-major, B MN-major
+      ATRACE(0);
       mbar_wait(&bar[0], 0);
+      ATRACE(1);
       for (int t = 0; t < T; ++t) {
         const uint32_t ph = t & 1;
         mbar_wait(&bar[1], ph);
+        ATRACE(2 + 8 * t);
         if (t > 0) mbar_wait(&bar[7], ph ^ 1);  // previous dQ drained from TMEM cols 0-63
         tc_fence_after();
 #pragma unroll
@@ -477,32 +495,40 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           umma_f16(tmem, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), id_nk, s > 0);
         umma_commit(&bar[2]);
         mbar_wait(&bar[3], ph);  // P_t written (S consumed)
+        ATRACE(3 + 8 * t);
         tc_fence_after();
 #pragma unroll
         for (int s = 0; s < 4; ++s)  // dP = dO V^T
           umma_f16(tmem, sw128_desc(dO + s * 32, 16, 1024), sw128_desc(v + s * 32, 16, 1024), id_nk, s > 0);
         umma_commit(&bar[4]);
         mbar_wait(&bar[5], ph);  // dS_t written (dP consumed)
+        ATRACE(4 + 8 * t);
         tc_fence_after();
+        // dK first (its completion frees Q_t), then dV (frees dO_t), then dQ:
+        // the next tile's Q / dO loads overlap dV, dQ and the dQ readout
         for (int half = 0; half < halves; ++half) {
 #pragma unroll
-          for (int s = 0; s < 8; ++s) {  // over the 128 queries of the tile
-            const uint64_t bdo = sw128_desc(dO + s * 2048, 8192, 1024);
-            const uint64_t bq = sw128_desc(q + s * 2048, 8192, 1024);
-            umma_f16(tmem + 256 + half * 64, sw128_desc(pp + half * 32768 + s * 2048, 16384, 1024), bdo, id_kv,
-                     (t > 0 || s > 0));  // dV += P^T dO
-            umma_f16(tmem + 384 + half * 64, sw128_desc(ds + half * 32768 + s * 2048, 16384, 1024), bq, id_kv,
-                     (t > 0 || s > 0));  // dK += dS^T Q
-          }
+          for (int s = 0; s < 8; ++s)  // over the 128 queries of the tile: dK += dS^T Q
+            umma_f16(tmem + 384 + half * 64, sw128_desc(ds + half * 32768 + s * 2048, 16384, 1024),
+                     sw128_desc(q + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
         }
+        umma_commit(&bar[8]);
+        for (int half = 0; half < halves; ++half) {
+#pragma unroll
+          for (int s = 0; s < 8; ++s)  // dV += P^T dO
+            umma_f16(tmem + 256 + half * 64, sw128_desc(pp + half * 32768 + s * 2048, 16384, 1024),
+                     sw128_desc(dO + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
+        }
+        umma_commit(&bar[9]);
         for (int s = 0; s < n_chunks; ++s)  // dQ = dS K
           umma_f16(tmem, sw128_desc(ds + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024), sw128_desc(k + s * 2048, 8192, 1024),
                    id_q, s > 0);
         umma_commit(&bar[6]);
-        if (t + 1 < T) {  // next tile's Q / dO once this tile's MMAs have read them
-          mbar_wait(&bar[6], ph);
+        if (t + 1 < T) {  // next tile's Q / dO as soon as this tile's MMAs have read them
           mbar_arrive_expect_tx(&bar[1], 2 * kAttnQ);
+          mbar_wait(&bar[8], ph);
           tma_load_4d(sQ, &tmQ, &bar[1], 0, (t + 1) * 128, h, b);
+          mbar_wait(&bar[9], ph);
           tma_load_4d(sdO, &tmdO, &bar[1], 0, (t + 1) * 128, h, b);
         }
       }
@@ -526,16 +552,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     for (int t = 0; t < T; ++t) {
       const uint32_t ph = t & 1;
       // ---- P = softmax(round(S * scale)) -> smem (as in the forward)
+      float2 st = make_float2(0.f, 0.f);  // the forward's (max, 1/sum), fetched while S is computed
+      if (P.stats) st = __ldg(P.stats + ((long long)blockIdx.x * T + t) * 128 + r);
       mbar_wait(&bar[2], ph);
+      if (warp == 4 && lane == 0) ATRACE(5 + 8 * t);
       tc_fence_after();
-      const float2* st = P.stats ? P.stats + ((long long)blockIdx.x * T + t) * 128 + r : nullptr;
-      softmax_bwd_p<kSplit>(trow, split, r, qd, P.N, P.scale, P.fmt, red, sP, st);
+      softmax_bwd_p<kSplit>(trow, split, r, qd, P.N, P.scale, P.fmt, red, sP, P.stats ? &st : nullptr);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&bar[3]);
       // ---- dS = P * (dP - sum(P * dP)) -> smem; dP rounded to the half
       // format first (the reference's dP is a half GEMM output), kept packed
       mbar_wait(&bar[4], ph);
+      if (warp == 4 && lane == 0) ATRACE(6 + 8 * t);
       tc_fence_after();
       uint32_t dpk[kMaxC][8];
       float tsum = 0.f;
@@ -585,6 +614,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_arrive(&bar[5]);
       // ---- dQ_t -> dqkv[:, q part]
       mbar_wait(&bar[6], ph);
+      if (warp == 4 && lane == 0) ATRACE(7 + 8 * t);
       tc_fence_after();
       const int qrow = t * 128 + r;
       uint16_t* o = static_cast<uint16_t*>(P.dqkv) + ((long long)b * P.N + qrow) * P.ld + (long long)h * P.hd;
@@ -603,6 +633,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bar[7]);
+      if (warp == 4 && lane == 0) ATRACE(8 + 8 * t);
     }
     // ---- dV, dK (keys r and 128 + r of this head): 4 (half, which) combos split over the warps
     for (int combo = split; combo < 4; combo += kSplit) {
@@ -628,6 +659,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) ATRACE(30);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -667,6 +699,13 @@ static int qkv_map(CUtensorMap* m, const void* base, int fmt, int N, int H, int 
 }  // namespace mpx
 
 using namespace mpx;
+
+#ifdef MPX_TRACE
+extern "C" int mpx_debug_attn_trace(long long* host_out) {  // kTraceCtas * kTraceSlots int64
+  MPX_CUDA_CHECK(cudaMemcpyFromSymbol(host_out, g_attn_trace, sizeof(long long) * kTraceCtas * kTraceSlots));
+  return 0;
+}
+#endif
 
 extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H, int hd, float scale, void* O,
                                  int64_t ldo, float* row_stats, void* stream) {
