@@ -38,9 +38,13 @@ constexpr int kBK = 64;
 constexpr int kBNMax = 256;
 constexpr int kATileBytes = kBM * kBK * 2;       // 16 KB
 constexpr int kBTileBytes = kBNMax * kBK * 2;    // 32 KB
-constexpr int kGemmThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps
+constexpr int kEpiWarps = 8;                  // epilogue warps: kEpiWarps / 4 per TMEM lane quarter (16: no gain)
+constexpr int kEpiPerQ = kEpiWarps / 4;
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // TMA warp, MMA warp, epilogue warps
+constexpr int kEpiStage = 65536;               // staging bytes (all epilogue warps)
+constexpr int kBufPerWarp = kEpiStage / kEpiWarps / 4096;  // 4 KB staging buffers per epilogue warp
 constexpr int kGroupM = 16;
-constexpr size_t kGemmSmem = 1024 + 5 * (kATileBytes + kBTileBytes / 2) + 8 * 8192 + 256;
+constexpr size_t kGemmSmem = 1024 + 5 * (kATileBytes + kBTileBytes / 2) + kEpiStage + 384;
 static_assert(3 * (kATileBytes + kBTileBytes) <= 5 * (kATileBytes + kBTileBytes / 2), "CG=1 ring exceeds the CG=2 one");
 
 // ACT_SOFTMAX: the tile holds whole rows (one N block, N <= 256): C = softmax
@@ -136,13 +140,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * kATileBytes;
-  uint8_t* stage_epi = sB + S * BT;  // 8 epilogue warps x 8 KB staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_epi + 8 * 8192);
+  uint8_t* stage_epi = sB + S * BT;  // kEpiWarps x kBufPerWarp x 4 KB staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_epi + kEpiStage);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint64_t* ebar = tempty + 2;  // per epilogue warp: its operand tile has landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 8);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + kEpiWarps);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -161,9 +165,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 256 * CG);
+      mbar_init(&tempty[i], 32 * kEpiWarps * CG);
     }
-    for (int i = 0; i < 8; ++i) mbar_init(&ebar[i], 1);
+    for (int i = 0; i < kEpiWarps; ++i) mbar_init(&ebar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -273,14 +277,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    // -------------------------------------------------- epilogue (256 thr)
-    // two warps per TMEM lane quarter (warp % 4); warp half h owns 64-column
-    // groups h, h+2, ... (TMA-store path) or 16-column chunks h, h+2, ...
+    // -------------------------------------------------- epilogue warps
+    // kEpiPerQ warps per TMEM lane quarter (warp % 4); warp h of a quarter
+    // owns column groups h, h + kEpiPerQ, ... (TMA-store path) or 16-column
+    // chunks h, h + kEpiPerQ, ... (direct path)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int h = (warp - 2) >> 2;
-    // two 4 KB staging buffers per warp (32 rows x 128 B, swizzled), used
-    // alternately by successive column groups
-    uint8_t* obuf = stage_epi + (warp - 2) * 8192;
+    // kBufPerWarp 4 KB staging buffers per warp (32 rows x 128 B, swizzled),
+    // used in turn by successive column groups
+    uint8_t* obuf = stage_epi + (warp - 2) * (kBufPerWarp * 4096);
     uint8_t* stg = obuf;
     uint32_t gcount = 0;  // staged column groups so far (selects the ping-pong buffer)
     uint32_t eph = 0;  // phase of this warp's operand barrier
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       auto round_half = [&](float x) { return half_to_f32(f32_to_half(x, P.ab_fmt), P.ab_fmt); };
       if (smx) {
         float m = -INFINITY, l = 0.f, tacc = 0.f;
-        for (int g = h; g * 64 < P.BN; g += 2) {
+        for (int g = h; g * 64 < P.BN; g += kEpiPerQ) {
           for (int cc = 0; cc < 4 && g * 64 + cc * 16 < P.BN; ++cc) {
             uint32_t r[16];
             tmem_ld16(taddr + g * 64 + cc * 16, r);
@@ -354,18 +359,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) bulk_wait_read0();
         __syncwarp();
         float* mine = reinterpret_cast<float*>(stg);
-        const float* other = reinterpret_cast<const float*>(stage_epi + ((((warp - 2) + 4) & 7) * 8192));
         mine[lane] = m;
         mine[32 + lane] = l;
         mine[64 + lane] = tacc;
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-        const float om = other[lane], ol = other[32 + lane], ot = other[64 + lane];
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-        const float M = fmaxf(m, om);
-        const float L = (m == -INFINITY ? 0.f : l * __expf(m - M)) + (om == -INFINITY ? 0.f : ol * __expf(om - M));
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * kEpiPerQ) : "memory");
+        float om[kEpiPerQ], ol[kEpiPerQ], M = -INFINITY, L = 0.f, T = 0.f;
+#pragma unroll
+        for (int j = 0; j < kEpiPerQ; ++j) {  // the warps of this lane quarter: e = (e & 3) + 4 j
+          const float* o = reinterpret_cast<const float*>(stage_epi + (((warp - 2) & 3) + 4 * j) * (kBufPerWarp * 4096));
+          om[j] = o[lane];
+          ol[j] = o[32 + lane];
+          T += o[64 + lane];
+          M = fmaxf(M, om[j]);
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * kEpiPerQ) : "memory");
+#pragma unroll
+        for (int j = 0; j < kEpiPerQ; ++j) L += om[j] == -INFINITY ? 0.f : ol[j] * __expf(om[j] - M);
         row_m = M;
         row_inv = 1.f / L;
-        row_t = tacc + ot;
+        row_t = T;
       }
 
       // xin: the 16 staged operand values of this chunk (TMA operand path) or unused
@@ -478,12 +490,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int GW = (f32out || kAuxOut) ? 32 : 64;
         const int cf = P.c_dtype == MPX_BF16 ? 1 : 0;
         const int n_groups = (P.BN + GW - 1) / GW;
-        const int my_groups = n_groups > h ? (n_groups - h + 1) / 2 : 0;
-        auto buf = [&](uint32_t c) { return obuf + (c & 1u) * 4096; };
+        const int my_groups = n_groups > h ? (n_groups - h + kEpiPerQ - 1) / kEpiPerQ : 0;
+        auto buf = [&](uint32_t c) { return obuf + (c % kBufPerWarp) * 4096; };
         auto x_load = [&](int g, uint32_t c) {  // operand tile of group g -> buffer of group count c
           const int xb1 = XO == XOP_RES_IN && P.r_sb1 == 0 ? 0 : b1;
           const int xb2 = XO == XOP_RES_IN && P.r_sb2 == 0 ? 0 : b2;
-          bulk_wait_read1();  // the store that last used this buffer (group c - 2) has read it
+          bulk_wait_read<kBufPerWarp - 1>();  // the store that last used this buffer has read it
           mbar_arrive_expect_tx(&ebar[warp - 2], 4096);
           tma_load_4d(buf(c), &tmX, &ebar[warp - 2], n0 + g * GW, row0, xb1, xb2);
         };
@@ -496,7 +508,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         };
         // TMEM -> epilogue math -> the group's staging buffer (in place over a staged operand)
         auto stage_group = [&](int g, int nch, uint8_t* bb, bool last) {
-          constexpr int kLd = XO == XOP_NONE ? 2 : 4;  // chunks in flight per TMEM wait
+          constexpr int kLd = kEpiWarps > 8 ? (XO == XOP_PLAIN || XO == XOP_AUX_OUT ? 2 : 1) : (XO == XOP_NONE ? 2 : 4);  // chunks per TMEM wait
 #pragma unroll
           for (int pair = 0; pair < 4 / kLd; ++pair) {
             if (pair * kLd >= nch) continue;
@@ -577,7 +589,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // one proxy fence and one bulk group per tile — the previous tile's
         // stores had a whole tile of MMA time to drain.  Otherwise (f32 / GELU-
         // aux-out groups, > 2 groups) ping-pong the buffers group by group.
-        const bool batched = !f32out && !kAuxOut && my_groups <= 2;
+        const bool batched = my_groups <= kBufPerWarp;
         if (batched) {
           if (lane == 0) {
             bulk_wait_read0();
@@ -586,7 +598,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               const int xb2 = XO == XOP_RES_IN && P.r_sb2 == 0 ? 0 : b2;
               mbar_arrive_expect_tx(&ebar[warp - 2], 4096u * my_groups);
               for (int j = 0; j < my_groups; ++j)
-                tma_load_4d(buf(j), &tmX, &ebar[warp - 2], n0 + (h + 2 * j) * GW, row0, xb1, xb2);
+                tma_load_4d(buf(j), &tmX, &ebar[warp - 2], n0 + (h + kEpiPerQ * j) * GW, row0, xb1, xb2);
             }
           }
           __syncwarp();
@@ -595,7 +607,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         if (my_groups == 0) release_acc();
         for (int j = 0; j < my_groups; ++j, ++gcount) {
-          const int g = h + 2 * j;
+          const int g = h + kEpiPerQ * j;
           const int nch = min(GW / 16, (P.BN - g * GW) / 16);
           uint8_t* bb = batched ? buf(j) : buf(gcount);
           if (kXin) {
@@ -604,7 +616,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               eph ^= 1u;
             }
           } else if (!batched) {
-            if (lane == 0) bulk_wait_read1();  // group gcount - 2's store has read this buffer
+            if (lane == 0) bulk_wait_read<kBufPerWarp - 1>();  // the store that last used this buffer has read it
             __syncwarp();
           }
           stage_group(g, nch, bb, j == my_groups - 1);
@@ -613,24 +625,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           __syncwarp();
           if (lane == 0) {
             if (batched) {
-              for (int jj = 0; jj < my_groups; ++jj) store_group(h + 2 * jj, buf(jj));
+              for (int jj = 0; jj < my_groups; ++jj) store_group(h + kEpiPerQ * jj, buf(jj));
             } else {
               store_group(g, bb);
             }
             bulk_commit();
-            if (!batched && kXin && j + 1 < my_groups) x_load(g + 2, gcount + 1);  // next group's operand
+            if (!batched && kXin && j + 1 < my_groups) x_load(g + kEpiPerQ, gcount + 1);  // next group's operand
           }
         }
       } else {
         uint32_t r[16];
         const int chunk0 = h * 16;
         if (chunk0 < P.BN) tmem_ld16(taddr + chunk0, r);
-        for (int c = chunk0; c < P.BN; c += 32) {
+        for (int c = chunk0; c < P.BN; c += 16 * kEpiPerQ) {
           tmem_ld_wait();
           float v[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]) * P.alpha;
-          if (c + 32 < P.BN) tmem_ld16(taddr + c + 32, r);  // next chunk in flight while this one is processed
+          if (c + 16 * kEpiPerQ < P.BN) tmem_ld16(taddr + c + 16 * kEpiPerQ, r);  // next chunk in flight
           const int col = n0 + c;
           if (col >= P.N_store || !row_ok) continue;
           const int ncols = min(16, P.N_store - col);  // 8 or 16
