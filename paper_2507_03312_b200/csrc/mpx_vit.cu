@@ -235,7 +235,36 @@ __global__ void __launch_bounds__(256) ln_colsum_kernel(const void* __restrict__
   float ag[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ax[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const bool live = c0 < D;
   if (live) {
-    for (int r = r0 + rl; r < r1; r += 8) {
+    int r = r0 + rl;
+    for (; r + 8 < r1; r += 16) {  // two rows in flight per thread
+      uint4 wx[2], wd[2], wo[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const long long rr = r + 8 * j;
+        wx[j] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + rr * ldx + c0));
+        wd[j] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dy) + rr * lddy + c0));
+        if (dx) wo[j] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dx) + rr * lddx + c0));
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        float xv[8], dv[8];
+        unpack8(wx[j], xv, fmt);
+        unpack8(wd[j], dv, fmt);
+        const float mu = mean[r + 8 * j], rs = rstd[r + 8 * j];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          ag[e] += dv[e] * (xv[e] - mu) * rs;
+          ab[e] += dv[e];
+        }
+        if (dx) {
+          float ov[8];
+          unpack8(wo[j], ov, fmt);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) ax[e] += ov[e];
+        }
+      }
+    }
+    for (; r < r1; r += 8) {
       float xv[8], dv[8];
       unpack8(*reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + (long long)r * ldx + c0), xv, fmt);
       unpack8(*reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dy) + (long long)r * lddy + c0), dv, fmt);
@@ -272,27 +301,36 @@ __global__ void __launch_bounds__(256) ln_colsum_kernel(const void* __restrict__
   }
 }
 
-// ws [nsum][nb][D] -> outputs; block = 32 columns x 8 partial lanes
+// ws [nsum][nb][D] -> outputs; grid (D/32, nsum), block = 32 columns x 8
+// partial lanes, four partial rows in flight per thread, fixed order
 __global__ void __launch_bounds__(256) partials_reduce3_kernel(const float* __restrict__ ws, int nb, int D,
                                                                void* out0, void* out1, void* out2, int fmt) {
-  __shared__ float sm[3][8][33];
+  __shared__ float sm[8][33];
   const int cl = threadIdx.x & 31, kl = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
-  void* outs[3] = {out0, out1, out2};
-  const int nsum = out2 ? 3 : 2;
-  for (int q = 0; q < nsum; ++q) {
-    float a = 0.f;
-    if (c < D)
-      for (int k = kl; k < nb; k += 8) a += ws[((long long)q * nb + k) * D + c];
-    sm[q][kl][cl] = a;
-  }
-  __syncthreads();
-  if (kl == 0 && c < D)
-    for (int q = 0; q < nsum; ++q) {
-      float t = 0.f;
-      for (int k = 0; k < 8; ++k) t += sm[q][k][cl];
-      if (outs[q]) st_h(outs[q], c, t, fmt);
+  const int q = blockIdx.y;
+  void* out = q == 0 ? out0 : (q == 1 ? out1 : out2);
+  float a = 0.f;
+  if (c < D) {
+    const float* w = ws + (long long)q * nb * D + c;
+    int k = kl;
+    for (; k + 24 < nb; k += 32) {
+      const float v0 = w[(long long)k * D], v1 = w[(long long)(k + 8) * D], v2 = w[(long long)(k + 16) * D],
+                  v3 = w[(long long)(k + 24) * D];
+      a += v0;
+      a += v1;
+      a += v2;
+      a += v3;
     }
+    for (; k < nb; k += 8) a += w[(long long)k * D];
+  }
+  sm[kl][cl] = a;
+  __syncthreads();
+  if (kl == 0 && c < D && out) {
+    float t = 0.f;
+    for (int k = 0; k < 8; ++k) t += sm[k][cl];
+    st_h(out, c, t, fmt);
+  }
 }
 
 // sum ws partials over blocks -> half outputs (ws[0..nb) -> out0, ws[nb..2nb) -> out1)
@@ -338,7 +376,22 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const void* __restr
   const uint16_t* base = static_cast<const uint16_t*>(x) + (long long)z * sbx;
   const bool vec = (c0 + 8 <= cols) && ((ldx & 7) == 0) && ((sbx & 7) == 0) &&
                    ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-  for (int r = r0 + rl; r < r1; r += 8) {
+  int r = r0 + rl;
+  if (vec) {  // four rows in flight per thread (memory-level parallelism), then the tail
+    for (; r + 24 < r1; r += 32) {
+      uint4 w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) w[j] = __ldcs(reinterpret_cast<const uint4*>(base + (long long)(r + 8 * j) * ldx + c0));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float v[8];
+        unpack8(w[j], v, fmt);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += v[e];
+      }
+    }
+  }
+  for (; r < r1; r += 8) {
     if (vec) {
       float v[8];
       unpack8(*reinterpret_cast<const uint4*>(base + (long long)r * ldx + c0), v, fmt);
@@ -927,13 +980,13 @@ int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, 
   MPX_LAUNCH_CHECK("ln_dx_kernel");
   const int cblocks = D / 256;
   const int nsum = dxsum ? 3 : 2;
-  int splits = std::max(1, std::min(rows / 64, current_num_sms() * 4 / cblocks));
+  int splits = std::max(1, std::min(rows / 64, current_num_sms() * 8 / cblocks));
   while ((long long)nsum * splits * D > workspace_floats && splits > 1) splits /= 2;
   const int rps = (rows + splits - 1) / splits;
   ln_colsum_kernel<<<dim3(cblocks, splits), 256, 0, st>>>(x, ldx, mean, rstd, dy, lddy, dxsum ? dx : nullptr, lddx, rows,
                                                          D, rps, workspace, f);
   MPX_LAUNCH_CHECK("ln_colsum_kernel");
-  partials_reduce3_kernel<<<(D + 31) / 32, 256, 0, st>>>(workspace, splits, D, dgain, dbias, dxsum, f);
+  partials_reduce3_kernel<<<dim3((D + 31) / 32, nsum), 256, 0, st>>>(workspace, splits, D, dgain, dbias, dxsum, f);
   MPX_LAUNCH_CHECK("partials_reduce3_kernel");
   return 0;
 }
@@ -944,7 +997,7 @@ int mpx_colsum(int dtype, const void* x, int64_t ldx, int64_t sbx, int rows, int
   if (rows <= 0 || cols <= 0 || batches <= 0) return 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int cblocks = (cols + 255) / 256;
-  const long long target = (long long)current_num_sms() * 4;
+  const long long target = (long long)current_num_sms() * 8;  // one full wave of 256-thread blocks
   int splits = (int)std::max<long long>(1, target / ((long long)cblocks * batches));
   splits = std::min(splits, std::max(1, rows / 64));
   while ((long long)splits * cols * batches > workspace_floats && splits > 1) splits /= 2;
