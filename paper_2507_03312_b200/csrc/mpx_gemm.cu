@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-// split-K: C = cast(sum_s ws[s]) (+ bias)
+// split-K: C = cast(sum_s ws[s]) (+ bias), summed in split order
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int split, long long mn, int N, void* C,
                                      long long ldc, int c_dtype, const void* bias, int ab_fmt) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < mn; i += (long long)gridDim.x * blockDim.x) {
@@ -706,6 +706,58 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int split, lo
       static_cast<float*>(C)[o] = s;
     else
       static_cast<uint16_t*>(C)[o] = f32_to_half(s, c_dtype == MPX_BF16 ? 1 : 0);
+  }
+}
+
+// the same, 4 columns per thread (N % 4 == 0, 16-byte aligned ws), all split
+// loads of a step in flight together; one 2D index per row block, no 64-bit divides
+__global__ void __launch_bounds__(256) splitk_reduce4_kernel(const float* __restrict__ ws, int split, int M, int N,
+                                                             void* C, long long ldc, int c_dtype, const void* bias,
+                                                             int ab_fmt) {
+  const int n4 = N / 4;
+  const long long mn = (long long)M * N;
+  const long long total = (long long)M * n4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(i / n4), c4 = (int)(i - (long long)row * n4);
+    const long long e = (long long)row * N + 4 * c4;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    int k = 0;
+    for (; k + 4 <= split; k += 4) {
+      float4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = __ldcs(reinterpret_cast<const float4*>(ws + (k + j) * mn + e));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a.x += v[j].x;
+        a.y += v[j].y;
+        a.z += v[j].z;
+        a.w += v[j].w;
+      }
+    }
+    for (; k < split; ++k) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(ws + k * mn + e));
+      a.x += v.x;
+      a.y += v.y;
+      a.z += v.z;
+      a.w += v.w;
+    }
+    float o[4] = {a.x, a.y, a.z, a.w};
+    if (bias) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] += half_to_f32(static_cast<const uint16_t*>(bias)[4 * c4 + j], ab_fmt);
+    }
+    const long long off = (long long)row * ldc + 4 * c4;
+    if (c_dtype == MPX_F32) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) static_cast<float*>(C)[off + j] = o[j];
+    } else {
+      const int f = c_dtype == MPX_BF16 ? 1 : 0;
+      const uint2 w = make_uint2(pack2_fmt(o[0], o[1], f), pack2_fmt(o[2], o[3], f));
+      if ((off & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 7) == 0)
+        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(C) + off) = w;
+      else
+        for (int j = 0; j < 4; ++j) static_cast<uint16_t*>(C)[off + j] = f32_to_half(o[j], f);
+    }
   }
 }
 
@@ -962,8 +1014,12 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   MPX_LAUNCH_CHECK("gemm_kernel");
   if (split > 1) {
     const long long mn = (long long)g->M * g->N;
-    splitk_reduce_kernel<<<current_num_sms() * 4, 256, 0, st>>>(P.ws, split, mn, g->N, g->C, g->ldc, g->c_dtype,
-                                                               g->bias, fmt);
+    if (g->N % 4 == 0 && reinterpret_cast<uintptr_t>(P.ws) % 16 == 0)
+      splitk_reduce4_kernel<<<current_num_sms() * 8, 256, 0, st>>>(P.ws, split, g->M, g->N, g->C, g->ldc, g->c_dtype,
+                                                                   g->bias, fmt);
+    else
+      splitk_reduce_kernel<<<current_num_sms() * 4, 256, 0, st>>>(P.ws, split, mn, g->N, g->C, g->ldc, g->c_dtype,
+                                                                 g->bias, fmt);
     MPX_LAUNCH_CHECK("splitk_reduce_kernel");
   }
   return 0;
