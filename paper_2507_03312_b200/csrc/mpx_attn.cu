@@ -310,7 +310,9 @@ __global__ void __launch_bounds__(kAttnThreadsF, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ AttnParams P) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB-aligned by indexing the __shared__ array (not via an integer cast), so
+  // derived pointers stay in the shared window: STS/LDS, 32-bit addressing
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sP = smem;               // P, aliasing Q (0-16K) and K (16K-48K) after MMA1
   uint8_t* sQ = smem;
   uint8_t* sK = smem + kAttnQ;
@@ -433,7 +435,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                     const __grid_constant__ AttnBwdParams P) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB-aligned by indexing the __shared__ array (not via an integer cast), so
+  // derived pointers stay in the shared window: STS/LDS, 32-bit addressing
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   if (reinterpret_cast<uintptr_t>(smem) - reinterpret_cast<uintptr_t>(smem_raw) + kAttnBwdBody > kAttnBwdSmem) __trap();
   uint8_t* sQ = smem;
   uint8_t* sdO = sQ + kAttnQ;

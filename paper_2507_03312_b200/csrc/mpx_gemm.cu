@@ -137,7 +137,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr int S = CG == 1 ? 3 : 5;           // smem ring depth (48 / 32 KB stages)
   constexpr int BT = kBTileBytes / CG;         // B bytes per stage per CTA
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB-aligned by indexing the __shared__ array (not via an integer cast), so
+  // derived pointers stay in the shared window: STS/LDS, 32-bit addressing
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * kATileBytes;
   uint8_t* stage_epi = sB + S * BT;  // kEpiWarps x kBufPerWarp x 4 KB staging
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // ---- softmax modes: row statistics over this warp's column groups,
       // combined with the partner warp (same TMEM lane quarter) through smem
       float row_m = 0.f, row_inv = 1.f, row_t = 0.f;
-      const bool smx = P.act == ACT_SOFTMAX || P.act == ACT_SOFTMAX_BWD;
+      const bool smx = XO == XOP_NONE && (P.act == ACT_SOFTMAX || P.act == ACT_SOFTMAX_BWD);
       auto round_half = [&](float x) { return half_to_f32(f32_to_half(x, P.ab_fmt), P.ab_fmt); };
       if (smx) {
         float m = -INFINITY, l = 0.f, tacc = 0.f;
