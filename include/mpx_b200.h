@@ -169,6 +169,13 @@ typedef struct mpx_gemm_desc {
   void* workspace;
   int cta_group; /* 0 = auto, 1 = one CTA per 128-row tile, 2 = CTA pair per 256-row tile */
   int tma_store; /* 0 = auto (16-bit C through smem + TMA stores), -1 = direct stores */
+  /* optional fused column sum of the stored C (the next layer's bias gradient,
+   * _unbroadcast autodiff.py:88-99): colsum_out[n] = sum_m C[m,n] over the
+   * rounded C values, through colsum_ws (>= ceil(M/32)*N f32) in two
+   * deterministic passes.  Needs the staged epilogue (batch 1, split_k 1, 16-bit
+   * C, no GELU-aux-out); colsum_out has C's dtype. */
+  float* colsum_ws;
+  void* colsum_out;
 } mpx_gemm_desc;
 
 int mpx_gemm(const mpx_gemm_desc* desc, void* stream);

@@ -58,6 +58,7 @@ class GemmDescC(ctypes.Structure):
         ("aux", ctypes.c_void_p), ("ld_aux", ctypes.c_int64),
         ("alpha", ctypes.c_float), ("act", ctypes.c_int), ("block_n", ctypes.c_int), ("split_k", ctypes.c_int),
         ("workspace", ctypes.c_void_p), ("cta_group", ctypes.c_int), ("tma_store", ctypes.c_int),
+        ("colsum_ws", ctypes.c_void_p), ("colsum_out", ctypes.c_void_p),
     ]
 
 

@@ -75,6 +75,7 @@ struct GemmParams {
   float alpha;
   int act;
   float* ws;  // split-K partials [split][M][N] (f32)
+  float* csum;  // fused column sum: per-32-row partials [ceil(M/32)][N] (f32), or null
   int tma_store;  // 16-bit C written through swizzled smem staging + TMA bulk stores
   int xop;        // epilogue operand through TMA (tmX): 0 none, 1 residual in, 2 aux in (GELU'), 3 aux out (GELU)
 };
@@ -635,6 +636,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (!batched && kXin && j + 1 < my_groups) x_load(g + kEpiPerQ, gcount + 1);  // next group's operand
           }
         }
+        if (XO != XOP_NONE && XO != XOP_AUX_OUT && P.csum != nullptr && batched && row0 < P.M) {
+          // fused column sum of the staged (rounded) C: lane l sums columns 2l, 2l+1
+          // of each group over this warp's 32 rows (conflict-free: one row per step)
+          __syncwarp();
+          for (int j = 0; j < my_groups; ++j) {
+            const int g = h + kEpiPerQ * j;
+            const int nch = min(GW / 16, (P.BN - g * GW) / 16);
+            const uint32_t base = smem_u32(buf(j)) + ((lane & 3) << 2);
+            float s0 = 0.f, s1 = 0.f;
+#pragma unroll 8
+            for (int rr = 0; rr < 32; ++rr) {
+              uint32_t w;
+              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w) : "r"(base + rr * 128 + (((lane >> 2) ^ (rr & 7)) << 4)));
+              s0 += half_to_f32((uint16_t)(w & 0xFFFFu), cf);
+              s1 += half_to_f32((uint16_t)(w >> 16), cf);
+            }
+            const int col = n0 + g * GW + 2 * lane;
+            if (2 * lane < nch * 16 && col < P.N) {
+              float* o = P.csum + (long long)(row0 >> 5) * P.N + col;
+              o[0] = s0;
+              if (col + 1 < P.N) o[1] = s1;
+            }
+          }
+        }
       } else {
         uint32_t r[16];
         const int chunk0 = h * 16;
@@ -692,6 +717,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tmem_dealloc_2sm<512>(tmem_base);
     else
       tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// fused column sum, second pass: out[c] = sum_k parts[k][c] over many partial
+// rows; block = 32 columns x 32 partial lanes, four rows in flight per
+// thread, fixed summation order
+__global__ void __launch_bounds__(1024) colsum_parts_kernel(const float* __restrict__ parts, int nparts, int N,
+                                                            void* out, int out_dtype) {
+  __shared__ float sm[32][33];
+  const int cl = threadIdx.x & 31, kl = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
+  float a = 0.f;
+  if (c < N) {
+    const float* w = parts + c;
+    int k = kl;
+    for (; k + 96 < nparts; k += 128) {
+      const float v0 = w[(long long)k * N], v1 = w[(long long)(k + 32) * N], v2 = w[(long long)(k + 64) * N],
+                  v3 = w[(long long)(k + 96) * N];
+      a += v0;
+      a += v1;
+      a += v2;
+      a += v3;
+    }
+    for (; k < nparts; k += 32) a += w[(long long)k * N];
+  }
+  sm[kl][cl] = a;
+  __syncthreads();
+  if (kl == 0 && c < N) {
+    float t = 0.f;
+    for (int k = 0; k < 32; ++k) t += sm[k][cl];
+    if (out_dtype == MPX_F32)
+      static_cast<float*>(out)[c] = t;
+    else
+      static_cast<uint16_t*>(out)[c] = f32_to_half(t, out_dtype == MPX_BF16 ? 1 : 0);
   }
 }
 
@@ -907,6 +966,7 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   P.alpha = g->alpha == 0.f ? 1.f : g->alpha;
   P.act = g->act;
   P.ws = static_cast<float*>(g->workspace);
+  P.csum = nullptr;
   if (split > 1 && (long long)(split - 1) * P.kb_per_split >= P.k_blocks)
     return fail(MPX_EINVAL, "mpx_gemm: split_k too large for K");
 
@@ -992,6 +1052,14 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
         attr_err = cudaFuncSetAttribute(kernels[c][x], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
   });
   if (attr_err != cudaSuccess) return fail((int)attr_err, "cudaFuncSetAttribute(gemm_kernel)");
+  // fused column sum: in the staged lean epilogues (16-bit C, one batch), else a separate pass
+  bool csum_fused = false;
+  if (g->colsum_out) {
+    if (!g->colsum_ws) return fail(MPX_EINVAL, "mpx_gemm: colsum_out needs colsum_ws");
+    csum_fused = P.tma_store && split == 1 && g->c_dtype != MPX_F32 && nb1 * nb2 == 1 && P.xop != XOP_NONE &&
+                 P.xop != XOP_AUX_OUT && BN <= 64 * kEpiPerQ * kBufPerWarp;
+    if (csum_fused) P.csum = g->colsum_ws;
+  }
   const KernelFn kern = kernels[CG - 1][P.xop];
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (CG == 1) {
@@ -1023,6 +1091,18 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
       splitk_reduce_kernel<<<current_num_sms() * 4, 256, 0, st>>>(P.ws, split, mn, g->N, g->C, g->ldc, g->c_dtype,
                                                                  g->bias, fmt);
     MPX_LAUNCH_CHECK("splitk_reduce_kernel");
+  }
+  if (g->colsum_out) {
+    if (csum_fused) {
+      const int parts = (g->M + 31) / 32;
+      colsum_parts_kernel<<<(unsigned)((g->N + 31) / 32), 1024, 0, st>>>(g->colsum_ws, parts, g->N, g->colsum_out,
+                                                                         g->c_dtype);
+      MPX_LAUNCH_CHECK("colsum_parts_kernel");
+    } else {
+      const int rc2 = mpx_colsum(g->c_dtype, g->C, g->ldc, 0, g->M, g->N, 1, g->colsum_ws,
+                                 (int64_t)((g->M + 31) / 32) * g->N, g->colsum_out, g->N, g->c_dtype, 1.f, stream);
+      if (rc2) return rc2;
+    }
   }
   return 0;
 }

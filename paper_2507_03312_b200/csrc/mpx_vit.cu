@@ -423,8 +423,19 @@ __global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restri
   const long long n = (long long)cols * batches;
   const long long z = i / cols, c = i - z * cols;
   float a = 0.f;
-  if (i < n)
-    for (int k = kl; k < splits; k += 8) a += ws[(z * splits + k) * cols + c];
+  if (i < n) {
+    const float* w = ws + z * splits * cols + c;
+    int k = kl;
+    for (; k + 24 < splits; k += 32) {  // four partial rows in flight, summed in order
+      const float v0 = w[(long long)k * cols], v1 = w[(long long)(k + 8) * cols], v2 = w[(long long)(k + 16) * cols],
+                  v3 = w[(long long)(k + 24) * cols];
+      a += v0;
+      a += v1;
+      a += v2;
+      a += v3;
+    }
+    for (; k < splits; k += 8) a += w[(long long)k * cols];
+  }
   sm[kl][cl] = a;
   __syncthreads();
   if (kl == 0 && i < n) {

@@ -109,7 +109,7 @@ class ViTEngine:
         if self.hw_pad is not None:
             self.hw_pad.zero_()
         self.dhw_pad = e(D, self.ldl) if c.classes % 8 else None
-        self.ws_floats = max(8 * 1024 * 1024, 2 * (D * 3 * D), 3 * c.mlp * D)
+        self.ws_floats = max(8 * 1024 * 1024, 2 * (D * 3 * D), 3 * c.mlp * D, VK.colsum_ws_numel(self.M, c.mlp))
         self.ws = f(self.ws_floats)
         self.lib = _nat.load()
 
@@ -264,10 +264,11 @@ class ViTEngine:
             q = f"blocks.{i}."
             # fc2: x_{i+1} = h @ W2 + b2 + xm
             VK.linear_wgrad(self.h[i], dX, out=g[q + "fc2.w"])  # fc2.b came with the LN backward above
-            VK.linear_dgrad(dX, p[q + "fc2.w"], aux=self.pre[i], out=self.dpre)  # dpre = (dX W2^T) * gelu'(pre)
+            # dpre = (dX W2^T) * gelu'(pre); its column sum (the fc1.b grad) fused into the epilogue
+            VK.linear_dgrad(dX, p[q + "fc2.w"], aux=self.pre[i], out=self.dpre, colsum_out=g[q + "fc1.b"],
+                            colsum_ws=self.ws)
             # fc1: pre = bn @ W1 + b1
             VK.linear_wgrad(self.bn[i], self.dpre, out=g[q + "fc1.w"])
-            self._colsum(self.dpre, c.mlp, M, c.mlp, g[q + "fc1.b"])
             VK.linear_dgrad(self.dpre, p[q + "fc1.w"], out=self.dA)
             # LN2 (+ residual): dxm = LN2'(dA) + dX; colsum(dxm) = proj.b grad
             self._ln_bwd2(self.xm[i], D, p[q + "ln2.g"], self.mu2[i], self.rs2[i], self.dA, D, dX, self.dXm, D,

@@ -21,7 +21,7 @@ def _ptr(t):
 def gemm(A, B, *, M, N, K, lda, ldb, a_mn=False, b_mn=False, out=None, ldc=None, out_dtype=None, bias=None,
          residual=None, ldr=None, aux=None, ld_aux=None, act=ACT_NONE, alpha=1.0, nb=(1, 1), a_sb=(0, 0),
          b_sb=(0, 0), c_sb=(0, 0), r_sb=(0, 0), split_k=1, workspace=None, block_n=0, cta_group=0,
-         tma_store=0):
+         tma_store=0, colsum_out=None, colsum_ws=None):
     """C = epi(alpha * A @ B) on the tcgen05 GEMM (see mpx_gemm_desc)."""
     require_cuda([A, B], "gemm")
     if A.dtype != B.dtype or A.dtype not in (torch.float16, torch.bfloat16):
@@ -52,8 +52,18 @@ def gemm(A, B, *, M, N, K, lda, ldb, a_mn=False, b_mn=False, out=None, ldc=None,
     d.workspace = _ptr(workspace)
     d.cta_group = cta_group
     d.tma_store = tma_store
+    if colsum_out is not None:
+        if colsum_ws is None:
+            colsum_ws = torch.empty(colsum_ws_numel(M, N), dtype=torch.float32, device=A.device)
+        assert colsum_ws.dtype == torch.float32 and colsum_ws.numel() >= colsum_ws_numel(M, N)
+        d.colsum_ws, d.colsum_out = colsum_ws.data_ptr(), colsum_out.data_ptr()
     _nat.check(_nat.load().mpx_gemm(ctypes.byref(d), stream_handle(A.device)), "mpx_gemm")
     return out
+
+
+def colsum_ws_numel(M: int, N: int) -> int:
+    """f32 workspace of the GEMM's fused column sum: one partial row per 32 rows of C."""
+    return -(-M // 32) * N
 
 
 # ---------------------------------------------------------------- linears
@@ -65,14 +75,15 @@ def linear_fwd(x, w, bias=None, act=ACT_NONE, aux=None, residual=None, out=None,
                 out=out, ldc=N_ if out is not None else None, cta_group=cta_group)
 
 
-def linear_dgrad(dy, w, aux=None, out=None, cta_group=0):
+def linear_dgrad(dy, w, aux=None, out=None, cta_group=0, colsum_out=None, colsum_ws=None):
     """dx[M,K] = dy[M,N] @ w[K,N]^T; with aux (the GELU pre-activation of
-    this layer's input) the GELU derivative is applied in the epilogue."""
+    this layer's input) the GELU derivative is applied in the epilogue;
+    colsum_out receives sum_m dx[m,:] (the producing layer's bias gradient)."""
     M, N_ = dy.shape
     K = w.shape[0]
     return gemm(dy, w, M=M, N=K, K=N_, lda=N_, ldb=N_, aux=aux, ld_aux=K,
                 act=ACT_GELU_BWD if aux is not None else ACT_NONE, out=out, ldc=K if out is not None else None,
-                cta_group=cta_group)
+                cta_group=cta_group, colsum_out=colsum_out, colsum_ws=colsum_ws)
 
 
 _SMS: dict = {}

@@ -162,3 +162,30 @@ def test_softmax_epilogues(cuda, dt, Nt):
     ph = P[..., :Nt].float()
     want = ph * (dp - (ph * dp).sum(-1, keepdim=True))
     close(dS[..., :Nt], want, rel=2e-2)
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("shape", [(1000, 384, 256), (4096, 768, 3072), (333, 200, 128)])
+def test_fused_colsum(cuda, dt, shape):
+    """colsum_out = sum over rows of the stored (rounded) C, for the plain,
+    GELU'-with-aux and bias+residual epilogues and the split-K fallback."""
+    M, N, K = shape
+    g = torch.Generator(device=cuda).manual_seed(M)
+    x = torch.randn(M, K, device=cuda, generator=g).to(dt)
+    w = (torch.randn(N, K, device=cuda, generator=g) * 0.05).to(dt)
+    aux = torch.randn(M, N, device=cuda, generator=g).to(dt)
+    bias = torch.randn(N, device=cuda, generator=g).to(dt)
+    res = torch.randn(M, N, device=cuda, generator=g).to(dt)
+    for kw in ({}, {"aux": aux}):
+        cs = torch.empty(N, device=cuda, dtype=dt)
+        y = VK.linear_dgrad(x, w, colsum_out=cs, **kw)
+        want = y.float().sum(0)
+        assert torch.allclose(cs.float(), want, rtol=1e-2, atol=1e-2 * want.abs().max().item()), kw.keys()
+    cs = torch.empty(N, device=cuda, dtype=dt)
+    y = VK.gemm(x, w, M=M, N=N, K=K, lda=K, ldb=K, bias=bias, residual=res, colsum_out=cs)
+    want = y.float().sum(0)
+    assert torch.allclose(cs.float(), want, rtol=1e-2, atol=1e-2 * want.abs().max().item())
+    cs = torch.empty(N, device=cuda, dtype=dt)
+    y = VK.gemm(x, w, M=M, N=N, K=K, lda=K, ldb=K, split_k=2, colsum_out=cs)
+    want = y.float().sum(0)
+    assert torch.allclose(cs.float(), want, rtol=1e-2, atol=1e-2 * want.abs().max().item())
