@@ -229,9 +229,11 @@ int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H, int hd, f
 /* K6 fused attention backward: given qkv and dO [B*N, H*hd], writes the whole
  * dqkv [B*N, 3*H*hd] (dQ = scale dS K, dK = scale dS^T Q, dV = P^T dO with
  * dS = P (dP - rowsum(P dP)), dP = dO V^T, P recomputed on chip — from the
- * forward's row_stats when given, else from the scores here; same P bits). */
+ * forward's row_stats when given, else from the scores here; same P bits).
+ * colsum_ws (f32 [B*3*H*hd]) + colsum_out (3*H*hd, dtype), both or neither:
+ * colsum_out = sum over rows of the stored dqkv (the qkv bias gradient). */
 int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int B, int N, int H, int hd, float scale,
-                      void* dqkv, const float* row_stats, void* stream);
+                      void* dqkv, const float* row_stats, float* colsum_ws, void* colsum_out, void* stream);
 /* image [B,H,W,C] -> patch rows [B*(H/P)*(W/P), P*P*C], order (py, px, c) */
 int mpx_patchify(int dtype, const void* img, void* patches, int B, int H, int W, int C, int P, void* stream);
 /* strided row copy dst[b][r][c] = src[b][r][c] */

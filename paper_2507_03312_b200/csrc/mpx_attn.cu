@@ -428,7 +428,27 @@ struct AttnBwdParams {
   void* dqkv;  // [B*N, 3*H*hd]
   long long ld;
   const float2* stats;  // the forward's row statistics, or null (recomputed here)
+  float* csum;          // optional per-image column sums of dqkv [B][3*H*hd] (the qkv bias gradient's partials)
 };
+
+// 16 values per lane -> column sums over the warp's 32 lanes (rows) by recursive
+// halving (16 shuffles, fixed order); returns the sum of column col16(lane)
+__device__ __forceinline__ float warp_colsum16(float* v, int lane) {
+#pragma unroll
+  for (int w = 8, m = 16; w >= 1; w >>= 1, m >>= 1) {
+    const bool up = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? v[i] : v[i + w];
+      const float keep = up ? v[i + w] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+__device__ __forceinline__ int col16(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
 
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -553,6 +573,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       for (int i = 0; i < 8; ++i) unpack2(u[i], P.fmt, pv[2 * i], pv[2 * i + 1]);
     };
     constexpr int kMaxC = 16 / kSplit;  // chunks per thread
+    static_assert(kSplit == 4, "dQ readout: one chunk per split");
+    float qsum = 0.f;  // column col16(lane) of chunk `split` of dQ, summed over this warp's rows and the tiles
     for (int t = 0; t < T; ++t) {
       const uint32_t ph = t & 1;
       // ---- P = softmax(round(S * scale)) -> smem (as in the forward)
@@ -622,17 +644,27 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tc_fence_after();
       const int qrow = t * 128 + r;
       uint16_t* o = static_cast<uint16_t*>(P.dqkv) + ((long long)b * P.N + qrow) * P.ld + (long long)h * P.hd;
-      for (int c = split; c < 4; c += kSplit) {
+      {
+        const int c = split;  // kSplit == 4: one 16-column chunk of dQ per thread
         uint32_t a[16];
         tmem_ld16(trow + c * 16, a);
         tmem_ld_wait();
-        if (qrow < P.N) {
-          uint32_t pk[8];
+        uint32_t pk[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * P.scale, __uint_as_float(a[2 * i + 1]) * P.scale, P.fmt);
+        for (int i = 0; i < 8; ++i)
+          pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * P.scale, __uint_as_float(a[2 * i + 1]) * P.scale, P.fmt);
+        if (qrow < P.N) {
           *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+        if (P.csum) {  // column sums of the stored (rounded) dQ rows
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            unpack2(pk[i], P.fmt, v[2 * i], v[2 * i + 1]);
+            if (qrow >= P.N) v[2 * i] = v[2 * i + 1] = 0.f;
+          }
+          qsum += warp_colsum16(v, lane);
         }
       }
       tc_fence_before();
@@ -640,8 +672,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (warp == 4 && lane == 0) ATRACE(8 + 8 * t);
     }
     // ---- dV, dK (keys r and 128 + r of this head): 4 (half, which) combos split over the warps
-    for (int combo = split; combo < 4; combo += kSplit) {
-      const int half = combo >> 1, which = combo & 1;
+    float kvsum[4] = {0.f, 0.f, 0.f, 0.f};  // per chunk: column col16(lane), this warp's 32 keys
+    const int half = split >> 1, which = split & 1;  // kSplit == 4: one combo per split
+    {
       const int key = half * 128 + r;
       uint16_t* o = static_cast<uint16_t*>(P.dqkv) + ((long long)b * P.N + key) * P.ld + (which ? D : 2 * D) +
                     (long long)h * P.hd;
@@ -650,14 +683,43 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         uint32_t a[16];
         tmem_ld16(trow + 256 + which * 128 + half * 64 + c * 16, a);
         tmem_ld_wait();
-        if (key < P.N) {
-          uint32_t pk[8];
+        uint32_t pk[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * mul, __uint_as_float(a[2 * i + 1]) * mul, P.fmt);
+        for (int i = 0; i < 8; ++i)
+          pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * mul, __uint_as_float(a[2 * i + 1]) * mul, P.fmt);
+        if (key < P.N) {
           *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
+        if (P.csum) {
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            unpack2(pk[i], P.fmt, v[2 * i], v[2 * i + 1]);
+            if (key >= P.N) v[2 * i] = v[2 * i + 1] = 0.f;
+          }
+          kvsum[c] = warp_colsum16(v, lane);
+        }
+      }
+    }
+    if (P.csum) {
+      // combine the warps' partials through the (now idle) Q tile: slots
+      // [part q/k/v][quarter (and key half)][64 columns], then one fixed-order sum
+      float* sc = reinterpret_cast<float*>(sQ);
+      if ((lane & 1) == 0) {
+        sc[(0 * 8 + qd) * 64 + split * 16 + col16(lane)] = qsum;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          sc[((1 + (which ? 0 : 1)) * 8 + half * 4 + qd) * 64 + c * 16 + col16(lane)] = kvsum[c];
+      }
+      asm volatile("bar.sync 6, %0;" ::"n"(128 * kSplit) : "memory");
+      const int tid = threadIdx.x - 128;
+      if (tid < 192) {
+        const int part = tid >> 6, col = tid & 63;  // part 0 q, 1 k, 2 v
+        float a = 0.f;
+        const int nslot = part == 0 ? 4 : 8;
+        for (int j = 0; j < nslot; ++j) a += sc[(part * 8 + j) * 64 + col];
+        P.csum[(long long)b * 3 * D + part * D + (long long)h * P.hd + col] = a;
       }
     }
   }
@@ -669,6 +731,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tmem_dealloc<512>(tmem);
   }
 }
+
+// the column-sum second pass (mpx_vit.cu)
+__global__ void colsum_final_kernel(const float* __restrict__ ws, int splits, int cols, int batches, void* out,
+                                    long long ld_out, int out_dtype, float alpha);
 
 static PFN_cuTensorMapEncodeTiled_v12000 attn_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -746,7 +812,8 @@ extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H
 }
 
 extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int B, int N, int H, int hd, float scale,
-                                 void* dqkv, const float* row_stats, void* stream) {
+                                 void* dqkv, const float* row_stats, float* colsum_ws, void* colsum_out,
+                                 void* stream) {
   if (dtype != MPX_F16 && dtype != MPX_BF16) return fail(MPX_EINVAL, "attention: f16/bf16 only");
   if (hd != 64 || N < 1 || N > 256) return fail(MPX_EINVAL, "attention_bwd: fused path needs hd == 64, N <= 256");
   const int fmt = dtype == MPX_BF16 ? 1 : 0;
@@ -768,6 +835,9 @@ extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int
   P.dqkv = dqkv;
   P.ld = 3LL * D;
   P.stats = reinterpret_cast<const float2*>(row_stats);
+  if ((colsum_ws == nullptr) != (colsum_out == nullptr))
+    return fail(MPX_EINVAL, "attention_bwd: colsum_ws and colsum_out go together");
+  P.csum = colsum_ws;
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
@@ -777,5 +847,11 @@ extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int
   attn_bwd_kernel<<<(unsigned)(B * H), kAttnThreads, kAttnBwdSmem, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, tdo,
                                                                                                        P);
   MPX_LAUNCH_CHECK("attn_bwd_kernel");
+  if (colsum_out) {  // the qkv bias gradient: sum the per-image partials [B][3D]
+    const int cols = 3 * D;
+    colsum_final_kernel<<<(unsigned)((cols + 31) / 32), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        colsum_ws, B, cols, 1, colsum_out, cols, dtype, 1.f);
+    MPX_LAUNCH_CHECK("colsum_final_kernel");
+  }
   return 0;
 }

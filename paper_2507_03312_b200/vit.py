@@ -279,13 +279,14 @@ class ViTEngine:
             VK.linear_dgrad(dXm, p[q + "proj.w"], out=self.dO)
             # attention
             qkv, dqkv = self.qkv[i], self.dqkv
-            if self.fused_attn:
-                VK.attention_bwd(qkv, self.dO, B, S, H, hd, scale, dqkv=dqkv, stats=self.attn_stats[i])
+            if self.fused_attn:  # (the qkv.b gradient, colsum(dqkv), comes out of the kernel)
+                VK.attention_bwd(qkv, self.dO, B, S, H, hd, scale, dqkv=dqkv, stats=self.attn_stats[i],
+                                 colsum_out=g[q + "qkv.b"], colsum_ws=self.ws)
             else:
                 self._attention_bwd_unfused(i, qkv, dqkv, scale)
+                self._colsum(dqkv, 3 * D, M, 3 * D, g[q + "qkv.b"])
             # qkv = a @ Wqkv + bqkv
             VK.linear_wgrad(self.a[i], dqkv, out=g[q + "qkv.w"])
-            self._colsum(dqkv, 3 * D, M, 3 * D, g[q + "qkv.b"])
             VK.linear_dgrad(dqkv, p[q + "qkv.w"], out=self.dA)
             # LN1 (+ residual): dX = LN1'(dA) + dXm; colsum(dX) = fc2.b grad of the block below
             self._ln_bwd2(self.x[i], D, p[q + "ln1.g"], self.mu1[i], self.rs1[i], self.dA, D, dXm, dX, D,

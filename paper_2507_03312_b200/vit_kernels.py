@@ -155,15 +155,23 @@ def attention_fwd(qkv, B: int, N: int, H: int, hd: int, scale: float, out=None, 
     return out
 
 
-def attention_bwd(qkv, dO, B: int, N: int, H: int, hd: int, scale: float, dqkv=None, stats=None):
+def attention_bwd(qkv, dO, B: int, N: int, H: int, hd: int, scale: float, dqkv=None, stats=None,
+                  colsum_out=None, colsum_ws=None):
     """Fused attention backward: the whole dqkv [B*N, 3*H*hd] from qkv and dO
-    (with the forward's `stats`, P is rebuilt without the statistics passes)."""
+    (with the forward's `stats`, P is rebuilt without the statistics passes);
+    colsum_out [3*H*hd] receives sum over rows of dqkv (the qkv bias gradient)."""
     require_cuda([qkv, dO], "attention_bwd")
     if dqkv is None:
         dqkv = torch.empty_like(qkv)
     if stats is not None:
         assert stats.dtype == torch.float32 and stats.numel() >= attention_stats_numel(B, N, H)
+    if colsum_out is not None and colsum_ws is None:
+        colsum_ws = torch.empty(B * 3 * H * hd, dtype=torch.float32, device=qkv.device)
+    if colsum_ws is not None:
+        assert colsum_ws.dtype == torch.float32 and colsum_ws.numel() >= B * 3 * H * hd
     _nat.check(_nat.load().mpx_attention_bwd(_CODE[qkv.dtype], qkv.data_ptr(), dO.data_ptr(), B, N, H, hd, scale,
                                              dqkv.data_ptr(), stats.data_ptr() if stats is not None else None,
+                                             colsum_ws.data_ptr() if colsum_out is not None else None,
+                                             colsum_out.data_ptr() if colsum_out is not None else None,
                                              stream_handle(qkv.device)), "mpx_attention_bwd")
     return dqkv

@@ -125,6 +125,11 @@ def test_fused_attention_backward(cuda, dt, Nt):
     stats = torch.empty(VK.attention_stats_numel(Bsz, Nt, H), device=cuda)
     VK.attention_fwd(qkv, Bsz, Nt, H, hd, 0.125, stats=stats)
     assert torch.equal(VK.attention_bwd(qkv, dO, Bsz, Nt, H, hd, 0.125, stats=stats), dqkv)
+    # fused bias gradient: colsum over the stored dqkv rows
+    cs = torch.empty(3 * D, device=cuda, dtype=dt)
+    assert torch.equal(VK.attention_bwd(qkv, dO, Bsz, Nt, H, hd, 0.125, stats=stats, colsum_out=cs), dqkv)
+    want = dqkv.float().sum(0)
+    assert torch.allclose(cs.float(), want, rtol=1e-2, atol=1e-2 * want.abs().max().item())
     x = qkv.float().requires_grad_(True)
     q, k, v = (x.view(Bsz, Nt, 3, H, hd)[:, :, i] for i in range(3))
     p = torch.softmax(torch.einsum("bnhd,bmhd->bhnm", q, k) * 0.125, -1)
