@@ -167,69 +167,78 @@ __device__ __forceinline__ void round_scores16(const uint32_t* a, float scale, i
             sv[2 * i], sv[2 * i + 1]);
 }
 
-// Forward softmax of row r over the chunks c = split, split + NS, ... < n_chunks:
-//   pass 1  row max of the rounded scores (no exponentials)
-//   pass 2  e = exp(s - M), row sum; e goes back into the same TMEM columns
-//   pass 3  P = e / L rounded to half, into the K-major P tile
-// One exponential per score; the masked tail (keys >= N) only in the last chunk.
+// Forward softmax of row r over the chunks c = split, split + NS, ... < n_chunks,
+// two TMEM passes (TMEM reads bound this kernel: 64 B/clk per SM):
+//   pass 1  online: running max m, e = exp(s - m) written back into the same
+//           TMEM columns, running sum rescaled when m grows; m kept per chunk
+//   pass 2  P = e * exp(m_chunk - M) / L rounded to half, into the K-major P tile
+// The masked tail (keys >= N) only touches the last chunk.
 template <int NS>
 __device__ __forceinline__ void softmax_fwd_p(uint32_t trow, int split, int r, int q, int N, float scale, int fmt,
                                               float* red, uint8_t* sP, float2* stats) {
   constexpr float kLog2e = 1.4426950408889634f;
+  constexpr int kMaxC = (16 + NS - 1) / NS;
   const int n_chunks = (N + 15) / 16;
   const int tail = N - (n_chunks - 1) * 16;  // valid keys in the last chunk (1..16)
-  float m = -INFINITY;
-  for (int c = split; c < n_chunks; c += NS) {
-    uint32_t a[16];
-    tmem_ld16(trow + c * 16, a);
-    tmem_ld_wait();
-    float sv[16];
-    round_scores16(a, scale, fmt, sv);
-    if (c == n_chunks - 1) {
+  float m = -INFINITY, l = 0.f;
+  float mc[kMaxC];  // running max used for each of this thread's chunks
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (i >= tail) sv[i] = -INFINITY;
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) m = fmaxf(m, sv[i]);
-  }
-  red[split * 128 + r] = m;
-  quarter_sync<NS>(q);
-  float M = -INFINITY;
-#pragma unroll
-  for (int j = 0; j < NS; ++j) M = fmaxf(M, red[j * 128 + r]);
-  const float ml = M * kLog2e;
-  float l = 0.f;
-  for (int c = split; c < n_chunks; c += NS) {
+  for (int j = 0; j < kMaxC; ++j) {
+    const int c = split + j * NS;
+    mc[j] = -INFINITY;
+    if (c >= n_chunks) continue;
     uint32_t a[16];
     tmem_ld16(trow + c * 16, a);
     tmem_ld_wait();
     float sv[16];
     round_scores16(a, scale, fmt, sv);
     const int lim = c == n_chunks - 1 ? tail : 16;
+    float cm = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < lim) cm = fmaxf(cm, sv[i]);
+    if (cm > m) {
+      if (m != -INFINITY) l *= ex2_approx((m - cm) * kLog2e);
+      m = cm;
+    }
+    mc[j] = m;
+    const float ml = m * kLog2e;
+    float add = 0.f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const float e = i < lim ? ex2_approx(fmaf(sv[i], kLog2e, -ml)) : 0.f;
-      l += e;
+      add += e;
       a[i] = __float_as_uint(e);
     }
+    l += add;
     tmem_st16(trow + c * 16, a);
   }
+  red[split * 128 + r] = m;
   red[NS * 128 + split * 128 + r] = l;
   quarter_sync<NS>(q);
+  float M = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < NS; ++j) M = fmaxf(M, red[j * 128 + r]);
   float L = 0.f;
 #pragma unroll
-  for (int j = 0; j < NS; ++j) L += red[NS * 128 + j * 128 + r];
+  for (int j = 0; j < NS; ++j) {
+    const float mj = red[j * 128 + r];
+    if (mj != -INFINITY) L += red[NS * 128 + j * 128 + r] * ex2_approx((mj - M) * kLog2e);
+  }
   const float inv = 1.f / L;
   if (stats != nullptr && split == 0) *stats = make_float2(M, inv);
   tmem_st_wait();
-  for (int c = split; c < n_chunks; c += NS) {
+#pragma unroll
+  for (int j = 0; j < kMaxC; ++j) {
+    const int c = split + j * NS;
+    if (c >= n_chunks) continue;
     uint32_t a[16];
     tmem_ld16(trow + c * 16, a);
     tmem_ld_wait();
+    const float f = ex2_approx((mc[j] - M) * kLog2e) * inv;
     uint32_t pk[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * inv, __uint_as_float(a[2 * i + 1]) * inv, fmt);
+    for (int i = 0; i < 8; ++i) pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * f, __uint_as_float(a[2 * i + 1]) * f, fmt);
     store_p_chunk(sP, c, r, pk);
   }
 }
@@ -247,8 +256,8 @@ __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, i
     const float2 st = *stats;
     M = st.x;
     inv = st.y;
-  } else {
-    float m = -INFINITY;
+  } else {  // the forward's statistics, recomputed in its order (online max / rescaled sum)
+    float m = -INFINITY, l = 0.f;
     for (int c = split; c < n_chunks; c += NS) {
       uint32_t a[16];
       tmem_ld16(trow + c * 16, a);
@@ -256,34 +265,35 @@ __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, i
       float sv[16];
       round_scores16(a, scale, fmt, sv);
       const int lim = c == n_chunks - 1 ? tail : 16;
+      float cm = -INFINITY;
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if (i < lim) m = fmaxf(m, sv[i]);
+        if (i < lim) cm = fmaxf(cm, sv[i]);
+      if (cm > m) {
+        if (m != -INFINITY) l *= ex2_approx((m - cm) * kLog2e);
+        m = cm;
+      }
+      const float mlc = m * kLog2e;
+      float add = 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) add += i < lim ? ex2_approx(fmaf(sv[i], kLog2e, -mlc)) : 0.f;
+      l += add;
     }
     red[split * 128 + r] = m;
     quarter_sync<NS>(q);
     M = -INFINITY;
 #pragma unroll
     for (int j = 0; j < NS; ++j) M = fmaxf(M, red[j * 128 + r]);
-    quarter_sync<NS>(q);  // one scratch row set (the backward's smem is full)
-    const float ml = M * kLog2e;
-    float l = 0.f;
-    for (int c = split; c < n_chunks; c += NS) {
-      uint32_t a[16];
-      tmem_ld16(trow + c * 16, a);
-      tmem_ld_wait();
-      float sv[16];
-      round_scores16(a, scale, fmt, sv);
-      const int lim = c == n_chunks - 1 ? tail : 16;
+    float mj[NS];
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (i < lim) l += ex2_approx(fmaf(sv[i], kLog2e, -ml));
-    }
+    for (int j = 0; j < NS; ++j) mj[j] = red[j * 128 + r];
+    quarter_sync<NS>(q);  // one scratch row set (the backward's smem is full)
     red[split * 128 + r] = l;
     quarter_sync<NS>(q);
     float L = 0.f;
 #pragma unroll
-    for (int j = 0; j < NS; ++j) L += red[j * 128 + r];
+    for (int j = 0; j < NS; ++j)
+      if (mj[j] != -INFINITY) L += red[j * 128 + r] * ex2_approx((mj[j] - M) * kLog2e);
     quarter_sync<NS>(q);  // red[] is reused by the caller
     inv = 1.f / L;
   }
