@@ -185,10 +185,15 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
     h_img.copy_(images)
     h_lab = torch.empty(labels.shape, dtype=torch.int32, pin_memory=True)
     h_lab.copy_(labels)
-    # the graph reads `images`/`labels`: land the host copies there (single
-    # buffer, the copy of step j+1 waits for step j's cast/patchify)
-    d_img = [images, images] if use_graph else [torch.empty_like(images), torch.empty_like(images)]
-    d_lab = [labels, labels] if use_graph else [torch.empty_like(labels), torch.empty_like(labels)]
+    # double-buffered device inputs; with graphs, one captured step per buffer
+    # (both share every state buffer), so the copy of step j+1 overlaps step j
+    d_img = [torch.empty_like(images), torch.empty_like(images)]
+    d_lab = [torch.empty_like(labels), torch.empty_like(labels)]
+    if use_graph:
+        for b in range(2):
+            d_img[b].copy_(images)
+            d_lab[b].copy_(labels)
+        gidx = [tr.capture(d_img[b], d_lab[b], warmup=1) for b in range(2)]
     out_loss = torch.empty(K, dtype=torch.float32, pin_memory=True)
     cs = torch.cuda.Stream(dev)
     copied = [torch.cuda.Event(), torch.cuda.Event()]
@@ -201,13 +206,13 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
     for j in range(K):
         b = j % 2
         with torch.cuda.stream(cs):
-            if j >= 2 or (use_graph and j >= 1):
-                cs.wait_event(consumed[(j - 1) % 2] if use_graph else consumed[b])
+            if j >= 2:
+                cs.wait_event(consumed[b])
             d_img[b].copy_(h_img, non_blocking=True)
             d_lab[b].copy_(h_lab, non_blocking=True)
             copied[b].record(cs)
         stream.wait_event(copied[b])
-        l2 = tr.replay() if use_graph else tr.step(d_img[b], d_lab[b])
+        l2 = tr.replay(gidx[b]) if use_graph else tr.step(d_img[b], d_lab[b])
         consumed[b].record(stream)
         out_loss[j].copy_(l2, non_blocking=True)
     s1.record(stream)

@@ -92,12 +92,15 @@ class ViTTrainer:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             self.step(images, labels)
-        self._graph = g
-        self._graph_inputs = (images, labels)
-        return g
+        # several captures (one per input buffer) may coexist: they share every
+        # state buffer, so replaying them in any order is stepping the trainer —
+        # double-buffered inputs let the next batch's H2D copy overlap a step
+        self._graphs = getattr(self, "_graphs", []) + [(g, images, labels)]
+        return len(self._graphs) - 1
 
-    def replay(self) -> torch.Tensor:
-        self._graph.replay()
+    def replay(self, which: int = 0) -> torch.Tensor:
+        """Replay the step captured for input buffer `which` (capture order)."""
+        self._graphs[which][0].replay()
         return self.engine.loss
 
     @property
