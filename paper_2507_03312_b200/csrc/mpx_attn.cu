@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <mutex>
+#include <type_traits>
 
 namespace mpx {
 
@@ -158,12 +159,27 @@ __device__ __forceinline__ void unpack2(uint32_t pk, int fmt, float& lo, float& 
     hi = f.y;
   }
 }
-// the 16 scores of a TMEM chunk, scaled and rounded to the half format (the
-// reference's score dtype) with paired conversions
-__device__ __forceinline__ void round_scores16(const uint32_t* a, float scale, int fmt, float* sv) {
+// Scores of a chunk on the half grid.  For bf16 and a power-of-two scale,
+// round(s * scale) == round(s) * scale exactly, so the scale is folded into the
+// exponent constant (sv stays unscaled, `sl` = scale * log2 e); otherwise sv is
+// round(s * scale) and sl = log2 e.  Either way e = 2^(sv * sl - m * log2 e).
+struct ScoreGrid {
+  float pre;  // multiplier before rounding (1 when folded)
+  float sl;   // sv -> log2 units
+  float ms;   // sv -> scaled score units (for the row max)
+  __device__ __forceinline__ ScoreGrid(float scale, int fmt) {
+    constexpr float kLog2e = 1.4426950408889634f;
+    const uint32_t b = __float_as_uint(scale);
+    const bool fold = fmt == 1 && (b & 0x807FFFFFu) == 0u && ((b >> 23) & 0xFFu) > 32u && ((b >> 23) & 0xFFu) < 222u;
+    pre = fold ? 1.f : scale;
+    sl = fold ? scale * kLog2e : kLog2e;
+    ms = fold ? scale : 1.f;
+  }
+};
+__device__ __forceinline__ void grid_scores16(const uint32_t* a, const ScoreGrid& G, int fmt, float* sv) {
 #pragma unroll
   for (int i = 0; i < 8; ++i)
-    unpack2(pack2_fmt(__uint_as_float(a[2 * i]) * scale, __uint_as_float(a[2 * i + 1]) * scale, fmt), fmt,
+    unpack2(pack2_fmt(__uint_as_float(a[2 * i]) * G.pre, __uint_as_float(a[2 * i + 1]) * G.pre, fmt), fmt,
             sv[2 * i], sv[2 * i + 1]);
 }
 
@@ -172,16 +188,40 @@ __device__ __forceinline__ void round_scores16(const uint32_t* a, float scale, i
 //   pass 1  online: running max m, e = exp(s - m) written back into the same
 //           TMEM columns, running sum rescaled when m grows; m kept per chunk
 //   pass 2  P = e * exp(m_chunk - M) / L rounded to half, into the K-major P tile
-// The masked tail (keys >= N) only touches the last chunk.
+// Full chunks run unpredicated; only the last chunk masks keys >= N.
 template <int NS>
 __device__ __forceinline__ void softmax_fwd_p(uint32_t trow, int split, int r, int q, int N, float scale, int fmt,
                                               float* red, uint8_t* sP, float2* stats) {
   constexpr float kLog2e = 1.4426950408889634f;
   constexpr int kMaxC = (16 + NS - 1) / NS;
+  const ScoreGrid G(scale, fmt);
   const int n_chunks = (N + 15) / 16;
   const int tail = N - (n_chunks - 1) * 16;  // valid keys in the last chunk (1..16)
-  float m = -INFINITY, l = 0.f;
-  float mc[kMaxC];  // running max used for each of this thread's chunks
+  float m = -INFINITY, l = 0.f;  // running max (scaled score units) and sum
+  float mc[kMaxC];               // running max used for each of this thread's chunks
+  auto pass1 = [&](uint32_t* a, auto masked) {
+    constexpr bool kMasked = decltype(masked)::value;
+    float sv[16];
+    grid_scores16(a, G, fmt, sv);
+    float cm = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (!kMasked || i < tail) cm = fmaxf(cm, sv[i]);
+    cm *= G.ms;
+    if (cm > m) {
+      if (m != -INFINITY) l *= ex2_approx((m - cm) * kLog2e);
+      m = cm;
+    }
+    const float ml = m * kLog2e;
+    float add = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float e = (!kMasked || i < tail) ? ex2_approx(fmaf(sv[i], G.sl, -ml)) : 0.f;
+      add += e;
+      a[i] = __float_as_uint(e);
+    }
+    l += add;
+  };
 #pragma unroll
   for (int j = 0; j < kMaxC; ++j) {
     const int c = split + j * NS;
@@ -190,27 +230,11 @@ __device__ __forceinline__ void softmax_fwd_p(uint32_t trow, int split, int r, i
     uint32_t a[16];
     tmem_ld16(trow + c * 16, a);
     tmem_ld_wait();
-    float sv[16];
-    round_scores16(a, scale, fmt, sv);
-    const int lim = c == n_chunks - 1 ? tail : 16;
-    float cm = -INFINITY;
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i < lim) cm = fmaxf(cm, sv[i]);
-    if (cm > m) {
-      if (m != -INFINITY) l *= ex2_approx((m - cm) * kLog2e);
-      m = cm;
-    }
+    if (c == n_chunks - 1 && tail < 16)
+      pass1(a, std::true_type{});
+    else
+      pass1(a, std::false_type{});
     mc[j] = m;
-    const float ml = m * kLog2e;
-    float add = 0.f;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float e = i < lim ? ex2_approx(fmaf(sv[i], kLog2e, -ml)) : 0.f;
-      add += e;
-      a[i] = __float_as_uint(e);
-    }
-    l += add;
     tmem_st16(trow + c * 16, a);
   }
   red[split * 128 + r] = m;
@@ -243,12 +267,13 @@ __device__ __forceinline__ void softmax_fwd_p(uint32_t trow, int split, int r, i
   }
 }
 
-// Backward: P_t of row r recomputed exactly as the forward wrote it — from
-// the forward's (M, 1/L) when given, else from two statistics passes here.
+// Backward: P_t of row r recomputed from the forward's (M, 1/L) when given,
+// else from statistics recomputed here in the forward's order (same bits).
 template <int NS>
 __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, int q, int N, float scale, int fmt,
                                               float* red, uint8_t* sP, const float2* stats) {
   constexpr float kLog2e = 1.4426950408889634f;
+  const ScoreGrid G(scale, fmt);
   const int n_chunks = (N + 15) / 16;
   const int tail = N - (n_chunks - 1) * 16;
   float M, inv;
@@ -258,17 +283,15 @@ __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, i
     inv = st.y;
   } else {  // the forward's statistics, recomputed in its order (online max / rescaled sum)
     float m = -INFINITY, l = 0.f;
-    for (int c = split; c < n_chunks; c += NS) {
-      uint32_t a[16];
-      tmem_ld16(trow + c * 16, a);
-      tmem_ld_wait();
+    auto stat = [&](const uint32_t* a, auto masked) {
+      constexpr bool kMasked = decltype(masked)::value;
       float sv[16];
-      round_scores16(a, scale, fmt, sv);
-      const int lim = c == n_chunks - 1 ? tail : 16;
+      grid_scores16(a, G, fmt, sv);
       float cm = -INFINITY;
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if (i < lim) cm = fmaxf(cm, sv[i]);
+        if (!kMasked || i < tail) cm = fmaxf(cm, sv[i]);
+      cm *= G.ms;
       if (cm > m) {
         if (m != -INFINITY) l *= ex2_approx((m - cm) * kLog2e);
         m = cm;
@@ -276,8 +299,17 @@ __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, i
       const float mlc = m * kLog2e;
       float add = 0.f;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) add += i < lim ? ex2_approx(fmaf(sv[i], kLog2e, -mlc)) : 0.f;
+      for (int i = 0; i < 16; ++i) add += (!kMasked || i < tail) ? ex2_approx(fmaf(sv[i], G.sl, -mlc)) : 0.f;
       l += add;
+    };
+    for (int c = split; c < n_chunks; c += NS) {
+      uint32_t a[16];
+      tmem_ld16(trow + c * 16, a);
+      tmem_ld_wait();
+      if (c == n_chunks - 1 && tail < 16)
+        stat(a, std::true_type{});
+      else
+        stat(a, std::false_type{});
     }
     red[split * 128 + r] = m;
     quarter_sync<NS>(q);
@@ -298,21 +330,27 @@ __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, i
     inv = 1.f / L;
   }
   const float ml = M * kLog2e;
+  auto write_p = [&](const uint32_t* a, int c, auto masked) {
+    constexpr bool kMasked = decltype(masked)::value;
+    float sv[16];
+    grid_scores16(a, G, fmt, sv);
+    uint32_t pk[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float e0 = (!kMasked || 2 * i < tail) ? ex2_approx(fmaf(sv[2 * i], G.sl, -ml)) : 0.f;
+      const float e1 = (!kMasked || 2 * i + 1 < tail) ? ex2_approx(fmaf(sv[2 * i + 1], G.sl, -ml)) : 0.f;
+      pk[i] = pack2_fmt(e0 * inv, e1 * inv, fmt);
+    }
+    store_p_chunk(sP, c, r, pk);
+  };
   for (int c = split; c < n_chunks; c += NS) {
     uint32_t a[16];
     tmem_ld16(trow + c * 16, a);
     tmem_ld_wait();
-    float sv[16];
-    round_scores16(a, scale, fmt, sv);
-    const int lim = c == n_chunks - 1 ? tail : 16;
-    uint32_t pk[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float e0 = 2 * i < lim ? ex2_approx(fmaf(sv[2 * i], kLog2e, -ml)) : 0.f;
-      const float e1 = 2 * i + 1 < lim ? ex2_approx(fmaf(sv[2 * i + 1], kLog2e, -ml)) : 0.f;
-      pk[i] = pack2_fmt(e0 * inv, e1 * inv, fmt);
-    }
-    store_p_chunk(sP, c, r, pk);
+    if (c == n_chunks - 1 && tail < 16)
+      write_p(a, c, std::true_type{});
+    else
+      write_p(a, c, std::false_type{});
   }
 }
 
