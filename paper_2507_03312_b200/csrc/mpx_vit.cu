@@ -13,6 +13,9 @@
 // float atomics, so reruns are bit-identical).
 #include "mpx_common.cuh"
 
+#include <cstdlib>
+#include <mutex>
+
 namespace mpx {
 
 __device__ __forceinline__ float ld_h(const void* p, long long i, int fmt) {
@@ -217,6 +220,108 @@ __global__ void __launch_bounds__(256) ln_dx_kernel(const void* __restrict__ x, 
 #pragma unroll
     for (int e = 0; e < 8; ++e) o[e] = rs * (dv[e] * gg[e] - s1 - (xv[e] - mu) * rs * s2) + (dres ? rv[e] : 0.f);
     *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dx) + row * lddx + c0) = pack8(o, fmt);
+  }
+}
+
+// ===========================================================================
+// K7 LayerNorm backward, one pass (v5): dx as ln_dx_kernel, and the column
+// partials of dy*xhat, dy and the stored (rounded) dx accumulated across the
+// rows of each warp in the warp's own shared-memory slab ([sum][j][e][lane]:
+// lane-consecutive, conflict-free), which frees the registers for the next
+// row's loads to be in flight while this row is reduced (persistent grid,
+// 4 warps per block, fixed row assignment).  The block's warps are combined
+// in a fixed order; ws layout [3][gridDim.x][D] for partials_reduce3_kernel.
+// ===========================================================================
+template <int V>
+__global__ void __launch_bounds__(128) ln_bwd_fused_kernel(const void* __restrict__ x, long long ldx,
+                                                           const void* __restrict__ g, const float* __restrict__ mean,
+                                                           const float* __restrict__ rstd, const void* __restrict__ dy,
+                                                           long long lddy, const void* __restrict__ dres,
+                                                           long long ldres, void* __restrict__ dx, long long lddx,
+                                                           float* __restrict__ ws, int rows, int D, int nsum,
+                                                           int fmt) {
+  extern __shared__ float acc_sh[];  // [4 warps][3][V][8][32]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* acc = acc_sh + warp * (3 * V * 256);
+  auto A = [&](int k, int j, int e) -> float& { return acc[((k * V + j) * 8 + e) * 32 + lane]; };
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) A(k, j, e) = 0.f;
+  const long long stride = (long long)gridDim.x * 4;
+  long long row = (long long)blockIdx.x * 4 + warp;
+  uint4 nx[V], nd[V], nr[V];  // the next row's words, in flight
+  auto load = [&](long long rr) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int c0 = (j * 32 + lane) * 8;
+      nx[j] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + rr * ldx + c0));
+      nd[j] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dy) + rr * lddy + c0));
+      if (dres) nr[j] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dres) + rr * ldres + c0));
+    }
+  };
+  if (row < rows) load(row);
+  for (; row < rows; row += stride) {
+    uint4 wx[V], wd[V], wr[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      wx[j] = nx[j];
+      wd[j] = nd[j];
+      wr[j] = nr[j];
+    }
+    if (row + stride < rows) load(row + stride);  // next row's bytes in flight during this row's work
+    const float mu = mean[row], rs = rstd[row];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int c0 = (j * 32 + lane) * 8;
+      float xv[8], dv[8], gg[8];
+      unpack8(wx[j], xv, fmt);
+      unpack8(wd[j], dv, fmt);
+      unpack8(__ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g) + c0)), gg, fmt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xh = (xv[e] - mu) * rs;
+        const float dg = dv[e] * gg[e];
+        s1 += dg;
+        s2 += dg * xh;
+        A(0, j, e) += dv[e] * xh;
+        A(1, j, e) += dv[e];
+      }
+    }
+    s1 = warp_sum(s1) / (float)D;
+    s2 = warp_sum(s2) / (float)D;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int c0 = (j * 32 + lane) * 8;
+      float xv[8], dv[8], gg[8], rv[8], o[8];
+      unpack8(wx[j], xv, fmt);
+      unpack8(wd[j], dv, fmt);
+      unpack8(__ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g) + c0)), gg, fmt);
+      if (dres) unpack8(wr[j], rv, fmt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = rs * (dv[e] * gg[e] - s1 - (xv[e] - mu) * rs * s2) + (dres ? rv[e] : 0.f);
+      const uint4 w = pack8(o, fmt);
+      *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dx) + row * lddx + c0) = w;
+      if (nsum == 3) {
+        float ov[8];
+        unpack8(w, ov, fmt);  // the column sum of the stored dx
+#pragma unroll
+        for (int e = 0; e < 8; ++e) A(2, j, e) += ov[e];
+      }
+    }
+  }
+  __syncthreads();
+  // combine the 4 warps' slabs in a fixed order, one partial row per block
+  for (int c = threadIdx.x; c < D; c += blockDim.x) {
+    const int j = c / 256, l = (c / 8) % 32, e = c % 8;
+    for (int k = 0; k < nsum; ++k) {
+      float t = 0.f;
+      for (int w = 0; w < 4; ++w) t += acc_sh[w * (3 * V * 256) + ((k * V + j) * 8 + e) * 32 + l];
+      ws[((long long)k * gridDim.x + blockIdx.x) * D + c] = t;
+    }
   }
 }
 
@@ -981,6 +1086,31 @@ int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, 
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int f = fmt_of(dtype);
+  static const bool fused_off = getenv("MPX_LN_FUSED") && getenv("MPX_LN_FUSED")[0] == '0';
+  if (D <= 768 && !fused_off) {  // one pass: dx + all column partials
+    const int nsum = dxsum ? 3 : 2;
+    int blocks = current_num_sms() * 4;
+    while ((long long)nsum * blocks * D > workspace_floats && blocks > 1) blocks /= 2;
+    const size_t shb = (size_t)4 * 3 * D * sizeof(float);  // per-warp accumulator slabs
+    static std::once_flag attr;
+    std::call_once(attr, [] {
+      cudaFuncSetAttribute(ln_bwd_fused_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
+      cudaFuncSetAttribute(ln_bwd_fused_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
+      cudaFuncSetAttribute(ln_bwd_fused_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
+    });
+    switch (D / 256) {
+      case 1: ln_bwd_fused_kernel<1><<<blocks, 128, shb, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx,
+                                                               workspace, rows, D, nsum, f); break;
+      case 2: ln_bwd_fused_kernel<2><<<blocks, 128, shb, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx,
+                                                               workspace, rows, D, nsum, f); break;
+      default: ln_bwd_fused_kernel<3><<<blocks, 128, shb, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx,
+                                                                lddx, workspace, rows, D, nsum, f); break;
+    }
+    MPX_LAUNCH_CHECK("ln_bwd_fused_kernel");
+    partials_reduce3_kernel<<<dim3((D + 31) / 32, nsum), 256, 0, st>>>(workspace, blocks, D, dgain, dbias, dxsum, f);
+    MPX_LAUNCH_CHECK("partials_reduce3_kernel");
+    return 0;
+  }
   const unsigned g1 = (unsigned)((rows + 7) / 8);
   switch (D / 256) {
     case 1: ln_dx_kernel<1><<<g1, 256, 0, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f); break;
