@@ -406,11 +406,11 @@ __global__ void __launch_bounds__(256) ln_colsum_kernel(const void* __restrict__
   }
 }
 
-// ws [nsum][nb][D] -> outputs; grid (D/32, nsum), block = 32 columns x 8
+// ws [nsum][nb][D] -> outputs; grid (D/32, nsum), block = 32 columns x 32
 // partial lanes, four partial rows in flight per thread, fixed order
-__global__ void __launch_bounds__(256) partials_reduce3_kernel(const float* __restrict__ ws, int nb, int D,
-                                                               void* out0, void* out1, void* out2, int fmt) {
-  __shared__ float sm[8][33];
+__global__ void __launch_bounds__(1024) partials_reduce3_kernel(const float* __restrict__ ws, int nb, int D,
+                                                                void* out0, void* out1, void* out2, int fmt) {
+  __shared__ float sm[32][33];
   const int cl = threadIdx.x & 31, kl = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
   const int q = blockIdx.y;
@@ -419,21 +419,21 @@ __global__ void __launch_bounds__(256) partials_reduce3_kernel(const float* __re
   if (c < D) {
     const float* w = ws + (long long)q * nb * D + c;
     int k = kl;
-    for (; k + 24 < nb; k += 32) {
-      const float v0 = w[(long long)k * D], v1 = w[(long long)(k + 8) * D], v2 = w[(long long)(k + 16) * D],
-                  v3 = w[(long long)(k + 24) * D];
+    for (; k + 96 < nb; k += 128) {
+      const float v0 = w[(long long)k * D], v1 = w[(long long)(k + 32) * D], v2 = w[(long long)(k + 64) * D],
+                  v3 = w[(long long)(k + 96) * D];
       a += v0;
       a += v1;
       a += v2;
       a += v3;
     }
-    for (; k < nb; k += 8) a += w[(long long)k * D];
+    for (; k < nb; k += 32) a += w[(long long)k * D];
   }
   sm[kl][cl] = a;
   __syncthreads();
   if (kl == 0 && c < D && out) {
     float t = 0.f;
-    for (int k = 0; k < 8; ++k) t += sm[k][cl];
+    for (int k = 0; k < 32; ++k) t += sm[k][cl];
     st_h(out, c, t, fmt);
   }
 }
@@ -946,6 +946,44 @@ __global__ void patchify_kernel(const uint16_t* __restrict__ img, uint16_t* __re
   }
 }
 
+// patchify by 16-byte vectors: a patch row's (py) segment of p*C contiguous
+// image elements is contiguous in both layouts; one thread per vector, one
+// 2-D index (segment, vector) per thread, no 64-bit divides in the loop body
+__global__ void __launch_bounds__(256) patchify_vec_kernel(const uint4* __restrict__ img, uint4* __restrict__ out,
+                                                           int B, int H, int W, int C, int p) {
+  const int nh = H / p, nw = W / p;
+  const int seg_v = p * C / 8;                  // 16-byte vectors per (patch, py) segment
+  const long long nseg = (long long)B * nh * nw * p;
+  const long long total = nseg * seg_v;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long sg = i / seg_v;
+    const int v = (int)(i - sg * seg_v);
+    const long long r = sg / p;  // patch index (b, ih, iw)
+    const int py = (int)(sg - r * p);
+    const int b = (int)(r / (nh * nw));
+    const int t = (int)(r - (long long)b * nh * nw);
+    const int ih = t / nw, iw = t - ih * nw;
+    const long long src = ((((long long)b * H + ih * p + py) * W + (long long)iw * p) * C) / 8 + v;
+    out[i] = __ldcs(img + src);  // out row r, columns [py*p*C, (py+1)*p*C) — i is already that flat index
+  }
+}
+
+// strided row copy by 16-byte vectors (cols % 8 == 0, 16-byte aligned rows)
+__global__ void __launch_bounds__(256) copy_rows_vec_kernel(const uint16_t* __restrict__ src, long long ld_src,
+                                                            long long sb_src, uint16_t* __restrict__ dst,
+                                                            long long ld_dst, long long sb_dst, int rows, int batches,
+                                                            int cols) {
+  const int cv = cols / 8;
+  const long long n = (long long)batches * rows * cv;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long bc = i / cv;
+    const int c = (int)(i - bc * cv) * 8;
+    const int b = (int)(bc / rows), r = (int)(bc - (long long)b * rows);
+    *reinterpret_cast<uint4*>(dst + b * sb_dst + r * ld_dst + c) =
+        *reinterpret_cast<const uint4*>(src + b * sb_src + r * ld_src + c);
+  }
+}
+
 // out[b][r][c] = src[b][r][c] (strided row copy), optional add of a
 // broadcast row (add[c]) and scaling
 __global__ void copy_rows_kernel(const uint16_t* __restrict__ src, long long ld_src, long long sb_src,
@@ -1107,7 +1145,7 @@ int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, 
                                                                 lddx, workspace, rows, D, nsum, f); break;
     }
     MPX_LAUNCH_CHECK("ln_bwd_fused_kernel");
-    partials_reduce3_kernel<<<dim3((D + 31) / 32, nsum), 256, 0, st>>>(workspace, blocks, D, dgain, dbias, dxsum, f);
+    partials_reduce3_kernel<<<dim3((D + 31) / 32, nsum), 1024, 0, st>>>(workspace, blocks, D, dgain, dbias, dxsum, f);
     MPX_LAUNCH_CHECK("partials_reduce3_kernel");
     return 0;
   }
@@ -1127,7 +1165,7 @@ int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, 
   ln_colsum_kernel<<<dim3(cblocks, splits), 256, 0, st>>>(x, ldx, mean, rstd, dy, lddy, dxsum ? dx : nullptr, lddx, rows,
                                                          D, rps, workspace, f);
   MPX_LAUNCH_CHECK("ln_colsum_kernel");
-  partials_reduce3_kernel<<<dim3((D + 31) / 32, nsum), 256, 0, st>>>(workspace, splits, D, dgain, dbias, dxsum, f);
+  partials_reduce3_kernel<<<dim3((D + 31) / 32, nsum), 1024, 0, st>>>(workspace, splits, D, dgain, dbias, dxsum, f);
   MPX_LAUNCH_CHECK("partials_reduce3_kernel");
   return 0;
 }
@@ -1209,6 +1247,13 @@ int mpx_cross_entropy_bwd(int dtype, const void* logits, int64_t ld, const int32
 int mpx_patchify(int dtype, const void* img, void* patches, int B, int H, int W, int C, int P, void* stream) {
   if (!half_dtype(dtype) || P <= 0 || H % P || W % P) return fail(MPX_EINVAL, "patchify: bad args");
   const long long n = (long long)B * H * W * C;
+  if ((P * C) % 8 == 0 && (W * C) % 8 == 0 &&
+      ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(patches)) & 15) == 0) {
+    patchify_vec_kernel<<<ew_grid(n / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4*>(img), static_cast<uint4*>(patches), B, H, W, C, P);
+    MPX_LAUNCH_CHECK("patchify_vec_kernel");
+    return 0;
+  }
   patchify_kernel<<<ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(img), static_cast<uint16_t*>(patches), B, H, W, C, P);
   MPX_LAUNCH_CHECK("patchify_kernel");
@@ -1220,6 +1265,14 @@ int mpx_copy_rows(int dtype, const void* src, int64_t ld_src, int64_t sb_src, vo
   if (!half_dtype(dtype)) return fail(MPX_EINVAL, "copy_rows: f16/bf16 only");
   const long long n = (long long)rows * batches * cols;
   if (n <= 0) return 0;
+  if (cols % 8 == 0 && ld_src % 8 == 0 && sb_src % 8 == 0 && ld_dst % 8 == 0 && sb_dst % 8 == 0 &&
+      ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    copy_rows_vec_kernel<<<ew_grid(n / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint16_t*>(src), ld_src, sb_src, static_cast<uint16_t*>(dst), ld_dst, sb_dst, rows, batches,
+        cols);
+    MPX_LAUNCH_CHECK("copy_rows_vec_kernel");
+    return 0;
+  }
   copy_rows_kernel<<<ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(src), ld_src, sb_src, static_cast<uint16_t*>(dst), ld_dst, sb_dst, rows, batches,
       cols);
