@@ -107,6 +107,28 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c0 * (1.f + 3.f * c1 * x * x);
 }
 
+// packed-f32x2 (FFMA2 / FMUL2) versions for the lean epilogues: two columns per
+// instruction on the FMA pipe; the same tanh form, c0 x (1 + c1 x^2) inside
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 gelu2(float2 x) {
+  const float c0 = 0.7978845608028654f, c1 = 0.044715f;
+  const float2 x2 = __fmul2_rn(x, x);
+  const float2 u = __fmul2_rn(__fmul2_rn(x, __ffma2_rn(x2, f2(c1), f2(1.f))), f2(c0));
+  const float2 th = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+  const float2 hx = __fmul2_rn(x, f2(0.5f));
+  return __ffma2_rn(hx, th, hx);
+}
+__device__ __forceinline__ float2 gelu_grad2(float2 x) {
+  const float c0 = 0.7978845608028654f, c1 = 0.044715f;
+  const float2 x2 = __fmul2_rn(x, x);
+  const float2 u = __fmul2_rn(__fmul2_rn(x, __ffma2_rn(x2, f2(c1), f2(1.f))), f2(c0));
+  const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+  const float2 a = __ffma2_rn(t, f2(0.5f), f2(0.5f));                      // 0.5 (1 + t)
+  const float2 sech2 = __ffma2_rn(make_float2(-t.x, -t.y), t, f2(1.f));    // 1 - t^2
+  const float2 k = __ffma2_rn(x2, f2(3.f * c0 * c1), f2(c0));              // c0 (1 + 3 c1 x^2)
+  return __ffma2_rn(__fmul2_rn(__fmul2_rn(x, f2(0.5f)), sech2), k, a);
+}
+
 struct TileCoord {
   int z, s, m_blk, n_blk;
 };
@@ -397,14 +419,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 bb[i] = col + i < P.N ? half_to_f32(static_cast<const uint16_t*>(P.bias)[col + i], P.ab_fmt) : 0.f;
             }
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += bb[i];
+            for (int i = 0; i < 8; ++i) {
+              const float2 r2 = __fadd2_rn(make_float2(v[2 * i], v[2 * i + 1]), make_float2(bb[2 * i], bb[2 * i + 1]));
+              v[2 * i] = r2.x;
+              v[2 * i + 1] = r2.y;
+            }
           }
           if (XO == XOP_RES_IN) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += xin[i];
+            for (int i = 0; i < 8; ++i) {
+              const float2 r2 =
+                  __fadd2_rn(make_float2(v[2 * i], v[2 * i + 1]), make_float2(xin[2 * i], xin[2 * i + 1]));
+              v[2 * i] = r2.x;
+              v[2 * i + 1] = r2.y;
+            }
           } else if (XO == XOP_AUX_IN) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] *= gelu_grad_f(xin[i]);
+            for (int i = 0; i < 8; ++i) {
+              const float2 r2 = __fmul2_rn(make_float2(v[2 * i], v[2 * i + 1]),
+                                           gelu_grad2(make_float2(xin[2 * i], xin[2 * i + 1])));
+              v[2 * i] = r2.x;
+              v[2 * i + 1] = r2.y;
+            }
           }
           return;  // XOP_AUX_OUT: the caller rounds (aux) and applies the GELU
         }
@@ -526,8 +562,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               const int k = pair * kLd + kk;
               if (k >= nch) continue;
               float v[16];
+              if (P.alpha != 1.f) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[kk][i]) * P.alpha;
+                for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[kk][i]) * P.alpha;
+              } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[kk][i]);
+              }
               if (f32out) {  // raw (split-K partial) or f32 output: 4 x 16 B, SW128
                 uint8_t* rowp = bb + lane * 128;
 #pragma unroll
@@ -545,7 +586,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   pa[i] = pack2_fmt(v[2 * i], v[2 * i + 1], P.ab_fmt);
                   const float a = half_to_f32((uint16_t)(pa[i] & 0xFFFFu), P.ab_fmt);
                   const float b = half_to_f32((uint16_t)(pa[i] >> 16), P.ab_fmt);
-                  pc[i] = pack2_fmt(gelu_f(a), gelu_f(b), cf);
+                  const float2 y = gelu2(make_float2(a, b));  // GELU of the rounded pre-activation
+                  pc[i] = pack2_fmt(y.x, y.y, cf);
                 }
                 const int s64 = (lane >> 1) & 3;
                 uint8_t* ra = bb + lane * 64;
