@@ -163,6 +163,8 @@ __device__ __forceinline__ void unpack2(uint32_t pk, int fmt, float& lo, float& 
 // round(s * scale) == round(s) * scale exactly, so the scale is folded into the
 // exponent constant (sv stays unscaled, `sl` = scale * log2 e); otherwise sv is
 // round(s * scale) and sl = log2 e.  Either way e = 2^(sv * sl - m * log2 e).
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
 struct ScoreGrid {
   float pre;  // multiplier before rounding (1 when folded)
   float sl;   // sv -> log2 units
@@ -213,14 +215,17 @@ __device__ __forceinline__ void softmax_fwd_p(uint32_t trow, int split, int r, i
       m = cm;
     }
     const float ml = m * kLog2e;
-    float add = 0.f;
+    float2 acc = f2(0.f);  // even / odd column partial sums (the backward recomputes them alike)
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float e = (!kMasked || i < tail) ? ex2_approx(fmaf(sv[i], G.sl, -ml)) : 0.f;
-      add += e;
-      a[i] = __float_as_uint(e);
+    for (int i = 0; i < 8; ++i) {
+      const float2 arg = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), f2(G.sl), f2(-ml));
+      const float e0 = (!kMasked || 2 * i < tail) ? ex2_approx(arg.x) : 0.f;
+      const float e1 = (!kMasked || 2 * i + 1 < tail) ? ex2_approx(arg.y) : 0.f;
+      acc = __fadd2_rn(acc, make_float2(e0, e1));
+      a[2 * i] = __float_as_uint(e0);
+      a[2 * i + 1] = __float_as_uint(e1);
     }
-    l += add;
+    l += acc.x + acc.y;
   };
 #pragma unroll
   for (int j = 0; j < kMaxC; ++j) {
@@ -262,7 +267,10 @@ __device__ __forceinline__ void softmax_fwd_p(uint32_t trow, int split, int r, i
     const float f = ex2_approx((mc[j] - M) * kLog2e) * inv;
     uint32_t pk[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * f, __uint_as_float(a[2 * i + 1]) * f, fmt);
+    for (int i = 0; i < 8; ++i) {
+      const float2 p2 = __fmul2_rn(make_float2(__uint_as_float(a[2 * i]), __uint_as_float(a[2 * i + 1])), f2(f));
+      pk[i] = pack2_fmt(p2.x, p2.y, fmt);
+    }
     store_p_chunk(sP, c, r, pk);
   }
 }
@@ -297,10 +305,15 @@ __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, i
         m = cm;
       }
       const float mlc = m * kLog2e;
-      float add = 0.f;
+      float2 acc = f2(0.f);  // as the forward's pass 1
 #pragma unroll
-      for (int i = 0; i < 16; ++i) add += (!kMasked || i < tail) ? ex2_approx(fmaf(sv[i], G.sl, -mlc)) : 0.f;
-      l += add;
+      for (int i = 0; i < 8; ++i) {
+        const float2 arg = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), f2(G.sl), f2(-mlc));
+        const float e0 = (!kMasked || 2 * i < tail) ? ex2_approx(arg.x) : 0.f;
+        const float e1 = (!kMasked || 2 * i + 1 < tail) ? ex2_approx(arg.y) : 0.f;
+        acc = __fadd2_rn(acc, make_float2(e0, e1));
+      }
+      l += acc.x + acc.y;
     };
     for (int c = split; c < n_chunks; c += NS) {
       uint32_t a[16];
@@ -337,9 +350,11 @@ __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, i
     uint32_t pk[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float e0 = (!kMasked || 2 * i < tail) ? ex2_approx(fmaf(sv[2 * i], G.sl, -ml)) : 0.f;
-      const float e1 = (!kMasked || 2 * i + 1 < tail) ? ex2_approx(fmaf(sv[2 * i + 1], G.sl, -ml)) : 0.f;
-      pk[i] = pack2_fmt(e0 * inv, e1 * inv, fmt);
+      const float2 arg = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), f2(G.sl), f2(-ml));
+      const float e0 = (!kMasked || 2 * i < tail) ? ex2_approx(arg.x) : 0.f;
+      const float e1 = (!kMasked || 2 * i + 1 < tail) ? ex2_approx(arg.y) : 0.f;
+      const float2 p2 = __fmul2_rn(make_float2(e0, e1), f2(inv));
+      pk[i] = pack2_fmt(p2.x, p2.y, fmt);
     }
     store_p_chunk(sP, c, r, pk);
   };
@@ -641,7 +656,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (warp == 4 && lane == 0) ATRACE(6 + 8 * t);
       tc_fence_after();
       uint32_t dpk[kMaxC][8];
-      float tsum = 0.f;
+      float2 tsum2 = f2(0.f);
 #pragma unroll
       for (int j = 0; j < kMaxC; ++j) {
         const int c = split + j * kSplit;
@@ -656,14 +671,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             dpk[j][i] = pack2_fmt(__uint_as_float(a[2 * i]), __uint_as_float(a[2 * i + 1]), P.fmt);
             float d0, d1;
             unpack2(dpk[j][i], P.fmt, d0, d1);
-            tsum += pv[2 * i] * d0;
-            tsum += pv[2 * i + 1] * d1;
+            tsum2 = __ffma2_rn(make_float2(pv[2 * i], pv[2 * i + 1]), make_float2(d0, d1), tsum2);
           }
         }
       }
-      red[split * 128 + r] = tsum;
+      red[split * 128 + r] = tsum2.x + tsum2.y;
       quarter_sync<kSplit>(qd);
-      tsum = 0.f;
+      float tsum = 0.f;
 #pragma unroll
       for (int j = 0; j < kSplit; ++j) tsum += red[j * 128 + r];
       quarter_sync<kSplit>(qd);
@@ -678,7 +692,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           for (int i = 0; i < 8; ++i) {
             float d0, d1;
             unpack2(dpk[j][i], P.fmt, d0, d1);
-            pk[i] = pack2_fmt(pv[2 * i] * (d0 - tsum), pv[2 * i + 1] * (d1 - tsum), P.fmt);
+            const float2 ds = __fmul2_rn(make_float2(pv[2 * i], pv[2 * i + 1]),
+                                         __fadd2_rn(make_float2(d0, d1), f2(-tsum)));
+            pk[i] = pack2_fmt(ds.x, ds.y, P.fmt);
           }
           store_p_chunk(sdS, c, r, pk);
         }
