@@ -4,9 +4,11 @@ on synthetic 32x32x3 batches of 64, f16 + LossScaling + Adam(lr 1e-3), built
 only from mpsim primitives and trained with
 mpsim.filter_value_and_grad / optimizer_update.
 
-    python tests/golden/gen_tiny_vit.py <init_scale_log2> <steps>
+    python tests/golden/gen_tiny_vit.py <init_scale_log2> <steps> [--hd64]
 
-writes tests/golden/tiny_vit_s<log2>.npz: the f32 initial parameters (so
+writes tests/golden/tiny_vit_s<log2>.npz (--hd64: dim 128 / 2 heads, head
+dim 64 — the shape the GPU's fused attention kernels take — written to
+tiny_vit_hd64_s<log2>.npz): the f32 initial parameters (so
 the GPU test starts from the same weights), and per step the loss, the
 scale used, grads_finite and a parameter checksum.  Images are
 np.random.default_rng((0, 1 + step)) N(0,1) [64,32,32,3], labels U{0..9}
@@ -30,6 +32,9 @@ from mpsim import F16, F32, I32, LossScaling, adam_init, filter_value_and_grad, 
 from mpsim import tensors as T  # noqa: E402
 
 IMG, P, C, D, DEPTH, H, MLP, NCLS, B = 32, 4, 3, 64, 2, 4, 256, 10, 64
+HD64 = "--hd64" in sys.argv
+if HD64:
+    D, H = 128, 2
 NP = (IMG // P) ** 2
 HD = D // H
 
@@ -118,8 +123,9 @@ def checksum(model):
 
 
 def main():
-    log2 = int(sys.argv[1]) if len(sys.argv) > 1 else 15
-    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    log2 = int(args[0]) if len(args) > 0 else 15
+    steps = int(args[1]) if len(args) > 1 else 20
     p0 = init_params()
     model = {k: tensor(v, F32) for k, v in p0.items()}
     opt = adam_init(model, 1e-3)
@@ -137,7 +143,7 @@ def main():
         scaling = res.scaling
         print(f"step {step} loss {losses[-1]:.6f} scale {scales[-1]} finite {flags[-1]} ({time.time() - t0:.1f}s)",
               flush=True)
-    out = Path(__file__).resolve().parent / f"tiny_vit_s{log2}.npz"
+    out = Path(__file__).resolve().parent / (f"tiny_vit_hd64_s{log2}.npz" if HD64 else f"tiny_vit_s{log2}.npz")
     np.savez_compressed(out, losses=np.asarray(losses), scales=np.asarray(scales), flags=np.asarray(flags),
                         checksums=np.asarray(sums, dtype=np.uint64), **{"init." + k: v for k, v in p0.items()})
     print("wrote", out)

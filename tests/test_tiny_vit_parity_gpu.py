@@ -20,7 +20,10 @@ import torch
 import paper_2507_03312_b200 as mpx
 from oracle import mpx_oracle as O
 from paper_2507_03312_b200.vit import vit_loss
-from paper_2507_03312_b200.vit_config import VIT_TINY
+from paper_2507_03312_b200.vit_config import VIT_TINY, ViTConfig
+
+# head dim 64: the shape the fused attention kernels (mpx_attn.cu) take
+VIT_TINY_HD64 = ViTConfig(img=32, patch=4, dim=128, depth=2, heads=2, mlp=256, classes=10, pool="mean")
 
 pytestmark = pytest.mark.gpu
 GOLD = Path(__file__).resolve().parent / "golden"
@@ -33,11 +36,11 @@ def batch(step):
     return x, y
 
 
-def run_gpu(init: dict, log2: int, steps: int, device):
+def run_gpu(init: dict, log2: int, steps: int, device, cfg=VIT_TINY):
     params = {k: torch.from_numpy(v).to(device) for k, v in init.items()}
     opt = mpx.adam_init(params, 1e-3)
     scaling = mpx.LossScaling(2.0 ** log2)
-    f = vit_loss(VIT_TINY)
+    f = vit_loss(cfg)
     losses, scales, flags = [], [], []
     for step in range(steps):
         x, y = batch(step)
@@ -51,16 +54,17 @@ def run_gpu(init: dict, log2: int, steps: int, device):
     return np.array(losses), np.array(scales), np.array(flags)
 
 
-@pytest.mark.parametrize("log2", [15, 32])
-def test_tiny_vit_trajectory_matches_reference(cuda, log2):
-    path = GOLD / f"tiny_vit_s{log2}.npz"
+@pytest.mark.parametrize("log2,variant", [(15, ""), (32, ""), (15, "hd64")])
+def test_tiny_vit_trajectory_matches_reference(cuda, log2, variant):
+    path = GOLD / (f"tiny_vit_{variant}_s{log2}.npz" if variant else f"tiny_vit_s{log2}.npz")
+    cfg = VIT_TINY_HD64 if variant == "hd64" else VIT_TINY
     if not path.exists():
         pytest.skip(f"{path.name} not generated")
     g = np.load(path)
     init = {k[5:]: g[k] for k in g.files if k.startswith("init.")}
     ref_loss, ref_scale, ref_flag = g["losses"], g["scales"], g["flags"]
     steps = len(ref_loss)
-    loss, scale, flag = run_gpu(init, log2, steps, cuda)
+    loss, scale, flag = run_gpu(init, log2, steps, cuda, cfg)
 
     # our scale column replays on the reference state machine given our flags
     sim = O.simulate_scaling(2.0 ** log2, 2.0, 0.5, 2000, 1.0, flag)
