@@ -41,11 +41,22 @@ constexpr int kBTileBytes = kBNMax * kBK * 2;    // 32 KB
 constexpr int kEpiWarps = 8;                  // epilogue warps: kEpiWarps / 4 per TMEM lane quarter (16: no gain)
 constexpr int kEpiPerQ = kEpiWarps / 4;
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // TMA warp, MMA warp, epilogue warps
-constexpr int kEpiStage = 65536;               // staging bytes (all epilogue warps)
-constexpr int kBufPerWarp = kEpiStage / kEpiWarps / 4096;  // 4 KB staging buffers per epilogue warp
-constexpr int kGroupM = 16;
-constexpr size_t kGemmSmem = 1024 + 5 * (kATileBytes + kBTileBytes / 2) + kEpiStage + 384;
-static_assert(3 * (kATileBytes + kBTileBytes) <= 5 * (kATileBytes + kBTileBytes / 2), "CG=1 ring exceeds the CG=2 one");
+// Shared memory = A/B ring + epilogue staging, 230 KB either way.  Variants
+// that stage an operand (residual / GELU aux in) keep two 4 KB buffers per
+// epilogue warp (64 KB: operand prefetch + in-place output) and a 5-deep ring;
+// the others one buffer per warp (32 KB) and a 6-deep ring (measured: plain
+// epilogue 209 -> 205 us, operand-in variants 250 -> 262 us with one buffer).
+template <int XO> struct GemmSmem {
+  static constexpr int kStageKB = (XO == 1 || XO == 2) ? 64 : 32;  // XOP_RES_IN, XOP_AUX_IN
+  static constexpr int kEpiStage = kStageKB * 1024;
+  static constexpr int kStages2 = (192 - kStageKB) / 32 + 1;  // CTA-pair ring depth (32 KB stages)
+  static constexpr int kStages1 = (kStages2 * 2) / 3;          // single-CTA ring depth (48 KB stages)
+  static constexpr int kBufPerWarp = kEpiStage / kEpiWarps / 4096;
+};
+constexpr int kGroupM = 16;  // tile raster: groups of kGroupM m-blocks, m fastest
+constexpr size_t kGemmSmem = 1024 + 5 * (kATileBytes + kBTileBytes / 2) + 65536 + 384;
+static_assert(1024 + 6 * (kATileBytes + kBTileBytes / 2) + 32768 + 384 == kGemmSmem, "variant smem budgets differ");
+static_assert(4 * (kATileBytes + kBTileBytes) <= 6 * (kATileBytes + kBTileBytes / 2), "CG=1 ring exceeds the CG=2 one");
 
 // ACT_SOFTMAX: the tile holds whole rows (one N block, N <= 256): C = softmax
 //   over the row of round_half(alpha * acc) (f32 island, tensors.py:431-446)
@@ -157,7 +168,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
                 const __grid_constant__ GemmParams P) {
-  constexpr int S = CG == 1 ? 3 : 5;           // smem ring depth (48 / 32 KB stages)
+  using SM = GemmSmem<XO>;
+  constexpr int S = CG == 1 ? SM::kStages1 : SM::kStages2;  // smem ring depth (48 / 32 KB stages)
+  constexpr int kBufPerWarp = SM::kBufPerWarp;
+  constexpr int kEpiStage = SM::kEpiStage;
   constexpr int BT = kBTileBytes / CG;         // B bytes per stage per CTA
   extern __shared__ uint8_t smem_raw[];
   // 1 KB-aligned by indexing the __shared__ array (not via an integer cast), so
@@ -1099,7 +1113,9 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   if (g->colsum_out) {
     if (!g->colsum_ws) return fail(MPX_EINVAL, "mpx_gemm: colsum_out needs colsum_ws");
     csum_fused = P.tma_store && split == 1 && g->c_dtype != MPX_F32 && nb1 * nb2 == 1 && P.xop != XOP_NONE &&
-                 P.xop != XOP_AUX_OUT && BN <= 64 * kEpiPerQ * kBufPerWarp;
+                 P.xop != XOP_AUX_OUT &&
+                 BN <= 64 * kEpiPerQ * (P.xop == XOP_PLAIN ? GemmSmem<XOP_PLAIN>::kBufPerWarp
+                                                           : GemmSmem<XOP_AUX_IN>::kBufPerWarp);
     if (csum_fused) P.csum = g->colsum_ws;
   }
   const KernelFn kern = kernels[CG - 1][P.xop];
