@@ -406,6 +406,7 @@ __global__ void __launch_bounds__(kAttnThreadsF, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  ::mpx::pdl_grid_sync();  // prologue done: wait for the predecessor's outputs
 
   if (warp == 0) {
     if (lane == 0) {
@@ -551,6 +552,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  ::mpx::pdl_grid_sync();  // prologue done: wait for the predecessor's outputs
 
   if (warp == 0) {
     if (lane == 0) {
@@ -870,7 +872,7 @@ extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H
   });
   if (err != cudaSuccess) return fail((int)err, "cudaFuncSetAttribute(attn_fwd_kernel)");
   const long long grid = (long long)B * H * P.m_tiles;
-  attn_fwd_kernel<<<(unsigned)grid, kAttnThreadsF, kAttnSmem, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, P);
+  MPX_CUDA_CHECK(::mpx::launch_k(attn_fwd_kernel, (unsigned)grid, kAttnThreadsF, kAttnSmem, static_cast<cudaStream_t>(stream), tq, tk, tv, P));
   MPX_LAUNCH_CHECK("attn_fwd_kernel");
   return 0;
 }
@@ -908,13 +910,12 @@ extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int
     err = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnBwdSmem);
   });
   if (err != cudaSuccess) return fail((int)err, "cudaFuncSetAttribute(attn_bwd_kernel)");
-  attn_bwd_kernel<<<(unsigned)(B * H), kAttnThreads, kAttnBwdSmem, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, tdo,
-                                                                                                       P);
+  MPX_CUDA_CHECK(::mpx::launch_k(attn_bwd_kernel, (unsigned)(B * H), kAttnThreads, kAttnBwdSmem, static_cast<cudaStream_t>(stream), tq, tk, tv, tdo,
+                                                                                                       P));
   MPX_LAUNCH_CHECK("attn_bwd_kernel");
   if (colsum_out) {  // the qkv bias gradient: sum the per-image partials [B][3D]
     const int cols = 3 * D;
-    colsum_final_kernel<<<(unsigned)((cols + 31) / 32), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        colsum_ws, B, cols, 1, colsum_out, cols, dtype, 1.f);
+    MPX_CUDA_CHECK(::mpx::launch_k(colsum_final_kernel, (unsigned)((cols + 31) / 32), 256, 0, static_cast<cudaStream_t>(stream), colsum_ws, B, cols, 1, colsum_out, cols, dtype, 1.f));
     MPX_LAUNCH_CHECK("colsum_final_kernel");
   }
   return 0;

@@ -220,6 +220,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (CG == 2) cluster_sync();  // the peer's barriers exist before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done (barriers, TMEM, descriptor prefetch): wait for the
+  // predecessor's outputs before the first global access
+  ::mpx::pdl_grid_sync();
 
   const uint32_t a_bytes = kATileBytes;
   const int bn_cta = P.BN / CG;  // B columns staged by this CTA
@@ -781,6 +784,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // thread, fixed summation order
 __global__ void __launch_bounds__(1024) colsum_parts_kernel(const float* __restrict__ parts, int nparts, int N,
                                                             void* out, int out_dtype) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   __shared__ float sm[32][33];
   const int cl = threadIdx.x & 31, kl = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
@@ -813,6 +817,7 @@ __global__ void __launch_bounds__(1024) colsum_parts_kernel(const float* __restr
 // split-K: C = cast(sum_s ws[s]) (+ bias), summed in split order
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int split, long long mn, int N, void* C,
                                      long long ldc, int c_dtype, const void* bias, int ab_fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < mn; i += (long long)gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int k = 0; k < split; ++k) s += ws[k * mn + i];
@@ -831,6 +836,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int split, lo
 __global__ void __launch_bounds__(256) splitk_reduce4_kernel(const float* __restrict__ ws, int split, int M, int N,
                                                              void* C, long long ldc, int c_dtype, const void* bias,
                                                              int ab_fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int n4 = N / 4;
   const long long mn = (long long)M * N;
   const long long total = (long long)M * n4;
@@ -1122,7 +1128,7 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (CG == 1) {
     const long long grid = std::min<long long>(P.total_tiles, current_num_sms());
-    kern<<<(unsigned)grid, kGemmThreads, kGemmSmem, st>>>(ta, tb, tc, tx, P);
+    MPX_CUDA_CHECK(::mpx::launch_k(kern, (unsigned)grid, kGemmThreads, kGemmSmem, st, ta, tb, tc, tx, P));
   } else {
     const long long pairs = std::min<long long>(P.total_tiles, current_num_sms() / 2);
     cudaLaunchConfig_t cfg{};
@@ -1130,31 +1136,31 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
     cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = kGemmSmem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 1;  // (no PDL for the ViT kernels, see launch_k)
     MPX_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, P));
   }
   MPX_LAUNCH_CHECK("gemm_kernel");
   if (split > 1) {
     const long long mn = (long long)g->M * g->N;
     if (g->N % 4 == 0 && reinterpret_cast<uintptr_t>(P.ws) % 16 == 0)
-      splitk_reduce4_kernel<<<current_num_sms() * 8, 256, 0, st>>>(P.ws, split, g->M, g->N, g->C, g->ldc, g->c_dtype,
-                                                                   g->bias, fmt);
+      MPX_CUDA_CHECK(::mpx::launch_k(splitk_reduce4_kernel, current_num_sms() * 8, 256, 0, st, P.ws, split, g->M, g->N, g->C, g->ldc, g->c_dtype,
+                                                                   g->bias, fmt));
     else
-      splitk_reduce_kernel<<<current_num_sms() * 4, 256, 0, st>>>(P.ws, split, mn, g->N, g->C, g->ldc, g->c_dtype,
-                                                                 g->bias, fmt);
+      MPX_CUDA_CHECK(::mpx::launch_k(splitk_reduce_kernel, current_num_sms() * 4, 256, 0, st, P.ws, split, mn, g->N, g->C, g->ldc, g->c_dtype,
+                                                                 g->bias, fmt));
     MPX_LAUNCH_CHECK("splitk_reduce_kernel");
   }
   if (g->colsum_out) {
     if (csum_fused) {
       const int parts = (g->M + 31) / 32;
-      colsum_parts_kernel<<<(unsigned)((g->N + 31) / 32), 1024, 0, st>>>(g->colsum_ws, parts, g->N, g->colsum_out,
-                                                                         g->c_dtype);
+      MPX_CUDA_CHECK(::mpx::launch_k(colsum_parts_kernel, (unsigned)((g->N + 31) / 32), 1024, 0, st, g->colsum_ws, parts, g->N, g->colsum_out,
+                                                                         g->c_dtype));
       MPX_LAUNCH_CHECK("colsum_parts_kernel");
     } else {
       const int rc2 = mpx_colsum(g->c_dtype, g->C, g->ldc, 0, g->M, g->N, 1, g->colsum_ws,

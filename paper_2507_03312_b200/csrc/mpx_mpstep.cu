@@ -16,6 +16,8 @@
 // vector accesses, grid sized to resident-blocks x SM count.
 #include "mpx_common.cuh"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <mutex>
 #include <vector>
@@ -27,6 +29,11 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
+}
+
+bool pdl_enabled() {
+  static const bool on = !(getenv("MPX_PDL") && getenv("MPX_PDL")[0] == '0');
+  return on;
 }
 
 int current_num_sms() {
@@ -95,6 +102,7 @@ struct CastParams {
 
 template <int SRC, int DST, bool SCALE>
 __global__ void __launch_bounds__(kThreads) cast_kernel(const __grid_constant__ CastParams P) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   float s = 1.f;
   if (SCALE) s = __double2float_rn(P.d_scale ? *P.d_scale : P.scale);
   for (int64_t tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
@@ -124,7 +132,7 @@ __global__ void __launch_bounds__(kThreads) cast_kernel(const __grid_constant__ 
 template <int SRC, int DST, bool SCALE>
 static int launch_cast(const CastParams& P, cudaStream_t st) {
   auto k = cast_kernel<SRC, DST, SCALE>;
-  k<<<grid_for(k, P.n_tiles), kThreads, 0, st>>>(P);
+  MPX_CUDA_CHECK(::mpx::launch_pdl(k, grid_for(k, P.n_tiles), kThreads, 0, st, P));
   MPX_LAUNCH_CHECK("cast_kernel");
   return 0;
 }
@@ -183,6 +191,7 @@ template <> __device__ __forceinline__ bool raw_nonfinite4<MPX_BF16>(const void*
 
 template <int GDT, bool OUT>
 __global__ void __launch_bounds__(kThreads) unscale_finite_kernel(const __grid_constant__ UnscaleParams P) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   Divisor d;
   d.init(__double2float_rn(P.d_scale ? *P.d_scale : P.scale));
   // Flag-only with |divisor| >= 1 (including +inf): |x/s| <= |x|, so x/s is
@@ -232,6 +241,7 @@ template <int GDT>
 __global__ void __launch_bounds__(kThreads) finite_scan_kernel(const uint16_t* __restrict__ g, int64_t n,
                                                                const double* d_scale, double scale,
                                                                uint32_t* __restrict__ flag) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   constexpr uint32_t EXP = GDT == MPX_F16 ? 0x7C00u : 0x7F80u;
   Divisor d;
   d.init(__double2float_rn(d_scale ? *d_scale : scale));
@@ -270,10 +280,10 @@ template <int GDT>
 static int launch_unscale(const UnscaleParams& P, bool out, cudaStream_t st) {
   if (out) {
     auto k = unscale_finite_kernel<GDT, true>;
-    k<<<grid_for(k, P.n_tiles), kThreads, 0, st>>>(P);
+    MPX_CUDA_CHECK(::mpx::launch_pdl(k, grid_for(k, P.n_tiles), kThreads, 0, st, P));
   } else {
     auto k = unscale_finite_kernel<GDT, false>;
-    k<<<grid_for(k, P.n_tiles), kThreads, 0, st>>>(P);
+    MPX_CUDA_CHECK(::mpx::launch_pdl(k, grid_for(k, P.n_tiles), kThreads, 0, st, P));
   }
   MPX_LAUNCH_CHECK("unscale_finite_kernel");
   return 0;
@@ -284,6 +294,7 @@ static int launch_unscale(const UnscaleParams& P, bool out, cudaStream_t st) {
 // ===========================================================================
 __global__ void scaling_adjust_kernel(mpx_scaling_state* st, const uint32_t* flag,
                                       int64_t* step_count, double* used_scale) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const double F32_MAX = 3.4028234663852886e38;  // float(np.finfo(np.float32).max)
   const bool finite = *flag != 0u;
   double scale = st->loss_scale;
@@ -427,6 +438,7 @@ __device__ __forceinline__ void opt_tile(const OptLeaf& L, int64_t off, int64_t 
 // first-to-last, so the tail of the gradient arena is still L2-resident.
 template <int GDT, int HDT, int MODE>
 __global__ void __launch_bounds__(kThreads) optimizer_kernel(const __grid_constant__ OptParams P) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   if (P.flag != nullptr && *P.flag == 0u) return;  // gate: skipped step leaves everything bit-identical
   Divisor d;
   d.init(__double2float_rn(P.d_scale ? *P.d_scale : P.scale));
@@ -470,7 +482,7 @@ __global__ void __launch_bounds__(kThreads) optimizer_kernel(const __grid_consta
 template <int GDT, int HDT, int MODE>
 static int launch_opt3(const OptParams& P, cudaStream_t st) {
   auto k = optimizer_kernel<GDT, HDT, MODE>;
-  k<<<grid_for(k, P.n_tiles), kThreads, 0, st>>>(P);
+  MPX_CUDA_CHECK(::mpx::launch_pdl(k, grid_for(k, P.n_tiles), kThreads, 0, st, P));
   MPX_LAUNCH_CHECK("optimizer_kernel");
   return 0;
 }
@@ -554,11 +566,11 @@ int mpx_unscale_finite(const void* const* h_g, float* const* h_out, const int64_
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((n / 8 + 4 * kThreads - 1) / (4 * kThreads), (int64_t)current_num_sms() * 8));
     if (g_dtype == MPX_F16)
-      finite_scan_kernel<MPX_F16><<<grid, kThreads, 0, st>>>(static_cast<const uint16_t*>(h_g[0]), n, d_scale, scale,
-                                                              d_flag);
+      MPX_CUDA_CHECK(::mpx::launch_pdl(finite_scan_kernel<MPX_F16>, grid, kThreads, 0, st, static_cast<const uint16_t*>(h_g[0]), n, d_scale, scale,
+                                                              d_flag));
     else
-      finite_scan_kernel<MPX_BF16><<<grid, kThreads, 0, st>>>(static_cast<const uint16_t*>(h_g[0]), n, d_scale, scale,
-                                                               d_flag);
+      MPX_CUDA_CHECK(::mpx::launch_pdl(finite_scan_kernel<MPX_BF16>, grid, kThreads, 0, st, static_cast<const uint16_t*>(h_g[0]), n, d_scale, scale,
+                                                               d_flag));
     MPX_LAUNCH_CHECK("finite_scan_kernel");
     return 0;
   }
@@ -597,8 +609,8 @@ int mpx_unscale_finite(const void* const* h_g, float* const* h_out, const int64_
 int mpx_scaling_adjust(mpx_scaling_state* d_state, const uint32_t* d_flag, int64_t* d_step_count,
                        double* d_used_scale, void* stream) {
   if (!d_state || !d_flag) return fail(MPX_EINVAL, "mpx_scaling_adjust: null pointer");
-  scaling_adjust_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(d_state, d_flag, d_step_count,
-                                                                       d_used_scale);
+  MPX_CUDA_CHECK(::mpx::launch_pdl(scaling_adjust_kernel, 1, 1, 0, static_cast<cudaStream_t>(stream), d_state, d_flag, d_step_count,
+                                                                       d_used_scale));
   MPX_LAUNCH_CHECK("scaling_adjust_kernel");
   return 0;
 }

@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const void* __restrict__ x,
                                                      const void* __restrict__ g, const void* __restrict__ b,
                                                      void* __restrict__ y, long long ldy, float* __restrict__ mean,
                                                      float* __restrict__ rstd, int rows, int D, float eps, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const void* __restrict__ x,
                                                      long long lddy, const void* __restrict__ dres, long long ldres,
                                                      void* __restrict__ dx, long long lddx, float* __restrict__ ws,
                                                      int rows, int D, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   extern __shared__ float sh[];  // [8 warps][2][D]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* my_dg = sh + warp * 2 * D;
@@ -180,6 +182,7 @@ __global__ void __launch_bounds__(256) ln_dx_kernel(const void* __restrict__ x, 
                                                     const float* __restrict__ rstd, const void* __restrict__ dy,
                                                     long long lddy, const void* __restrict__ dres, long long ldres,
                                                     void* __restrict__ dx, long long lddx, int rows, int D, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -240,6 +243,7 @@ __global__ void __launch_bounds__(128) ln_bwd_fused_kernel(const void* __restric
                                                            long long ldres, void* __restrict__ dx, long long lddx,
                                                            float* __restrict__ ws, int rows, int D, int nsum,
                                                            int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   extern __shared__ float acc_sh[];  // [4 warps][3][V][8][32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* acc = acc_sh + warp * (3 * V * 256);
@@ -332,6 +336,7 @@ __global__ void __launch_bounds__(256) ln_colsum_kernel(const void* __restrict__
                                                         const void* __restrict__ dy, long long lddy,
                                                         const void* __restrict__ dx, long long lddx, int rows, int D,
                                                         int rows_per_split, float* __restrict__ ws, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   __shared__ float sh[3][8][257];
   const int cv = threadIdx.x & 31, rl = threadIdx.x >> 5;
   const int c0 = blockIdx.x * 256 + cv * 8;
@@ -410,6 +415,7 @@ __global__ void __launch_bounds__(256) ln_colsum_kernel(const void* __restrict__
 // partial lanes, four partial rows in flight per thread, fixed order
 __global__ void __launch_bounds__(1024) partials_reduce3_kernel(const float* __restrict__ ws, int nb, int D,
                                                                 void* out0, void* out1, void* out2, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   __shared__ float sm[32][33];
   const int cl = threadIdx.x & 31, kl = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
@@ -442,6 +448,7 @@ __global__ void __launch_bounds__(1024) partials_reduce3_kernel(const float* __r
 // block = 32 columns x 8 partial lanes (coalesced 128-byte reads), fixed order
 __global__ void __launch_bounds__(256) partials_reduce_kernel(const float* __restrict__ ws, int nb, int D, void* out0,
                                                               void* out1, float alpha, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   __shared__ float sa[8][33], sb[8][33];
   const int cl = threadIdx.x & 31, kl = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
@@ -472,6 +479,7 @@ __global__ void __launch_bounds__(256) partials_reduce_kernel(const float* __res
 __global__ void __launch_bounds__(256) colsum_partial_kernel(const void* __restrict__ x, long long ldx,
                                                              long long sbx, int rows, int cols, int rows_per_split,
                                                              float* __restrict__ ws, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   __shared__ float sh[8][256];
   const int cv = threadIdx.x & 31, rl = threadIdx.x >> 5;
   const int c0 = blockIdx.x * 256 + cv * 8;
@@ -522,6 +530,7 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const void* __restr
 __global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restrict__ ws, int splits, int cols,
                                                            int batches, void* out, long long ld_out, int out_dtype,
                                                            float alpha) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   __shared__ float sm[8][33];
   const int cl = threadIdx.x & 31, kl = threadIdx.x >> 5;
   const long long i = (long long)blockIdx.x * 32 + cl;  // flat (z, c)
@@ -562,6 +571,7 @@ __global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restri
 template <int R>
 __global__ void __launch_bounds__(256) softmax_fwd_rows_kernel(const void* __restrict__ S, void* __restrict__ P,
                                                                long long rows, int L, long long ld, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int lane = threadIdx.x & 31;
   const long long row0 = ((long long)blockIdx.x * 8 + (threadIdx.x >> 5)) * R;
   const int c0 = lane * 8;
@@ -600,6 +610,7 @@ template <int R>
 __global__ void __launch_bounds__(256) softmax_bwd_rows_kernel(const void* __restrict__ S, const void* __restrict__ dP,
                                                                void* __restrict__ dS, long long rows, int L,
                                                                long long ld, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int lane = threadIdx.x & 31;
   const long long row0 = ((long long)blockIdx.x * 8 + (threadIdx.x >> 5)) * R;
   const int c0 = lane * 8;
@@ -653,6 +664,7 @@ __global__ void __launch_bounds__(256) softmax_bwd_rows_kernel(const void* __res
 template <int CH>
 __global__ void __launch_bounds__(256) softmax_fwd_vec_kernel(const void* __restrict__ S, void* __restrict__ P,
                                                               long long rows, int L, long long ld, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -700,6 +712,7 @@ template <int CH>
 __global__ void __launch_bounds__(256) softmax_bwd_vec_kernel(const void* __restrict__ S, const void* __restrict__ dP,
                                                               void* __restrict__ dS, long long rows, int L,
                                                               long long ld, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -768,6 +781,7 @@ __global__ void __launch_bounds__(256) ln_bwd_vec_kernel(const void* __restrict_
                                                          long long lddy, const void* __restrict__ dres, long long ldres,
                                                          void* __restrict__ dx, long long lddx, float* __restrict__ ws,
                                                          int rows, int D, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   extern __shared__ float sh[];  // [8 warps][2][D]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float adg[V][8], adb[V][8];
@@ -834,6 +848,7 @@ __global__ void __launch_bounds__(256) ln_bwd_vec_kernel(const void* __restrict_
 // ===========================================================================
 __global__ void __launch_bounds__(256) softmax_fwd_kernel(const void* __restrict__ S, void* __restrict__ P,
                                                           long long rows, int L, long long ld, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -852,6 +867,7 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const void* __restrict
 __global__ void __launch_bounds__(256) softmax_bwd_kernel(const void* __restrict__ S, const void* __restrict__ dP,
                                                           void* __restrict__ dS, long long rows, int L, long long ld,
                                                           int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -878,6 +894,7 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const void* __restrict
 __global__ void __launch_bounds__(256) ce_fwd_kernel(const void* __restrict__ logits, long long ld,
                                                      const int32_t* __restrict__ labels, int B, int C,
                                                      float* __restrict__ nll, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= B) return;
@@ -891,6 +908,7 @@ __global__ void __launch_bounds__(256) ce_fwd_kernel(const void* __restrict__ lo
   if (lane == 0) nll[row] = logf(s) - (ld_h(logits, base + labels[row], fmt) - m);
 }
 __global__ void ce_mean_kernel(const float* __restrict__ nll, int B, float* __restrict__ loss) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   __shared__ float sh[32];
   float s = 0.f;
   for (int i = threadIdx.x; i < B; i += blockDim.x) s += nll[i];
@@ -908,6 +926,7 @@ __global__ void __launch_bounds__(256) ce_bwd_kernel(const void* __restrict__ lo
                                                      const int32_t* __restrict__ labels, int B, int C,
                                                      const float* __restrict__ dloss, void* __restrict__ dz,
                                                      long long ldd, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= B) return;
@@ -933,6 +952,7 @@ __global__ void __launch_bounds__(256) ce_bwd_kernel(const void* __restrict__ lo
 // ===========================================================================
 __global__ void patchify_kernel(const uint16_t* __restrict__ img, uint16_t* __restrict__ out, int B, int H, int W,
                                 int C, int p) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int nh = H / p, nw = W / p, K = p * p * C;
   const long long n = (long long)B * nh * nw * K;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -951,6 +971,7 @@ __global__ void patchify_kernel(const uint16_t* __restrict__ img, uint16_t* __re
 // 2-D index (segment, vector) per thread, no 64-bit divides in the loop body
 __global__ void __launch_bounds__(256) patchify_vec_kernel(const uint4* __restrict__ img, uint4* __restrict__ out,
                                                            int B, int H, int W, int C, int p) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int nh = H / p, nw = W / p;
   const int seg_v = p * C / 8;                  // 16-byte vectors per (patch, py) segment
   const long long nseg = (long long)B * nh * nw * p;
@@ -973,6 +994,7 @@ __global__ void __launch_bounds__(256) copy_rows_vec_kernel(const uint16_t* __re
                                                             long long sb_src, uint16_t* __restrict__ dst,
                                                             long long ld_dst, long long sb_dst, int rows, int batches,
                                                             int cols) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int cv = cols / 8;
   const long long n = (long long)batches * rows * cv;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -989,6 +1011,7 @@ __global__ void __launch_bounds__(256) copy_rows_vec_kernel(const uint16_t* __re
 __global__ void copy_rows_kernel(const uint16_t* __restrict__ src, long long ld_src, long long sb_src,
                                  uint16_t* __restrict__ dst, long long ld_dst, long long sb_dst, int rows, int batches,
                                  int cols) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const long long n = (long long)batches * rows * cols;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const long long bc = i / cols;
@@ -1001,6 +1024,7 @@ __global__ void copy_rows_kernel(const uint16_t* __restrict__ src, long long ld_
 // dst[b*sb + c] = round(a[c] + b[c])  (cls token + its position embedding)
 __global__ void rows_add_kernel(const void* __restrict__ a, const void* __restrict__ b2, void* __restrict__ dst,
                                 long long sb, int B, int D, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const long long n = (long long)B * D;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const long long b = i / D;
@@ -1012,6 +1036,7 @@ __global__ void rows_add_kernel(const void* __restrict__ a, const void* __restri
 // dst[b][r][c] = alpha * src[b][c]   (mean-pool backward broadcast)
 __global__ void bcast_rows_kernel(const void* __restrict__ src, long long ld_src, void* __restrict__ dst,
                                   long long ld_dst, long long sb_dst, int rows, int B, int D, float alpha, int fmt) {
+  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const long long n = (long long)B * rows * D;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const long long bc = i / D;
@@ -1046,13 +1071,13 @@ int mpx_layernorm_fwd(int dtype, const void* x, int64_t ldx, const void* gain, c
                                                          reinterpret_cast<uintptr_t>(bias)) % 16 == 0);
   const int f = fmt_of(dtype);
   if (vec && D == 768)
-    ln_fwd_kernel<3><<<grid, 256, 0, st>>>(x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f);
+    MPX_CUDA_CHECK(::mpx::launch_k(ln_fwd_kernel<3>, grid, 256, 0, st, x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f));
   else if (vec && D == 1024)
-    ln_fwd_kernel<4><<<grid, 256, 0, st>>>(x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f);
+    MPX_CUDA_CHECK(::mpx::launch_k(ln_fwd_kernel<4>, grid, 256, 0, st, x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f));
   else if (vec && D == 512)
-    ln_fwd_kernel<2><<<grid, 256, 0, st>>>(x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f);
+    MPX_CUDA_CHECK(::mpx::launch_k(ln_fwd_kernel<2>, grid, 256, 0, st, x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f));
   else
-    ln_fwd_kernel<0><<<grid, 256, 0, st>>>(x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f);
+    MPX_CUDA_CHECK(::mpx::launch_k(ln_fwd_kernel<0>, grid, 256, 0, st, x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f));
   MPX_LAUNCH_CHECK("ln_fwd_kernel");
   return 0;
 }
@@ -1089,19 +1114,19 @@ int mpx_layernorm_bwd(int dtype, const void* x, int64_t ldx, const void* gain, c
     }
   }
   if (vec && D == 768)
-    ln_bwd_vec_kernel<3><<<nb, 256, sh, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace,
-                                              rows, D, f);
+    MPX_CUDA_CHECK(::mpx::launch_k(ln_bwd_vec_kernel<3>, nb, 256, sh, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace,
+                                              rows, D, f));
   else if (vec && D == 1024)  // (v2 would spill at 4 vectors per lane)
-    ln_bwd_vec_kernel<4><<<nb, 256, sh, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace,
-                                              rows, D, f);
+    MPX_CUDA_CHECK(::mpx::launch_k(ln_bwd_vec_kernel<4>, nb, 256, sh, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace,
+                                              rows, D, f));
   else if (vec && D == 256)
-    ln_bwd_vec_kernel<1><<<nb, 256, sh, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace,
-                                              rows, D, f);
+    MPX_CUDA_CHECK(::mpx::launch_k(ln_bwd_vec_kernel<1>, nb, 256, sh, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace,
+                                              rows, D, f));
   else
-    ln_bwd_kernel<<<nb, 256, sh, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace, rows, D,
-                                       f);
+    MPX_CUDA_CHECK(::mpx::launch_k(ln_bwd_kernel, nb, 256, sh, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace, rows, D,
+                                       f));
   MPX_LAUNCH_CHECK("ln_bwd_kernel");
-  partials_reduce_kernel<<<(D + 31) / 32, 256, 0, st>>>(workspace, nb, D, dgain, dbias, 1.f, f);
+  MPX_CUDA_CHECK(::mpx::launch_k(partials_reduce_kernel, (D + 31) / 32, 256, 0, st, workspace, nb, D, dgain, dbias, 1.f, f));
   MPX_LAUNCH_CHECK("partials_reduce_kernel");
   return 0;
 }
@@ -1137,24 +1162,24 @@ int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, 
       cudaFuncSetAttribute(ln_bwd_fused_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
     });
     switch (D / 256) {
-      case 1: ln_bwd_fused_kernel<1><<<blocks, 128, shb, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx,
-                                                               workspace, rows, D, nsum, f); break;
-      case 2: ln_bwd_fused_kernel<2><<<blocks, 128, shb, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx,
-                                                               workspace, rows, D, nsum, f); break;
-      default: ln_bwd_fused_kernel<3><<<blocks, 128, shb, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx,
-                                                                lddx, workspace, rows, D, nsum, f); break;
+      case 1: MPX_CUDA_CHECK(::mpx::launch_k(ln_bwd_fused_kernel<1>, blocks, 128, shb, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx,
+                                                               workspace, rows, D, nsum, f)); break;
+      case 2: MPX_CUDA_CHECK(::mpx::launch_k(ln_bwd_fused_kernel<2>, blocks, 128, shb, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx,
+                                                               workspace, rows, D, nsum, f)); break;
+      default: MPX_CUDA_CHECK(::mpx::launch_k(ln_bwd_fused_kernel<3>, blocks, 128, shb, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx,
+                                                                lddx, workspace, rows, D, nsum, f)); break;
     }
     MPX_LAUNCH_CHECK("ln_bwd_fused_kernel");
-    partials_reduce3_kernel<<<dim3((D + 31) / 32, nsum), 1024, 0, st>>>(workspace, blocks, D, dgain, dbias, dxsum, f);
+    MPX_CUDA_CHECK(::mpx::launch_k(partials_reduce3_kernel, dim3((D + 31) / 32, nsum), 1024, 0, st, workspace, blocks, D, dgain, dbias, dxsum, f));
     MPX_LAUNCH_CHECK("partials_reduce3_kernel");
     return 0;
   }
   const unsigned g1 = (unsigned)((rows + 7) / 8);
   switch (D / 256) {
-    case 1: ln_dx_kernel<1><<<g1, 256, 0, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f); break;
-    case 2: ln_dx_kernel<2><<<g1, 256, 0, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f); break;
-    case 3: ln_dx_kernel<3><<<g1, 256, 0, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f); break;
-    default: ln_dx_kernel<4><<<g1, 256, 0, st>>>(x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f); break;
+    case 1: MPX_CUDA_CHECK(::mpx::launch_k(ln_dx_kernel<1>, g1, 256, 0, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f)); break;
+    case 2: MPX_CUDA_CHECK(::mpx::launch_k(ln_dx_kernel<2>, g1, 256, 0, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f)); break;
+    case 3: MPX_CUDA_CHECK(::mpx::launch_k(ln_dx_kernel<3>, g1, 256, 0, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f)); break;
+    default: MPX_CUDA_CHECK(::mpx::launch_k(ln_dx_kernel<4>, g1, 256, 0, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, rows, D, f)); break;
   }
   MPX_LAUNCH_CHECK("ln_dx_kernel");
   const int cblocks = D / 256;
@@ -1162,10 +1187,10 @@ int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, 
   int splits = std::max(1, std::min(rows / 64, current_num_sms() * 8 / cblocks));
   while ((long long)nsum * splits * D > workspace_floats && splits > 1) splits /= 2;
   const int rps = (rows + splits - 1) / splits;
-  ln_colsum_kernel<<<dim3(cblocks, splits), 256, 0, st>>>(x, ldx, mean, rstd, dy, lddy, dxsum ? dx : nullptr, lddx, rows,
-                                                         D, rps, workspace, f);
+  MPX_CUDA_CHECK(::mpx::launch_k(ln_colsum_kernel, dim3(cblocks, splits), 256, 0, st, x, ldx, mean, rstd, dy, lddy, dxsum ? dx : nullptr, lddx, rows,
+                                                         D, rps, workspace, f));
   MPX_LAUNCH_CHECK("ln_colsum_kernel");
-  partials_reduce3_kernel<<<dim3((D + 31) / 32, nsum), 1024, 0, st>>>(workspace, splits, D, dgain, dbias, dxsum, f);
+  MPX_CUDA_CHECK(::mpx::launch_k(partials_reduce3_kernel, dim3((D + 31) / 32, nsum), 1024, 0, st, workspace, splits, D, dgain, dbias, dxsum, f));
   MPX_LAUNCH_CHECK("partials_reduce3_kernel");
   return 0;
 }
@@ -1183,10 +1208,10 @@ int mpx_colsum(int dtype, const void* x, int64_t ldx, int64_t sbx, int rows, int
   if ((long long)splits * cols * batches > workspace_floats) return fail(MPX_EINVAL, "colsum: workspace too small");
   const int rps = (rows + splits - 1) / splits;
   dim3 grid(cblocks, splits, batches);
-  colsum_partial_kernel<<<grid, 256, 0, st>>>(x, ldx, sbx, rows, cols, rps, workspace, fmt_of(dtype));
+  MPX_CUDA_CHECK(::mpx::launch_k(colsum_partial_kernel, grid, 256, 0, st, x, ldx, sbx, rows, cols, rps, workspace, fmt_of(dtype)));
   MPX_LAUNCH_CHECK("colsum_partial_kernel");
-  colsum_final_kernel<<<(unsigned)(((long long)cols * batches + 31) / 32), 256, 0, st>>>(workspace, splits, cols, batches,
-                                                                                      out, ld_out, out_dtype, alpha);
+  MPX_CUDA_CHECK(::mpx::launch_k(colsum_final_kernel, (unsigned)(((long long)cols * batches + 31) / 32), 256, 0, st, workspace, splits, cols, batches,
+                                                                                      out, ld_out, out_dtype, alpha));
   MPX_LAUNCH_CHECK("colsum_final_kernel");
   return 0;
 }
@@ -1198,11 +1223,11 @@ int mpx_softmax_fwd(int dtype, const void* S, void* P, int64_t rows, int L, int6
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool vec = ld % 8 == 0 && ((reinterpret_cast<uintptr_t>(S) | reinterpret_cast<uintptr_t>(P)) % 16 == 0);
   if (vec && ld <= 256)
-    softmax_fwd_rows_kernel<4><<<(unsigned)((rows + 31) / 32), 256, 0, st>>>(S, P, rows, L, ld, fmt_of(dtype));
+    MPX_CUDA_CHECK(::mpx::launch_k(softmax_fwd_rows_kernel<4>, (unsigned)((rows + 31) / 32), 256, 0, st, S, P, rows, L, ld, fmt_of(dtype)));
   else if (vec && ld <= 512)
-    softmax_fwd_vec_kernel<2><<<grid, 256, 0, st>>>(S, P, rows, L, ld, fmt_of(dtype));
+    MPX_CUDA_CHECK(::mpx::launch_k(softmax_fwd_vec_kernel<2>, grid, 256, 0, st, S, P, rows, L, ld, fmt_of(dtype)));
   else
-    softmax_fwd_kernel<<<grid, 256, 0, st>>>(S, P, rows, L, ld, fmt_of(dtype));
+    MPX_CUDA_CHECK(::mpx::launch_k(softmax_fwd_kernel, grid, 256, 0, st, S, P, rows, L, ld, fmt_of(dtype)));
   MPX_LAUNCH_CHECK("softmax_fwd_kernel");
   return 0;
 }
@@ -1215,11 +1240,11 @@ int mpx_softmax_bwd(int dtype, const void* S, const void* dP, void* dS, int64_t 
   const bool vec = ld % 8 == 0 && ((reinterpret_cast<uintptr_t>(S) | reinterpret_cast<uintptr_t>(dP) |
                                     reinterpret_cast<uintptr_t>(dS)) % 16 == 0);
   if (vec && ld <= 256)
-    softmax_bwd_rows_kernel<4><<<(unsigned)((rows + 31) / 32), 256, 0, st>>>(S, dP, dS, rows, L, ld, fmt_of(dtype));
+    MPX_CUDA_CHECK(::mpx::launch_k(softmax_bwd_rows_kernel<4>, (unsigned)((rows + 31) / 32), 256, 0, st, S, dP, dS, rows, L, ld, fmt_of(dtype)));
   else if (vec && ld <= 512)
-    softmax_bwd_vec_kernel<2><<<grid, 256, 0, st>>>(S, dP, dS, rows, L, ld, fmt_of(dtype));
+    MPX_CUDA_CHECK(::mpx::launch_k(softmax_bwd_vec_kernel<2>, grid, 256, 0, st, S, dP, dS, rows, L, ld, fmt_of(dtype)));
   else
-    softmax_bwd_kernel<<<grid, 256, 0, st>>>(S, dP, dS, rows, L, ld, fmt_of(dtype));
+    MPX_CUDA_CHECK(::mpx::launch_k(softmax_bwd_kernel, grid, 256, 0, st, S, dP, dS, rows, L, ld, fmt_of(dtype)));
   MPX_LAUNCH_CHECK("softmax_bwd_kernel");
   return 0;
 }
@@ -1228,9 +1253,9 @@ int mpx_cross_entropy_fwd(int dtype, const void* logits, int64_t ld, const int32
                           float* nll_ws, float* loss, void* stream) {
   if (!half_dtype(dtype)) return fail(MPX_EINVAL, "cross_entropy: f16/bf16 logits only");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  ce_fwd_kernel<<<(B + 7) / 8, 256, 0, st>>>(logits, ld, labels, B, C, nll_ws, fmt_of(dtype));
+  MPX_CUDA_CHECK(::mpx::launch_k(ce_fwd_kernel, (B + 7) / 8, 256, 0, st, logits, ld, labels, B, C, nll_ws, fmt_of(dtype)));
   MPX_LAUNCH_CHECK("ce_fwd_kernel");
-  ce_mean_kernel<<<1, 1024, 0, st>>>(nll_ws, B, loss);
+  MPX_CUDA_CHECK(::mpx::launch_k(ce_mean_kernel, 1, 1024, 0, st, nll_ws, B, loss));
   MPX_LAUNCH_CHECK("ce_mean_kernel");
   return 0;
 }
@@ -1238,8 +1263,8 @@ int mpx_cross_entropy_fwd(int dtype, const void* logits, int64_t ld, const int32
 int mpx_cross_entropy_bwd(int dtype, const void* logits, int64_t ld, const int32_t* labels, int B, int C,
                           const float* d_dloss, void* dlogits, int64_t ld_d, void* stream) {
   if (!half_dtype(dtype)) return fail(MPX_EINVAL, "cross_entropy_bwd: f16/bf16 only");
-  ce_bwd_kernel<<<(B + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(logits, ld, labels, B, C, d_dloss, dlogits,
-                                                                             ld_d, fmt_of(dtype));
+  MPX_CUDA_CHECK(::mpx::launch_k(ce_bwd_kernel, (B + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream), logits, ld, labels, B, C, d_dloss, dlogits,
+                                                                             ld_d, fmt_of(dtype)));
   MPX_LAUNCH_CHECK("ce_bwd_kernel");
   return 0;
 }
@@ -1249,13 +1274,11 @@ int mpx_patchify(int dtype, const void* img, void* patches, int B, int H, int W,
   const long long n = (long long)B * H * W * C;
   if ((P * C) % 8 == 0 && (W * C) % 8 == 0 &&
       ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(patches)) & 15) == 0) {
-    patchify_vec_kernel<<<ew_grid(n / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const uint4*>(img), static_cast<uint4*>(patches), B, H, W, C, P);
+    MPX_CUDA_CHECK(::mpx::launch_k(patchify_vec_kernel, ew_grid(n / 8), 256, 0, static_cast<cudaStream_t>(stream), static_cast<const uint4*>(img), static_cast<uint4*>(patches), B, H, W, C, P));
     MPX_LAUNCH_CHECK("patchify_vec_kernel");
     return 0;
   }
-  patchify_kernel<<<ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint16_t*>(img), static_cast<uint16_t*>(patches), B, H, W, C, P);
+  MPX_CUDA_CHECK(::mpx::launch_k(patchify_kernel, ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream), static_cast<const uint16_t*>(img), static_cast<uint16_t*>(patches), B, H, W, C, P));
   MPX_LAUNCH_CHECK("patchify_kernel");
   return 0;
 }
@@ -1267,23 +1290,21 @@ int mpx_copy_rows(int dtype, const void* src, int64_t ld_src, int64_t sb_src, vo
   if (n <= 0) return 0;
   if (cols % 8 == 0 && ld_src % 8 == 0 && sb_src % 8 == 0 && ld_dst % 8 == 0 && sb_dst % 8 == 0 &&
       ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
-    copy_rows_vec_kernel<<<ew_grid(n / 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const uint16_t*>(src), ld_src, sb_src, static_cast<uint16_t*>(dst), ld_dst, sb_dst, rows, batches,
-        cols);
+    MPX_CUDA_CHECK(::mpx::launch_k(copy_rows_vec_kernel, ew_grid(n / 8), 256, 0, static_cast<cudaStream_t>(stream), static_cast<const uint16_t*>(src), ld_src, sb_src, static_cast<uint16_t*>(dst), ld_dst, sb_dst, rows, batches,
+        cols));
     MPX_LAUNCH_CHECK("copy_rows_vec_kernel");
     return 0;
   }
-  copy_rows_kernel<<<ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint16_t*>(src), ld_src, sb_src, static_cast<uint16_t*>(dst), ld_dst, sb_dst, rows, batches,
-      cols);
+  MPX_CUDA_CHECK(::mpx::launch_k(copy_rows_kernel, ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream), static_cast<const uint16_t*>(src), ld_src, sb_src, static_cast<uint16_t*>(dst), ld_dst, sb_dst, rows, batches,
+      cols));
   MPX_LAUNCH_CHECK("copy_rows_kernel");
   return 0;
 }
 
 int mpx_rows_add(int dtype, const void* a, const void* b, void* dst, int64_t sb, int B, int D, void* stream) {
   if (!half_dtype(dtype)) return fail(MPX_EINVAL, "rows_add: f16/bf16 only");
-  rows_add_kernel<<<ew_grid((long long)B * D), 256, 0, static_cast<cudaStream_t>(stream)>>>(a, b, dst, sb, B, D,
-                                                                                            fmt_of(dtype));
+  MPX_CUDA_CHECK(::mpx::launch_k(rows_add_kernel, ew_grid((long long)B * D), 256, 0, static_cast<cudaStream_t>(stream), a, b, dst, sb, B, D,
+                                                                                            fmt_of(dtype)));
   MPX_LAUNCH_CHECK("rows_add_kernel");
   return 0;
 }
@@ -1291,8 +1312,7 @@ int mpx_rows_add(int dtype, const void* a, const void* b, void* dst, int64_t sb,
 int mpx_bcast_rows(int dtype, const void* src, int64_t ld_src, void* dst, int64_t ld_dst, int64_t sb_dst, int rows,
                    int B, int D, float alpha, void* stream) {
   if (!half_dtype(dtype)) return fail(MPX_EINVAL, "bcast_rows: f16/bf16 only");
-  bcast_rows_kernel<<<ew_grid((long long)B * rows * D), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      src, ld_src, dst, ld_dst, sb_dst, rows, B, D, alpha, fmt_of(dtype));
+  MPX_CUDA_CHECK(::mpx::launch_k(bcast_rows_kernel, ew_grid((long long)B * rows * D), 256, 0, static_cast<cudaStream_t>(stream), src, ld_src, dst, ld_dst, sb_dst, rows, B, D, alpha, fmt_of(dtype)));
   MPX_LAUNCH_CHECK("bcast_rows_kernel");
   return 0;
 }
