@@ -21,6 +21,7 @@
 
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
 #include <type_traits>
 
@@ -493,6 +494,7 @@ struct AttnBwdParams {
   long long ld;
   const float2* stats;  // the forward's row statistics, or null (recomputed here)
   float* csum;          // optional per-image column sums of dqkv [B][3*H*hd] (the qkv bias gradient's partials)
+  int items;            // B * H work items, walked by a persistent grid
 };
 
 // 16 values per lane -> column sums over the warp's 32 lanes (rows) by recursive
@@ -529,13 +531,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* sV = sK + kAttnKV;
   uint8_t* sP = sV + kAttnKV;
   uint8_t* sdS = sP + kAttnP;
-  // 0 kv, 1 q/dO, 2 S, 3 P, 4 dP, 5 dS, 6 dQ(+dV,dK), 7 dQ read, 8 Q free (dK), 9 dO free (dV)
+  // 0 kv, 1 q/dO, 2 S, 3 P, 4 dP, 5 dS, 6 dQ(+dV,dK), 7 dQ read, 8 Q free (dK), 9 dO free (dV),
+  // 10 dV/dK read out (the next item may overwrite TMEM cols 256-511)
   float* red = reinterpret_cast<float*>(sdS + kAttnP);
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + kSplit * 128);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int h = blockIdx.x % P.H, b = blockIdx.x / P.H;
   const int T = P.m_tiles;
   const long long D = (long long)P.H * P.hd;
 
@@ -544,7 +546,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     tma_prefetch(&tmdO);
-    for (int i = 0; i < 10; ++i) mbar_init(&bar[i], (i == 3 || i == 5 || i == 7) ? 128 * kSplit : 1);
+    for (int i = 0; i < 11; ++i) mbar_init(&bar[i], (i == 3 || i == 5 || i == 7 || i == 10) ? 128 * kSplit : 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -556,12 +558,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(&bar[0], 2 * kAttnKV);
-      tma_load_4d(sK, &tmK, &bar[0], 0, 0, h, b);
-      tma_load_4d(sV, &tmV, &bar[0], 0, 0, h, b);
-      mbar_arrive_expect_tx(&bar[1], 2 * kAttnQ);
-      tma_load_4d(sQ, &tmQ, &bar[1], 0, 0, h, b);
-      tma_load_4d(sdO, &tmdO, &bar[1], 0, 0, h, b);
+      // persistent: items blockIdx.x, + gridDim.x, ...; the next item's K/V/Q/dO
+      // are loaded as soon as this item's last MMAs have read the tiles, so
+      // they land during the dQ / dV / dK readouts
+      auto load_item = [&](int item) {
+        const int hh = item % P.H, bb = item / P.H;
+        mbar_arrive_expect_tx(&bar[0], 2 * kAttnKV);
+        tma_load_4d(sK, &tmK, &bar[0], 0, 0, hh, bb);
+        tma_load_4d(sV, &tmV, &bar[0], 0, 0, hh, bb);
+        mbar_arrive_expect_tx(&bar[1], 2 * kAttnQ);
+        tma_load_4d(sQ, &tmQ, &bar[1], 0, 0, hh, bb);
+        tma_load_4d(sdO, &tmdO, &bar[1], 0, 0, hh, bb);
+      };
       const uint32_t q = smem_u32(sQ), dO = smem_u32(sdO), k = smem_u32(sK), v = smem_u32(sV);
       const uint32_t pp = smem_u32(sP), ds = smem_u32(sdS);
       const int n_chunks = (P.N + 15) / 16;
@@ -570,55 +578,65 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t id_nk = idesc_f16(P.fmt, 128, 16 * n_chunks, 0, 0);
       const uint32_t id_kv = idesc_f16(P.fmt, 128, 64, 1, 1);   // dV / dK halves: A, B MN-major
       const uint32_t id_q = idesc_f16(P.fmt, 128, 64, 0, 1);    // dQ: A K-major, B MN-major
-      ATRACE(0);
-      mbar_wait(&bar[0], 0);
-      ATRACE(1);
-      for (int t = 0; t < T; ++t) {
-        const uint32_t ph = t & 1;
-        mbar_wait(&bar[1], ph);
-        ATRACE(2 + 8 * t);
-        if (t > 0) mbar_wait(&bar[7], ph ^ 1);  // previous dQ drained from TMEM cols 0-63
-        tc_fence_after();
+      uint32_t gt = 0;  // tiles so far (barrier phases)
+      int it = 0;       // items so far
+      if (blockIdx.x < P.items) load_item(blockIdx.x);
+      for (int item = blockIdx.x; item < P.items; item += gridDim.x, ++it) {
+        const int h = item % P.H, b = item / P.H;
+        ATRACE(0);
+        mbar_wait(&bar[0], it & 1);
+        ATRACE(1);
+        for (int t = 0; t < T; ++t, ++gt) {
+          const uint32_t ph = gt & 1;
+          mbar_wait(&bar[1], ph);
+          if (it == 0) ATRACE(2 + 8 * t);
+          if (gt > 0) mbar_wait(&bar[7], ph ^ 1);  // previous dQ drained from TMEM cols 0-63
+          tc_fence_after();
 #pragma unroll
-        for (int s = 0; s < 4; ++s)  // S = Q K^T
-          umma_f16(tmem, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), id_nk, s > 0);
-        umma_commit(&bar[2]);
-        mbar_wait(&bar[3], ph);  // P_t written (S consumed)
-        ATRACE(3 + 8 * t);
-        tc_fence_after();
+          for (int s = 0; s < 4; ++s)  // S = Q K^T
+            umma_f16(tmem, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), id_nk, s > 0);
+          umma_commit(&bar[2]);
+          mbar_wait(&bar[3], ph);  // P_t written (S consumed)
+          if (it == 0) ATRACE(3 + 8 * t);
+          tc_fence_after();
 #pragma unroll
-        for (int s = 0; s < 4; ++s)  // dP = dO V^T
-          umma_f16(tmem, sw128_desc(dO + s * 32, 16, 1024), sw128_desc(v + s * 32, 16, 1024), id_nk, s > 0);
-        umma_commit(&bar[4]);
-        mbar_wait(&bar[5], ph);  // dS_t written (dP consumed)
-        ATRACE(4 + 8 * t);
-        tc_fence_after();
-        // dK first (its completion frees Q_t), then dV (frees dO_t), then dQ:
-        // the next tile's Q / dO loads overlap dV, dQ and the dQ readout
-        for (int half = 0; half < halves; ++half) {
+          for (int s = 0; s < 4; ++s)  // dP = dO V^T
+            umma_f16(tmem, sw128_desc(dO + s * 32, 16, 1024), sw128_desc(v + s * 32, 16, 1024), id_nk, s > 0);
+          umma_commit(&bar[4]);
+          mbar_wait(&bar[5], ph);  // dS_t written (dP consumed)
+          if (it == 0) ATRACE(4 + 8 * t);
+          if (t == 0 && it > 0) mbar_wait(&bar[10], (it - 1) & 1);  // last item's dV/dK read out of TMEM
+          tc_fence_after();
+          // dK first (its completion frees Q_t), then dV (frees dO_t), then dQ:
+          // the next tile's Q / dO loads overlap dV, dQ and the dQ readout
+          for (int half = 0; half < halves; ++half) {
 #pragma unroll
-          for (int s = 0; s < 8; ++s)  // over the 128 queries of the tile: dK += dS^T Q
-            umma_f16(tmem + 384 + half * 64, sw128_desc(ds + half * 32768 + s * 2048, 16384, 1024),
-                     sw128_desc(q + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
-        }
-        umma_commit(&bar[8]);
-        for (int half = 0; half < halves; ++half) {
+            for (int s = 0; s < 8; ++s)  // over the 128 queries of the tile: dK += dS^T Q
+              umma_f16(tmem + 384 + half * 64, sw128_desc(ds + half * 32768 + s * 2048, 16384, 1024),
+                       sw128_desc(q + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
+          }
+          umma_commit(&bar[8]);
+          for (int half = 0; half < halves; ++half) {
 #pragma unroll
-          for (int s = 0; s < 8; ++s)  // dV += P^T dO
-            umma_f16(tmem + 256 + half * 64, sw128_desc(pp + half * 32768 + s * 2048, 16384, 1024),
-                     sw128_desc(dO + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
-        }
-        umma_commit(&bar[9]);
-        for (int s = 0; s < n_chunks; ++s)  // dQ = dS K
-          umma_f16(tmem, sw128_desc(ds + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024), sw128_desc(k + s * 2048, 8192, 1024),
-                   id_q, s > 0);
-        umma_commit(&bar[6]);
-        if (t + 1 < T) {  // next tile's Q / dO as soon as this tile's MMAs have read them
-          mbar_arrive_expect_tx(&bar[1], 2 * kAttnQ);
-          mbar_wait(&bar[8], ph);
-          tma_load_4d(sQ, &tmQ, &bar[1], 0, (t + 1) * 128, h, b);
-          mbar_wait(&bar[9], ph);
-          tma_load_4d(sdO, &tmdO, &bar[1], 0, (t + 1) * 128, h, b);
+            for (int s = 0; s < 8; ++s)  // dV += P^T dO
+              umma_f16(tmem + 256 + half * 64, sw128_desc(pp + half * 32768 + s * 2048, 16384, 1024),
+                       sw128_desc(dO + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
+          }
+          umma_commit(&bar[9]);
+          for (int s = 0; s < n_chunks; ++s)  // dQ = dS K
+            umma_f16(tmem, sw128_desc(ds + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
+                     sw128_desc(k + s * 2048, 8192, 1024), id_q, s > 0);
+          umma_commit(&bar[6]);
+          if (t + 1 < T) {  // next tile's Q / dO as soon as this tile's MMAs have read them
+            mbar_arrive_expect_tx(&bar[1], 2 * kAttnQ);
+            mbar_wait(&bar[8], ph);
+            tma_load_4d(sQ, &tmQ, &bar[1], 0, (t + 1) * 128, h, b);
+            mbar_wait(&bar[9], ph);
+            tma_load_4d(sdO, &tmdO, &bar[1], 0, (t + 1) * 128, h, b);
+          } else if (item + (int)gridDim.x < P.items) {  // next item, once every tile has been read
+            mbar_wait(&bar[6], ph);
+            load_item(item + gridDim.x);
+          }
         }
       }
     }
@@ -639,14 +657,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     };
     constexpr int kMaxC = 16 / kSplit;  // chunks per thread
     static_assert(kSplit == 4, "dQ readout: one chunk per split");
+    uint32_t gt = 0;  // tiles so far (barrier phases)
+    int it = 0;       // items so far
+    for (int item = blockIdx.x; item < P.items; item += gridDim.x, ++it) {
+    const int h = item % P.H, b = item / P.H;
     float qsum = 0.f;  // column col16(lane) of chunk `split` of dQ, summed over this warp's rows and the tiles
-    for (int t = 0; t < T; ++t) {
-      const uint32_t ph = t & 1;
+    for (int t = 0; t < T; ++t, ++gt) {
+      const uint32_t ph = gt & 1;
       // ---- P = softmax(round(S * scale)) -> smem (as in the forward)
       float2 st = make_float2(0.f, 0.f);  // the forward's (max, 1/sum), fetched while S is computed
-      if (P.stats) st = __ldg(P.stats + ((long long)blockIdx.x * T + t) * 128 + r);
+      if (P.stats) st = __ldg(P.stats + ((long long)item * T + t) * 128 + r);
       mbar_wait(&bar[2], ph);
-      if (warp == 4 && lane == 0) ATRACE(5 + 8 * t);
+      if (warp == 4 && lane == 0 && it == 0) ATRACE(5 + 8 * t);
       tc_fence_after();
       softmax_bwd_p<kSplit>(trow, split, r, qd, P.N, P.scale, P.fmt, red, sP, P.stats ? &st : nullptr);
       fence_async_smem();
@@ -655,7 +677,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       // ---- dS = P * (dP - sum(P * dP)) -> smem; dP rounded to the half
       // format first (the reference's dP is a half GEMM output), kept packed
       mbar_wait(&bar[4], ph);
-      if (warp == 4 && lane == 0) ATRACE(6 + 8 * t);
+      if (warp == 4 && lane == 0 && it == 0) ATRACE(6 + 8 * t);
       tc_fence_after();
       uint32_t dpk[kMaxC][8];
       float2 tsum2 = f2(0.f);
@@ -706,7 +728,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_arrive(&bar[5]);
       // ---- dQ_t -> dqkv[:, q part]
       mbar_wait(&bar[6], ph);
-      if (warp == 4 && lane == 0) ATRACE(7 + 8 * t);
+      if (warp == 4 && lane == 0 && it == 0) ATRACE(7 + 8 * t);
       tc_fence_after();
       const int qrow = t * 128 + r;
       uint16_t* o = static_cast<uint16_t*>(P.dqkv) + ((long long)b * P.N + qrow) * P.ld + (long long)h * P.hd;
@@ -735,7 +757,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bar[7]);
-      if (warp == 4 && lane == 0) ATRACE(8 + 8 * t);
+      if (warp == 4 && lane == 0 && it == 0) ATRACE(8 + 8 * t);
     }
     // ---- dV, dK (keys r and 128 + r of this head): 4 (half, which) combos split over the warps
     float kvsum[4] = {0.f, 0.f, 0.f, 0.f};  // per chunk: column col16(lane), this warp's 32 keys
@@ -769,9 +791,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
     }
     if (P.csum) {
-      // combine the warps' partials through the (now idle) Q tile: slots
+      // combine the warps' partials through the (now idle) P tile — the next
+      // item's Q may already be landing in the Q tile: slots
       // [part q/k/v][quarter (and key half)][64 columns], then one fixed-order sum
-      float* sc = reinterpret_cast<float*>(sQ);
+      float* sc = reinterpret_cast<float*>(sP);
       if ((lane & 1) == 0) {
         sc[(0 * 8 + qd) * 64 + split * 16 + col16(lane)] = qsum;
 #pragma unroll
@@ -787,6 +810,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int j = 0; j < nslot; ++j) a += sc[(part * 8 + j) * 64 + col];
         P.csum[(long long)b * 3 * D + part * D + (long long)h * P.hd + col] = a;
       }
+      asm volatile("bar.sync 6, %0;" ::"n"(128 * kSplit) : "memory");  // scratch read before the next P tile
+    }
+    // dV/dK (and the scratch) consumed: the next item may accumulate into TMEM cols 256-511
+    tc_fence_before();
+    mbar_arrive(&bar[10]);
     }
   }
   tc_fence_before();
@@ -910,8 +938,10 @@ extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int
     err = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnBwdSmem);
   });
   if (err != cudaSuccess) return fail((int)err, "cudaFuncSetAttribute(attn_bwd_kernel)");
-  MPX_CUDA_CHECK(::mpx::launch_k(attn_bwd_kernel, (unsigned)(B * H), kAttnThreads, kAttnBwdSmem, static_cast<cudaStream_t>(stream), tq, tk, tv, tdo,
-                                                                                                       P));
+  P.items = B * H;  // persistent: one CTA per SM walks the (image, head) items
+  const unsigned grid = (unsigned)std::min(B * H, current_num_sms());
+  MPX_CUDA_CHECK(::mpx::launch_k(attn_bwd_kernel, grid, kAttnThreads, kAttnBwdSmem, static_cast<cudaStream_t>(stream),
+                                 tq, tk, tv, tdo, P));
   MPX_LAUNCH_CHECK("attn_bwd_kernel");
   if (colsum_out) {  // the qkv bias gradient: sum the per-image partials [B][3D]
     const int cols = 3 * D;
