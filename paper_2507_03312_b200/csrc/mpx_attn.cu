@@ -826,9 +826,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   }
 }
 
-// the column-sum second pass (mpx_vit.cu)
-__global__ void colsum_final_kernel(const float* __restrict__ ws, int splits, int cols, int batches, void* out,
-                                    long long ld_out, int out_dtype, float alpha);
+// the column-sum second pass over many partial rows (mpx_gemm.cu)
+__global__ void colsum_parts_kernel(const float* __restrict__ parts, int nparts, int N, void* out, int out_dtype);
 
 static PFN_cuTensorMapEncodeTiled_v12000 attn_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -945,8 +944,8 @@ extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int
   MPX_LAUNCH_CHECK("attn_bwd_kernel");
   if (colsum_out) {  // the qkv bias gradient: sum the per-image partials [B][3D]
     const int cols = 3 * D;
-    MPX_CUDA_CHECK(::mpx::launch_k(colsum_final_kernel, (unsigned)((cols + 31) / 32), 256, 0, static_cast<cudaStream_t>(stream), colsum_ws, B, cols, 1, colsum_out, cols, dtype, 1.f));
-    MPX_LAUNCH_CHECK("colsum_final_kernel");
+    MPX_CUDA_CHECK(::mpx::launch_k(colsum_parts_kernel, (unsigned)((cols + 31) / 32), 1024, 0,
+                                   static_cast<cudaStream_t>(stream), colsum_ws, B, cols, colsum_out, dtype));
   }
   return 0;
 }
