@@ -151,7 +151,9 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
     from paper_2507_03312_b200.vit_config import VIT_B16
 
     cfg, B = VIT_B16, args.vit_batch
-    half = as_dtype(args.vit_half)
+    # configs[2] is bf16 on one GPU, configs[3] fp16 data-parallel: auto picks by world size
+    vit_half = args.vit_half or ("bf16" if ws == 1 else "f16")
+    half = as_dtype(vit_half)
     tr = ViTTrainer(cfg, B, half=half, lr=1e-3, device=dev, group=group, world_size=ws, seed=0)
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)
@@ -229,7 +231,7 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
         "metric": "ViT-B/16 mixed-precision train images/sec", "value": round(ws * B * K / (ms * 1e-3), 1),
         "unit": "img/s", "ms_per_step": round(ms / K, 3), "steps": K, "warmup": args.vit_warmup,
         "config": {"model": "ViT-B/16 224x224 (86.6M params, cls token, 1000 classes)", "per_gpu_batch": B,
-                   "global_batch": B * ws, "half": args.vit_half, "loss_scaling": "dynamic, init 2^15",
+                   "global_batch": B * ws, "half": vit_half, "loss_scaling": "dynamic, init 2^15",
                    "optimizer": "Adam lr 1e-3 (fused K4, f32 master)", "data": "synthetic N(0,1) images",
                    "parallelism": f"dp{ws}" + (" (per-block NCCL grad all-reduce overlapped with backward)"
                                                if ws > 1 else ""),
@@ -488,7 +490,8 @@ def main():
     ap.add_argument("--vit-batch", type=int, default=256)
     ap.add_argument("--vit-steps", type=int, default=10)
     ap.add_argument("--vit-warmup", type=int, default=3)
-    ap.add_argument("--vit-half", choices=["f16", "bf16"], default="bf16")
+    ap.add_argument("--vit-half", choices=["f16", "bf16"], default=None,
+                    help="ViT section half format (default: bf16 at 1 GPU = configs[2], f16 at N > 1 = configs[3])")
     ap.add_argument("--no-graph", action="store_true", help="ViT section: eager launches instead of a CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3:
