@@ -223,17 +223,23 @@ int mpx_cross_entropy_bwd(int dtype, const void* logits, int64_t ld, const int32
  * TMEM, probabilities in shared memory — nothing N x N reaches HBM.
  * Requires hd == 64 and N <= 256 (ViT-B/16, ViT-L/16: N = 197).  row_stats
  * (nullable, f32 [B*H*ceil(N/128)*128*2]) receives each query row's softmax
- * (max, 1/sum) for mpx_attention_bwd. */
+ * (max, 1/sum) for mpx_attention_bwd; p_save (nullable, 16-byte aligned,
+ * mpx_attention_psave_bytes) receives the rounded probabilities P exactly as
+ * the P V product consumed them (the saved softmax output of the reference's
+ * autodiff), in the kernel's tile layout. */
 int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H, int hd, float scale, void* O, int64_t ldo,
-                      float* row_stats, void* stream);
+                      float* row_stats, void* p_save, void* stream);
+int64_t mpx_attention_psave_bytes(int B, int N, int H);
 /* K6 fused attention backward: given qkv and dO [B*N, H*hd], writes the whole
  * dqkv [B*N, 3*H*hd] (dQ = scale dS K, dK = scale dS^T Q, dV = P^T dO with
- * dS = P (dP - rowsum(P dP)), dP = dO V^T, P recomputed on chip — from the
- * forward's row_stats when given, else from the scores here; same P bits).
+ * dS = P (dP - rowsum(P dP)), dP = dO V^T.  P is the forward's saved tiles
+ * when p_saved is given (reloaded, no score recompute), else recomputed on chip
+ * — from the forward's row_stats when given, else from the scores here).
  * colsum_ws (f32 [B*3*H*hd]) + colsum_out (3*H*hd, dtype), both or neither:
  * colsum_out = sum over rows of the stored dqkv (the qkv bias gradient). */
 int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int B, int N, int H, int hd, float scale,
-                      void* dqkv, const float* row_stats, float* colsum_ws, void* colsum_out, void* stream);
+                      void* dqkv, const float* row_stats, const void* p_saved, float* colsum_ws, void* colsum_out,
+                      void* stream);
 /* image [B,H,W,C] -> patch rows [B*(H/P)*(W/P), P*P*C], order (py, px, c) */
 int mpx_patchify(int dtype, const void* img, void* patches, int B, int H, int W, int C, int P, void* stream);
 /* strided row copy dst[b][r][c] = src[b][r][c] */

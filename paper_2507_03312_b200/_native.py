@@ -95,9 +95,10 @@ SIGNATURES = {
     "mpx_cross_entropy_bwd": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, _P, ctypes.c_int, ctypes.c_int, _P,
                                              _P, ctypes.c_int64, _P]),
     "mpx_attention_fwd": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                         ctypes.c_float, _P, ctypes.c_int64, _P, _P]),
+                                         ctypes.c_float, _P, ctypes.c_int64, _P, _P, _P]),
+    "mpx_attention_psave_bytes": (ctypes.c_int64, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "mpx_attention_bwd": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                         ctypes.c_int, ctypes.c_float, _P, _P, _P, _P, _P]),
+                                         ctypes.c_int, ctypes.c_float, _P, _P, _P, _P, _P, _P]),
     "mpx_patchify": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_int, _P]),
     "mpx_copy_rows": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, ctypes.c_int64, _P, ctypes.c_int64,

@@ -62,6 +62,7 @@ struct AttnParams {
   void* O;
   long long ldo;  // O row stride (elements); head h at column h*hd
   float2* stats;  // optional [(b*H + h)*m_tiles*128 + row] = (row max, 1 / row sum) for the backward
+  uint8_t* psave;  // optional: each tile's P (the swizzled 64 KB smem image) for the backward
 };
 
 __device__ __forceinline__ float h2f(uint16_t h, int fmt) { return fmt ? to_f32<MPX_BF16>(h) : to_f32<MPX_F16>(h); }
@@ -426,12 +427,18 @@ __global__ void __launch_bounds__(kAttnThreadsF, 2)
       umma_commit(&bar[1]);
       mbar_wait(&bar[2], 0);
       tc_fence_after();
+      if (P.psave)  // the rounded P tile as the MMAs read it: the backward reloads it verbatim
+        bulk_store(P.psave + (size_t)tile * kAttnP, sP, kAttnP);
       const uint32_t idesc2 = idesc_f16(P.fmt, 128, 64, 0, 1);
       const uint32_t p = smem_u32(sP), v = smem_u32(sV);
       for (int s = 0; s < n_chunks; ++s)  // O = P V into TMEM cols 0-63 (S is consumed)
         umma_f16(tmem, sw128_desc(p + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
                  sw128_desc(v + s * 2048, 8192, 1024), idesc2, s > 0);
       umma_commit(&bar[3]);
+      if (P.psave) {
+        bulk_commit();
+        bulk_wait_read0();  // P read out of smem before the CTA may exit
+      }
     }
   } else if (warp >= 4) {
     const int q = warp & 3, split = (warp - 4) >> 2;
@@ -495,6 +502,7 @@ struct AttnBwdParams {
   const float2* stats;  // the forward's row statistics, or null (recomputed here)
   float* csum;          // optional per-image column sums of dqkv [B][3*H*hd] (the qkv bias gradient's partials)
   int items;            // B * H work items, walked by a persistent grid
+  const uint8_t* psaved;  // optional: the forward's P tiles (attn_fwd psave) — reloaded instead of recomputed
 };
 
 // 16 values per lane -> column sums over the warp's 32 lanes (rows) by recursive
@@ -561,14 +569,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       // persistent: items blockIdx.x, + gridDim.x, ...; the next item's K/V/Q/dO
       // are loaded as soon as this item's last MMAs have read the tiles, so
       // they land during the dQ / dV / dK readouts
+      const bool saved = P.psaved != nullptr;
+      const uint32_t qtx = 2 * kAttnQ + (saved ? kAttnP : 0);  // Q, dO (+ the saved P) per tile
       auto load_item = [&](int item) {
         const int hh = item % P.H, bb = item / P.H;
         mbar_arrive_expect_tx(&bar[0], 2 * kAttnKV);
         tma_load_4d(sK, &tmK, &bar[0], 0, 0, hh, bb);
         tma_load_4d(sV, &tmV, &bar[0], 0, 0, hh, bb);
-        mbar_arrive_expect_tx(&bar[1], 2 * kAttnQ);
+        mbar_arrive_expect_tx(&bar[1], qtx);
         tma_load_4d(sQ, &tmQ, &bar[1], 0, 0, hh, bb);
         tma_load_4d(sdO, &tmdO, &bar[1], 0, 0, hh, bb);
+        if (saved) bulk_load(sP, P.psaved + (size_t)item * T * kAttnP, kAttnP, &bar[1]);
       };
       const uint32_t q = smem_u32(sQ), dO = smem_u32(sdO), k = smem_u32(sK), v = smem_u32(sV);
       const uint32_t pp = smem_u32(sP), ds = smem_u32(sdS);
@@ -592,13 +603,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           if (it == 0) ATRACE(2 + 8 * t);
           if (gt > 0) mbar_wait(&bar[7], ph ^ 1);  // previous dQ drained from TMEM cols 0-63
           tc_fence_after();
+          if (!saved) {  // recompute P: S = Q K^T, softmax by the softmax warps
 #pragma unroll
-          for (int s = 0; s < 4; ++s)  // S = Q K^T
-            umma_f16(tmem, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), id_nk, s > 0);
-          umma_commit(&bar[2]);
-          mbar_wait(&bar[3], ph);  // P_t written (S consumed)
-          if (it == 0) ATRACE(3 + 8 * t);
-          tc_fence_after();
+            for (int s = 0; s < 4; ++s)  // S = Q K^T
+              umma_f16(tmem, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), id_nk, s > 0);
+            umma_commit(&bar[2]);
+            mbar_wait(&bar[3], ph);  // P_t written (S consumed)
+            if (it == 0) ATRACE(3 + 8 * t);
+            tc_fence_after();
+          }
 #pragma unroll
           for (int s = 0; s < 4; ++s)  // dP = dO V^T
             umma_f16(tmem, sw128_desc(dO + s * 32, 16, 1024), sw128_desc(v + s * 32, 16, 1024), id_nk, s > 0);
@@ -627,12 +640,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             umma_f16(tmem, sw128_desc(ds + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
                      sw128_desc(k + s * 2048, 8192, 1024), id_q, s > 0);
           umma_commit(&bar[6]);
-          if (t + 1 < T) {  // next tile's Q / dO as soon as this tile's MMAs have read them
-            mbar_arrive_expect_tx(&bar[1], 2 * kAttnQ);
+          if (t + 1 < T) {  // next tile's Q / dO (/ P) as soon as this tile's MMAs have read them
+            mbar_arrive_expect_tx(&bar[1], qtx);
             mbar_wait(&bar[8], ph);
             tma_load_4d(sQ, &tmQ, &bar[1], 0, (t + 1) * 128, h, b);
-            mbar_wait(&bar[9], ph);
+            mbar_wait(&bar[9], ph);  // dV done: dO and P free
             tma_load_4d(sdO, &tmdO, &bar[1], 0, (t + 1) * 128, h, b);
+            if (saved) bulk_load(sP, P.psaved + ((size_t)item * T + t + 1) * kAttnP, kAttnP, &bar[1]);
           } else if (item + (int)gridDim.x < P.items) {  // next item, once every tile has been read
             mbar_wait(&bar[6], ph);
             load_item(item + gridDim.x);
@@ -664,16 +678,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     float qsum = 0.f;  // column col16(lane) of chunk `split` of dQ, summed over this warp's rows and the tiles
     for (int t = 0; t < T; ++t, ++gt) {
       const uint32_t ph = gt & 1;
-      // ---- P = softmax(round(S * scale)) -> smem (as in the forward)
-      float2 st = make_float2(0.f, 0.f);  // the forward's (max, 1/sum), fetched while S is computed
-      if (P.stats) st = __ldg(P.stats + ((long long)item * T + t) * 128 + r);
-      mbar_wait(&bar[2], ph);
-      if (warp == 4 && lane == 0 && it == 0) ATRACE(5 + 8 * t);
-      tc_fence_after();
-      softmax_bwd_p<kSplit>(trow, split, r, qd, P.N, P.scale, P.fmt, red, sP, P.stats ? &st : nullptr);
-      fence_async_smem();
-      tc_fence_before();
-      mbar_arrive(&bar[3]);
+      if (P.psaved == nullptr) {
+        // ---- P = softmax(round(S * scale)) -> smem (as in the forward)
+        float2 st = make_float2(0.f, 0.f);  // the forward's (max, 1/sum), fetched while S is computed
+        if (P.stats) st = __ldg(P.stats + ((long long)item * T + t) * 128 + r);
+        mbar_wait(&bar[2], ph);
+        if (warp == 4 && lane == 0 && it == 0) ATRACE(5 + 8 * t);
+        tc_fence_after();
+        softmax_bwd_p<kSplit>(trow, split, r, qd, P.N, P.scale, P.fmt, red, sP, P.stats ? &st : nullptr);
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(&bar[3]);
+      } else {
+        mbar_wait(&bar[1], ph);  // the forward's P tile has landed (TMA) before it is read here
+      }
       // ---- dS = P * (dP - sum(P * dP)) -> smem; dP rounded to the half
       // format first (the reference's dP is a half GEMM output), kept packed
       mbar_wait(&bar[4], ph);
@@ -791,10 +809,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
     }
     if (P.csum) {
-      // combine the warps' partials through the (now idle) P tile — the next
-      // item's Q may already be landing in the Q tile: slots
+      // combine the warps' partials through the (now idle) dS tile — the next
+      // item's Q / P may already be landing: slots
       // [part q/k/v][quarter (and key half)][64 columns], then one fixed-order sum
-      float* sc = reinterpret_cast<float*>(sP);
+      float* sc = reinterpret_cast<float*>(sdS);
       if ((lane & 1) == 0) {
         sc[(0 * 8 + qd) * 64 + split * 16 + col16(lane)] = qsum;
 #pragma unroll
@@ -871,7 +889,7 @@ extern "C" int mpx_debug_attn_trace(long long* host_out) {  // kTraceCtas * kTra
 #endif
 
 extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H, int hd, float scale, void* O,
-                                 int64_t ldo, float* row_stats, void* stream) {
+                                 int64_t ldo, float* row_stats, void* p_save, void* stream) {
   if (dtype != MPX_F16 && dtype != MPX_BF16) return fail(MPX_EINVAL, "attention: f16/bf16 only");
   if (hd != 64 || N < 1 || N > 256) return fail(MPX_EINVAL, "attention_fwd: fused path needs hd == 64, N <= 256");
   const int fmt = dtype == MPX_BF16 ? 1 : 0;
@@ -892,6 +910,8 @@ extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H
   P.O = O;
   P.ldo = ldo;
   P.stats = reinterpret_cast<float2*>(row_stats);
+  P.psave = static_cast<uint8_t*>(p_save);
+  if (p_save && (reinterpret_cast<uintptr_t>(p_save) & 15)) return fail(MPX_EINVAL, "attention_fwd: p_save not 16-byte aligned");
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
@@ -904,9 +924,13 @@ extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H
   return 0;
 }
 
+extern "C" int64_t mpx_attention_psave_bytes(int B, int N, int H) {
+  return (int64_t)B * H * ((N + 127) / 128) * kAttnP;
+}
+
 extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int B, int N, int H, int hd, float scale,
-                                 void* dqkv, const float* row_stats, float* colsum_ws, void* colsum_out,
-                                 void* stream) {
+                                 void* dqkv, const float* row_stats, const void* p_saved, float* colsum_ws,
+                                 void* colsum_out, void* stream) {
   if (dtype != MPX_F16 && dtype != MPX_BF16) return fail(MPX_EINVAL, "attention: f16/bf16 only");
   if (hd != 64 || N < 1 || N > 256) return fail(MPX_EINVAL, "attention_bwd: fused path needs hd == 64, N <= 256");
   const int fmt = dtype == MPX_BF16 ? 1 : 0;
@@ -928,6 +952,8 @@ extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int
   P.dqkv = dqkv;
   P.ld = 3LL * D;
   P.stats = reinterpret_cast<const float2*>(row_stats);
+  P.psaved = static_cast<const uint8_t*>(p_saved);
+  if (p_saved && (reinterpret_cast<uintptr_t>(p_saved) & 15)) return fail(MPX_EINVAL, "attention_bwd: p_saved not 16-byte aligned");
   if ((colsum_ws == nullptr) != (colsum_out == nullptr))
     return fail(MPX_EINVAL, "attention_bwd: colsum_ws and colsum_out go together");
   P.csum = colsum_ws;

@@ -71,9 +71,10 @@ class ViTEngine:
         if not self.fused_attn:
             self.Sm = [e(B * H * S, self.ldS) for _ in range(c.depth)]  # scaled scores
             self.P = [e(B * H * S, self.ldS) for _ in range(c.depth)]
-        else:  # per-row softmax statistics saved by the forward for the backward
-            self.attn_stats = [torch.empty(VK.attention_stats_numel(B, S, H), dtype=torch.float32, device=self.dev)
-                               for _ in range(c.depth)]
+        else:  # the forward's probabilities, saved for the backward (as the reference's autodiff saves
+            # the softmax output): the backward reloads P instead of recomputing scores and softmax
+            self.attn_p = [torch.empty(VK.attention_psave_bytes(B, S, H), dtype=torch.uint8, device=self.dev)
+                           for _ in range(c.depth)]
         self.O = [e(M, D) for _ in range(c.depth)]
         self.xm = [e(M, D) for _ in range(c.depth)]  # after attention residual
         self.bn = [e(M, D) for _ in range(c.depth)]  # LN2 out
@@ -171,7 +172,7 @@ class ViTEngine:
             VK.linear_fwd(a, p[q + "qkv.w"], bias=p[q + "qkv.b"], out=qkv)
             O = self.O[i]
             if self.fused_attn:
-                VK.attention_fwd(qkv, B, S, H, hd, scale, out=O, stats=self.attn_stats[i])
+                VK.attention_fwd(qkv, B, S, H, hd, scale, out=O, p_save=self.attn_p[i])
             else:
                 Sm, P_ = self.Sm[i], self.P[i]
                 VK.gemm(qkv, qkv[:, D:], M=S, N=S, K=hd, lda=3 * D, ldb=3 * D, nb=(H, B), a_sb=(hd, S * 3 * D),
@@ -280,7 +281,7 @@ class ViTEngine:
             # attention
             qkv, dqkv = self.qkv[i], self.dqkv
             if self.fused_attn:  # (the qkv.b gradient, colsum(dqkv), comes out of the kernel)
-                VK.attention_bwd(qkv, self.dO, B, S, H, hd, scale, dqkv=dqkv, stats=self.attn_stats[i],
+                VK.attention_bwd(qkv, self.dO, B, S, H, hd, scale, dqkv=dqkv, p_saved=self.attn_p[i],
                                  colsum_out=g[q + "qkv.b"], colsum_ws=self.ws)
             else:
                 self._attention_bwd_unfused(i, qkv, dqkv, scale)

@@ -140,23 +140,32 @@ def attention_stats_numel(B: int, N: int, H: int) -> int:
     return B * H * ((N + 127) // 128) * 128 * 2
 
 
-def attention_fwd(qkv, B: int, N: int, H: int, hd: int, scale: float, out=None, stats=None):
+def attention_psave_bytes(B: int, N: int, H: int) -> int:
+    """Bytes of the forward's saved P tiles (mpx_attention_psave_bytes)."""
+    return B * H * ((N + 127) // 128) * 65536
+
+
+def attention_fwd(qkv, B: int, N: int, H: int, hd: int, scale: float, out=None, stats=None, p_save=None):
     """Fused softmax(Q K^T * scale) V from qkv [B*N, 3*H*hd] into out [B*N, H*hd];
-    `stats` (f32, attention_stats_numel) receives the row statistics for the backward."""
+    `stats` (f32, attention_stats_numel) receives the row statistics, `p_save`
+    (uint8, attention_psave_bytes) the probabilities, for the backward."""
     require_cuda([qkv], "attention_fwd")
     D = H * hd
     if out is None:
         out = torch.empty(B * N, D, dtype=qkv.dtype, device=qkv.device)
     if stats is not None:
         assert stats.dtype == torch.float32 and stats.numel() >= attention_stats_numel(B, N, H)
+    if p_save is not None:
+        assert p_save.dtype == torch.uint8 and p_save.numel() >= attention_psave_bytes(B, N, H)
     _nat.check(_nat.load().mpx_attention_fwd(_CODE[qkv.dtype], qkv.data_ptr(), B, N, H, hd, scale, out.data_ptr(),
                                              out.stride(0), stats.data_ptr() if stats is not None else None,
+                                             p_save.data_ptr() if p_save is not None else None,
                                              stream_handle(qkv.device)), "mpx_attention_fwd")
     return out
 
 
 def attention_bwd(qkv, dO, B: int, N: int, H: int, hd: int, scale: float, dqkv=None, stats=None,
-                  colsum_out=None, colsum_ws=None):
+                  colsum_out=None, colsum_ws=None, p_saved=None):
     """Fused attention backward: the whole dqkv [B*N, 3*H*hd] from qkv and dO
     (with the forward's `stats`, P is rebuilt without the statistics passes);
     colsum_out [3*H*hd] receives sum over rows of dqkv (the qkv bias gradient)."""
@@ -169,8 +178,11 @@ def attention_bwd(qkv, dO, B: int, N: int, H: int, hd: int, scale: float, dqkv=N
         colsum_ws = torch.empty(B * 3 * H * hd, dtype=torch.float32, device=qkv.device)
     if colsum_ws is not None:
         assert colsum_ws.dtype == torch.float32 and colsum_ws.numel() >= B * 3 * H * hd
+    if p_saved is not None:
+        assert p_saved.dtype == torch.uint8 and p_saved.numel() >= attention_psave_bytes(B, N, H)
     _nat.check(_nat.load().mpx_attention_bwd(_CODE[qkv.dtype], qkv.data_ptr(), dO.data_ptr(), B, N, H, hd, scale,
                                              dqkv.data_ptr(), stats.data_ptr() if stats is not None else None,
+                                             p_saved.data_ptr() if p_saved is not None else None,
                                              colsum_ws.data_ptr() if colsum_out is not None else None,
                                              colsum_out.data_ptr() if colsum_out is not None else None,
                                              stream_handle(qkv.device)), "mpx_attention_bwd")

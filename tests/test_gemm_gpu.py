@@ -130,15 +130,22 @@ def test_fused_attention_backward(cuda, dt, Nt):
     assert torch.equal(VK.attention_bwd(qkv, dO, Bsz, Nt, H, hd, 0.125, stats=stats, colsum_out=cs), dqkv)
     want = dqkv.float().sum(0)
     assert torch.allclose(cs.float(), want, rtol=1e-2, atol=1e-2 * want.abs().max().item())
+    # the forward's saved P reloaded instead of recomputed (the engine's path)
+    psave = torch.empty(VK.attention_psave_bytes(Bsz, Nt, H), dtype=torch.uint8, device=cuda)
+    VK.attention_fwd(qkv, Bsz, Nt, H, hd, 0.125, p_save=psave)
+    cs2 = torch.empty(3 * D, device=cuda, dtype=dt)
+    dqkv_saved = VK.attention_bwd(qkv, dO, Bsz, Nt, H, hd, 0.125, p_saved=psave, colsum_out=cs2)
+    want2 = dqkv_saved.float().sum(0)
+    assert torch.allclose(cs2.float(), want2, rtol=1e-2, atol=1e-2 * want2.abs().max().item())
     x = qkv.float().requires_grad_(True)
     q, k, v = (x.view(Bsz, Nt, 3, H, hd)[:, :, i] for i in range(3))
     p = torch.softmax(torch.einsum("bnhd,bmhd->bhnm", q, k) * 0.125, -1)
     o = torch.einsum("bhnm,bmhd->bnhd", p, v).reshape(Bsz * Nt, D)
     o.backward(dO.float())
     for i, name in enumerate("qkv"):
-        got = dqkv[:, i * D:(i + 1) * D]
         want = x.grad[:, i * D:(i + 1) * D]
-        close(got, want, rel=3e-2)
+        close(dqkv[:, i * D:(i + 1) * D], want, rel=3e-2)
+        close(dqkv_saved[:, i * D:(i + 1) * D], want, rel=3e-2)
 
 
 @pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
