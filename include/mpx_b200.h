@@ -226,7 +226,7 @@ int mpx_cross_entropy_bwd(int dtype, const void* logits, int64_t ld, const int32
  * (max, 1/sum) for mpx_attention_bwd; p_save (nullable, 16-byte aligned,
  * mpx_attention_psave_bytes) receives the rounded probabilities P exactly as
  * the P V product consumed them (the saved softmax output of the reference's
- * autodiff), in the kernel's tile layout. */
+ * autodiff), as [B*H][N][16*ceil(N/16)] half. */
 int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H, int hd, float scale, void* O, int64_t ldo,
                       float* row_stats, void* p_save, void* stream);
 int64_t mpx_attention_psave_bytes(int B, int N, int H);

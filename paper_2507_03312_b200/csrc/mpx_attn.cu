@@ -62,7 +62,7 @@ struct AttnParams {
   void* O;
   long long ldo;  // O row stride (elements); head h at column h*hd
   float2* stats;  // optional [(b*H + h)*m_tiles*128 + row] = (row max, 1 / row sum) for the backward
-  uint8_t* psave;  // optional: each tile's P (the swizzled 64 KB smem image) for the backward
+  uint8_t* psave;  // optional: P (rounded, as the P V MMA read it) to [B*H][N][16 ceil(N/16)] for the backward
 };
 
 __device__ __forceinline__ float h2f(uint16_t h, int fmt) { return fmt ? to_f32<MPX_BF16>(h) : to_f32<MPX_F16>(h); }
@@ -373,7 +373,8 @@ __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, i
 
 __global__ void __launch_bounds__(kAttnThreadsF, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ AttnParams P) {
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmP,
+                    const __grid_constant__ AttnParams P) {
   extern __shared__ uint8_t smem_raw[];
   // 1 KB-aligned by indexing the __shared__ array (not via an integer cast), so
   // derived pointers stay in the shared window: STS/LDS, 32-bit addressing
@@ -427,8 +428,9 @@ __global__ void __launch_bounds__(kAttnThreadsF, 2)
       umma_commit(&bar[1]);
       mbar_wait(&bar[2], 0);
       tc_fence_after();
-      if (P.psave)  // the rounded P tile as the MMAs read it: the backward reloads it verbatim
-        bulk_store(P.psave + (size_t)tile * kAttnP, sP, kAttnP);
+      if (P.psave) {  // the rounded P tile as the MMAs read it (rows < N, keys < 16 n_chunks)
+        for (int blk = 0; blk * 4 < n_chunks; ++blk) tma_store_4d(&tmP, sP + blk * 16384, blk * 64, m0, bh, 0);
+      }
       const uint32_t idesc2 = idesc_f16(P.fmt, 128, 64, 0, 1);
       const uint32_t p = smem_u32(sP), v = smem_u32(sV);
       for (int s = 0; s < n_chunks; ++s)  // O = P V into TMEM cols 0-63 (S is consumed)
@@ -527,7 +529,7 @@ __device__ __forceinline__ int col16(int lane) {
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                    const __grid_constant__ AttnBwdParams P) {
+                    const __grid_constant__ CUtensorMap tmP, const __grid_constant__ AttnBwdParams P) {
   extern __shared__ uint8_t smem_raw[];
   // 1 KB-aligned by indexing the __shared__ array (not via an integer cast), so
   // derived pointers stay in the shared window: STS/LDS, 32-bit addressing
@@ -570,7 +572,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       // are loaded as soon as this item's last MMAs have read the tiles, so
       // they land during the dQ / dV / dK readouts
       const bool saved = P.psaved != nullptr;
-      const uint32_t qtx = 2 * kAttnQ + (saved ? kAttnP : 0);  // Q, dO (+ the saved P) per tile
+      const int n_pblk = ((P.N + 15) / 16 + 3) / 4;  // 64-key blocks of the saved P
+      const uint32_t qtx = 2 * kAttnQ + (saved ? n_pblk * 16384 : 0);  // Q, dO (+ the saved P) per tile
+      auto load_p = [&](int item, int t) {
+        for (int blk = 0; blk < n_pblk; ++blk)
+          tma_load_4d(sP + blk * 16384, &tmP, &bar[1], blk * 64, t * 128, item, 0);
+      };
       auto load_item = [&](int item) {
         const int hh = item % P.H, bb = item / P.H;
         mbar_arrive_expect_tx(&bar[0], 2 * kAttnKV);
@@ -579,7 +586,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mbar_arrive_expect_tx(&bar[1], qtx);
         tma_load_4d(sQ, &tmQ, &bar[1], 0, 0, hh, bb);
         tma_load_4d(sdO, &tmdO, &bar[1], 0, 0, hh, bb);
-        if (saved) bulk_load(sP, P.psaved + (size_t)item * T * kAttnP, kAttnP, &bar[1]);
+        if (saved) load_p(item, 0);
       };
       const uint32_t q = smem_u32(sQ), dO = smem_u32(sdO), k = smem_u32(sK), v = smem_u32(sV);
       const uint32_t pp = smem_u32(sP), ds = smem_u32(sdS);
@@ -646,7 +653,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             tma_load_4d(sQ, &tmQ, &bar[1], 0, (t + 1) * 128, h, b);
             mbar_wait(&bar[9], ph);  // dV done: dO and P free
             tma_load_4d(sdO, &tmdO, &bar[1], 0, (t + 1) * 128, h, b);
-            if (saved) bulk_load(sP, P.psaved + ((size_t)item * T + t + 1) * kAttnP, kAttnP, &bar[1]);
+            if (saved) load_p(item, t + 1);
           } else if (item + (int)gridDim.x < P.items) {  // next item, once every tile has been read
             mbar_wait(&bar[6], ph);
             load_item(item + gridDim.x);
@@ -877,6 +884,23 @@ static int qkv_map(CUtensorMap* m, const void* base, int fmt, int N, int H, int 
   return 0;
 }
 
+// map over the saved probabilities: [B*H][N rows][16*ceil(N/16) keys] half,
+// boxes of 64 keys x 128 rows, 128B-swizzled = exactly the smem P tile's blocks
+static int p_map(CUtensorMap* m, const void* base, int fmt, int N, int BH) {
+  auto fn = attn_encode_fn();
+  if (!fn) return fail(MPX_EINVAL, "cuTensorMapEncodeTiled unavailable");
+  const uint64_t keys = 16ull * ((N + 15) / 16);
+  cuuint64_t dims[4] = {(cuuint64_t)keys, (cuuint64_t)N, (cuuint64_t)BH, 1};
+  cuuint64_t strides[3] = {keys * 2, keys * 2 * N, keys * 2 * N * BH};
+  cuuint32_t box[4] = {64, 128, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, fmt ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+                  const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MPX_EINVAL, "attention P tensor map failed (" + std::to_string((int)r) + ")");
+  return 0;
+}
+
 }  // namespace mpx
 
 using namespace mpx;
@@ -899,6 +923,8 @@ extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H
   int rc = qkv_map(&tq, base, fmt, N, H, hd, B, 128);
   if (!rc) rc = qkv_map(&tk, base + D, fmt, N, H, hd, B, 256);
   if (!rc) rc = qkv_map(&tv, base + 2 * D, fmt, N, H, hd, B, 256);
+  CUtensorMap tp = tv;
+  if (!rc && p_save) rc = p_map(&tp, p_save, fmt, N, B * H);
   if (rc) return rc;
   AttnParams P{};
   P.N = N;
@@ -911,7 +937,6 @@ extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H
   P.ldo = ldo;
   P.stats = reinterpret_cast<float2*>(row_stats);
   P.psave = static_cast<uint8_t*>(p_save);
-  if (p_save && (reinterpret_cast<uintptr_t>(p_save) & 15)) return fail(MPX_EINVAL, "attention_fwd: p_save not 16-byte aligned");
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
@@ -919,13 +944,13 @@ extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H
   });
   if (err != cudaSuccess) return fail((int)err, "cudaFuncSetAttribute(attn_fwd_kernel)");
   const long long grid = (long long)B * H * P.m_tiles;
-  MPX_CUDA_CHECK(::mpx::launch_k(attn_fwd_kernel, (unsigned)grid, kAttnThreadsF, kAttnSmem, static_cast<cudaStream_t>(stream), tq, tk, tv, P));
+  MPX_CUDA_CHECK(::mpx::launch_k(attn_fwd_kernel, (unsigned)grid, kAttnThreadsF, kAttnSmem, static_cast<cudaStream_t>(stream), tq, tk, tv, tp, P));
   MPX_LAUNCH_CHECK("attn_fwd_kernel");
   return 0;
 }
 
 extern "C" int64_t mpx_attention_psave_bytes(int B, int N, int H) {
-  return (int64_t)B * H * ((N + 127) / 128) * kAttnP;
+  return (int64_t)B * H * N * (16 * ((N + 15) / 16)) * 2;  // [B*H][N][16 ceil(N/16)] half
 }
 
 extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int B, int N, int H, int hd, float scale,
@@ -941,6 +966,8 @@ extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int
   if (!rc) rc = qkv_map(&tk, base + D, fmt, N, H, hd, B, 256);
   if (!rc) rc = qkv_map(&tv, base + 2 * D, fmt, N, H, hd, B, 256);
   if (!rc) rc = qkv_map(&tdo, dO, fmt, N, H, hd, B, 128, 1);
+  CUtensorMap tp = tv;
+  if (!rc && p_saved) rc = p_map(&tp, p_saved, fmt, N, B * H);
   if (rc) return rc;
   AttnBwdParams P{};
   P.N = N;
@@ -953,7 +980,6 @@ extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int
   P.ld = 3LL * D;
   P.stats = reinterpret_cast<const float2*>(row_stats);
   P.psaved = static_cast<const uint8_t*>(p_saved);
-  if (p_saved && (reinterpret_cast<uintptr_t>(p_saved) & 15)) return fail(MPX_EINVAL, "attention_bwd: p_saved not 16-byte aligned");
   if ((colsum_ws == nullptr) != (colsum_out == nullptr))
     return fail(MPX_EINVAL, "attention_bwd: colsum_ws and colsum_out go together");
   P.csum = colsum_ws;
@@ -966,7 +992,7 @@ extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int
   P.items = B * H;  // persistent: one CTA per SM walks the (image, head) items
   const unsigned grid = (unsigned)std::min(B * H, current_num_sms());
   MPX_CUDA_CHECK(::mpx::launch_k(attn_bwd_kernel, grid, kAttnThreads, kAttnBwdSmem, static_cast<cudaStream_t>(stream),
-                                 tq, tk, tv, tdo, P));
+                                 tq, tk, tv, tdo, tp, P));
   MPX_LAUNCH_CHECK("attn_bwd_kernel");
   if (colsum_out) {  // the qkv bias gradient: sum the per-image partials [B][3D]
     const int cols = 3 * D;

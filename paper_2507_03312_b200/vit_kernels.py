@@ -141,8 +141,8 @@ def attention_stats_numel(B: int, N: int, H: int) -> int:
 
 
 def attention_psave_bytes(B: int, N: int, H: int) -> int:
-    """Bytes of the forward's saved P tiles (mpx_attention_psave_bytes)."""
-    return B * H * ((N + 127) // 128) * 65536
+    """Bytes of the forward's saved P ([B*H][N][16 ceil(N/16)] half, mpx_attention_psave_bytes)."""
+    return B * H * N * (16 * -(-N // 16)) * 2
 
 
 def attention_fwd(qkv, B: int, N: int, H: int, hd: int, scale: float, out=None, stats=None, p_save=None):
