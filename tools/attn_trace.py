@@ -19,17 +19,17 @@ from paper_2507_03312_b200 import vit_kernels as VK  # noqa: E402
 B, S, H, hd = 256, 197, 12, 64
 qkv = torch.randn(B * S, 3 * H * hd, device="cuda").to(torch.bfloat16)
 dO = torch.randn(B * S, H * hd, device="cuda").to(torch.bfloat16)
-st = torch.empty(VK.attention_stats_numel(B, S, H), device="cuda")
+ps = torch.empty(VK.attention_psave_bytes(B, S, H), dtype=torch.uint8, device="cuda")
 for _ in range(3):
-    VK.attention_fwd(qkv, B, S, H, hd, 0.125, stats=st)
-    VK.attention_bwd(qkv, dO, B, S, H, hd, 0.125, stats=st)
+    VK.attention_fwd(qkv, B, S, H, hd, 0.125, p_save=ps)
+    VK.attention_bwd(qkv, dO, B, S, H, hd, 0.125, p_saved=ps)
 torch.cuda.synchronize()
 lib = _native.load()
 buf = (ctypes.c_longlong * (64 * 32))()
 assert lib.mpx_debug_attn_trace(buf) == 0
 a = np.frombuffer(buf, dtype=np.int64).reshape(64, 32).astype(np.float64)
 a = a - a[:, :1]
-names = {0: "mma: loads issued", 1: "mma: K,V landed", 30: "end"}
+names = {0: "mma: item start (last item)", 1: "mma: K,V landed (last item)", 30: "end"}
 for t in range(2):
     names.update({2 + 8 * t: f"t{t} mma: Q,dO landed", 3 + 8 * t: f"t{t} mma: P ready", 4 + 8 * t: f"t{t} mma: dS ready",
                   5 + 8 * t: f"t{t} smx: S ready", 6 + 8 * t: f"t{t} smx: dP ready", 7 + 8 * t: f"t{t} smx: dQ ready",
