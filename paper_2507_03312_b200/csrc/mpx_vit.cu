@@ -244,16 +244,16 @@ __global__ void __launch_bounds__(128) ln_bwd_fused_kernel(const void* __restric
                                                            float* __restrict__ ws, int rows, int D, int nsum,
                                                            int fmt) {
   ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
-  extern __shared__ float acc_sh[];  // [4 warps][3][V][8][32]
+  extern __shared__ float acc_sh[];  // [4 warps][3 sums][V][4 column pairs][32 lanes] float2
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float* acc = acc_sh + warp * (3 * V * 256);
-  auto A = [&](int k, int j, int e) -> float& { return acc[((k * V + j) * 8 + e) * 32 + lane]; };
+  float2* acc = reinterpret_cast<float2*>(acc_sh) + warp * (3 * V * 128);
+  auto A = [&](int k, int j, int e2) -> float2& { return acc[((k * V + j) * 4 + e2) * 32 + lane]; };
 #pragma unroll
   for (int k = 0; k < 3; ++k)
 #pragma unroll
     for (int j = 0; j < V; ++j)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) A(k, j, e) = 0.f;
+      for (int e2 = 0; e2 < 4; ++e2) A(k, j, e2) = make_float2(0.f, 0.f);
   const long long stride = (long long)gridDim.x * 4;
   long long row = (long long)blockIdx.x * 4 + warp;
   uint4 nx[V], nd[V], nr[V];  // the next row's words, in flight
@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(128) ln_bwd_fused_kernel(const void* __restric
       if (dres) nr[j] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dres) + rr * ldres + c0));
     }
   };
+  auto f2v = [](float a) { return make_float2(a, a); };
   if (row < rows) load(row);
   for (; row < rows; row += stride) {
     uint4 wx[V], wd[V], wr[V];
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(128) ln_bwd_fused_kernel(const void* __restric
     }
     if (row + stride < rows) load(row + stride);  // next row's bytes in flight during this row's work
     const float mu = mean[row], rs = rstd[row];
-    float s1 = 0.f, s2 = 0.f;
+    float2 s1 = f2v(0.f), s2 = f2v(0.f);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const int c0 = (j * 32 + lane) * 8;
@@ -286,17 +287,18 @@ __global__ void __launch_bounds__(128) ln_bwd_fused_kernel(const void* __restric
       unpack8(wd[j], dv, fmt);
       unpack8(__ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g) + c0)), gg, fmt);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float xh = (xv[e] - mu) * rs;
-        const float dg = dv[e] * gg[e];
-        s1 += dg;
-        s2 += dg * xh;
-        A(0, j, e) += dv[e] * xh;
-        A(1, j, e) += dv[e];
+      for (int e2 = 0; e2 < 4; ++e2) {
+        const float2 xx = make_float2(xv[2 * e2], xv[2 * e2 + 1]), d2 = make_float2(dv[2 * e2], dv[2 * e2 + 1]);
+        const float2 xh = __fmul2_rn(__fadd2_rn(xx, f2v(-mu)), f2v(rs));
+        const float2 dg = __fmul2_rn(d2, make_float2(gg[2 * e2], gg[2 * e2 + 1]));
+        s1 = __fadd2_rn(s1, dg);
+        s2 = __ffma2_rn(dg, xh, s2);
+        A(0, j, e2) = __ffma2_rn(d2, xh, A(0, j, e2));
+        A(1, j, e2) = __fadd2_rn(A(1, j, e2), d2);
       }
     }
-    s1 = warp_sum(s1) / (float)D;
-    s2 = warp_sum(s2) / (float)D;
+    const float m1 = warp_sum(s1.x + s1.y) / (float)D;
+    const float m2 = warp_sum(s2.x + s2.y) / (float)D;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const int c0 = (j * 32 + lane) * 8;
@@ -305,25 +307,35 @@ __global__ void __launch_bounds__(128) ln_bwd_fused_kernel(const void* __restric
       unpack8(wd[j], dv, fmt);
       unpack8(__ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g) + c0)), gg, fmt);
       if (dres) unpack8(wr[j], rv, fmt);
+      // o = rs (dy g - m1 - xhat m2) + dres = a (dy g) + (c x + b) + dres, packed by column pairs
+      const float a = rs, c = -rs * rs * m2, bb = -rs * m1 + rs * rs * m2 * mu;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] = rs * (dv[e] * gg[e] - s1 - (xv[e] - mu) * rs * s2) + (dres ? rv[e] : 0.f);
+      for (int e2 = 0; e2 < 4; ++e2) {
+        const float2 t1 = __fmul2_rn(make_float2(dv[2 * e2], dv[2 * e2 + 1]), make_float2(gg[2 * e2], gg[2 * e2 + 1]));
+        const float2 t2 = __ffma2_rn(f2v(c), make_float2(xv[2 * e2], xv[2 * e2 + 1]), f2v(bb));
+        float2 r2 = __ffma2_rn(f2v(a), t1, t2);
+        if (dres) r2 = __fadd2_rn(r2, make_float2(rv[2 * e2], rv[2 * e2 + 1]));
+        o[2 * e2] = r2.x;
+        o[2 * e2 + 1] = r2.y;
+      }
       const uint4 w = pack8(o, fmt);
       *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dx) + row * lddx + c0) = w;
       if (nsum == 3) {
         float ov[8];
         unpack8(w, ov, fmt);  // the column sum of the stored dx
 #pragma unroll
-        for (int e = 0; e < 8; ++e) A(2, j, e) += ov[e];
+        for (int e2 = 0; e2 < 4; ++e2) A(2, j, e2) = __fadd2_rn(A(2, j, e2), make_float2(ov[2 * e2], ov[2 * e2 + 1]));
       }
     }
   }
   __syncthreads();
   // combine the 4 warps' slabs in a fixed order, one partial row per block
+  const float* accf = acc_sh;
   for (int c = threadIdx.x; c < D; c += blockDim.x) {
     const int j = c / 256, l = (c / 8) % 32, e = c % 8;
     for (int k = 0; k < nsum; ++k) {
       float t = 0.f;
-      for (int w = 0; w < 4; ++w) t += acc_sh[w * (3 * V * 256) + ((k * V + j) * 8 + e) * 32 + l];
+      for (int w = 0; w < 4; ++w) t += accf[(w * (3 * V * 128) + ((k * V + j) * 4 + e / 2) * 32 + l) * 2 + (e & 1)];
       ws[((long long)k * gridDim.x + blockIdx.x) * D + c] = t;
     }
   }
