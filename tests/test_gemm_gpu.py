@@ -98,7 +98,7 @@ def test_batched_strided_attention_shapes(cuda):
 
 
 @pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
-@pytest.mark.parametrize("Nt", [197, 64, 130])
+@pytest.mark.parametrize("Nt", [197, 64, 130, 256, 17])
 def test_fused_attention_forward(cuda, dt, Nt):
     Bsz, H, hd = 3, 4, 64
     D = H * hd
@@ -113,7 +113,7 @@ def test_fused_attention_forward(cuda, dt, Nt):
 
 
 @pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
-@pytest.mark.parametrize("Nt", [197, 64, 130])
+@pytest.mark.parametrize("Nt", [197, 64, 130, 256, 17])
 def test_fused_attention_backward(cuda, dt, Nt):
     Bsz, H, hd = 2, 3, 64
     D = H * hd
