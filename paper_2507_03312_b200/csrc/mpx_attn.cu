@@ -448,8 +448,13 @@ __global__ void __launch_bounds__(kAttnThreadsF, 2)
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     mbar_wait(&bar[1], 0);
     tc_fence_after();
-    float2* st = P.stats ? P.stats + ((long long)bh * P.m_tiles + mt) * 128 + r : nullptr;
-    softmax_fwd_p<kSplitF>(trow, split, r, q, P.N, P.scale, P.fmt, red, sP, st);
+    // a lane quarter whose 32 query rows are all padding (rows >= N of the last
+    // tile) skips the softmax: its P rows stay whatever finite bytes the tile
+    // held, feed only O rows that are never stored, and are clipped from the saved P
+    if (m0 + q * 32 < P.N) {
+      float2* st = P.stats ? P.stats + ((long long)bh * P.m_tiles + mt) * 128 + r : nullptr;
+      softmax_fwd_p<kSplitF>(trow, split, r, q, P.N, P.scale, P.fmt, red, sP, st);
+    }
     fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
     tc_fence_before();
     mbar_arrive(&bar[2]);
@@ -457,7 +462,7 @@ __global__ void __launch_bounds__(kAttnThreadsF, 2)
     tc_fence_after();
     const int qrow = m0 + r;
     uint16_t* o = static_cast<uint16_t*>(P.O) + ((long long)b * P.N + qrow) * P.ldo + (long long)h * P.hd;
-    for (int c = split; c < 4; c += kSplitF) {
+    for (int c = split; c < 4 && m0 + q * 32 < P.N; c += kSplitF) {
       uint32_t a[16];
       tmem_ld16(trow + c * 16, a);
       tmem_ld_wait();
