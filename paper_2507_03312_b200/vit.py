@@ -115,6 +115,16 @@ class ViTEngine:
         self.lib = _nat.load()
 
     # ------------------------------------------------------------------
+    def activation_bytes(self) -> int:
+        """Bytes of the activations the forward keeps for the backward (the
+        reference tape's activation_bytes, autodiff.py:43) — in their physical
+        formats: half activations 2 B, f32 LayerNorm statistics 4 B."""
+        kept = [self.patches, self.fin, self.muf, self.rsf, self.pooled, self.logits]
+        for name in ("x", "a", "qkv", "O", "xm", "bn", "pre", "h", "mu1", "rs1", "mu2", "rs2"):
+            kept += list(getattr(self, name))
+        kept += list(getattr(self, "attn_p", []) or []) + list(getattr(self, "P", []) or [])
+        return int(sum(t.numel() * t.element_size() for t in kept))
+
     def _st(self):
         return stream_handle(self.dev)
 

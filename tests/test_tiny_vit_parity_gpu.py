@@ -78,3 +78,36 @@ def test_tiny_vit_trajectory_matches_reference(cuda, log2, variant):
     ok = np.isfinite(loss) & np.isfinite(ref_loss)
     rel = np.abs(loss[ok] - ref_loss[ok]) / np.abs(ref_loss[ok])
     assert rel[0] <= 1e-2 and rel.max() <= 3e-2, (loss.tolist(), ref_loss.tolist())
+
+
+def test_run_record_replays(cuda, tmp_path):
+    """A GPU run written as a reference-format run record
+    replays: scale column = the state machine on its own flags, skipped steps
+    leave the parameter checksum unchanged (init scale 2^32 forces skips)."""
+    import time
+
+    from paper_2507_03312_b200 import runrecord as RR
+    from paper_2507_03312_b200.vit import ViTEngine
+
+    g = np.load(GOLD / "tiny_vit_s32.npz")
+    params = {k[5:]: torch.from_numpy(g[k]).to(cuda) for k in g.files if k.startswith("init.")}
+    opt = mpx.adam_init(params, 1e-3)
+    scaling = mpx.LossScaling(2.0 ** 32)
+    f = vit_loss(VIT_TINY)
+    recs, init_sum = [], RR.param_checksum(params)
+    for step in range(8):
+        t0 = time.perf_counter()
+        x, y = batch(step)
+        res = mpx.filter_value_and_grad(f, scaling)(
+            params, {"x": torch.from_numpy(x).to(cuda), "y": torch.from_numpy(y).to(cuda)})
+        params, opt = mpx.optimizer_update(params, opt, res.grads, res.grads_finite)
+        recs.append(RR.StepRecord(step, float(res.value.item()), scaling.loss_scale, bool(res.grads_finite), 0,
+                                  time.perf_counter() - t0, RR.param_checksum(params)))
+        scaling = res.scaling
+    path = tmp_path / "run.csv"
+    RR.write_csv(recs, str(path), debug_checksums=True)
+    back = RR.read_csv(str(path))
+    rep = RR.replay(back, init_scale=2.0 ** 32, init_checksum=init_sum)
+    assert rep.ok and rep.skipped >= 1, rep
+    eng = ViTEngine(VIT_TINY, 64, mpx.as_dtype(torch.float16), cuda)
+    assert eng.activation_bytes() > 0
