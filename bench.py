@@ -154,7 +154,8 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
     # configs[2] is bf16 on one GPU, configs[3] fp16 data-parallel: auto picks by world size
     vit_half = args.vit_half or ("bf16" if ws == 1 else "f16")
     half = as_dtype(vit_half)
-    tr = ViTTrainer(cfg, B, half=half, lr=1e-3, device=dev, group=group, world_size=ws, seed=0)
+    tr = ViTTrainer(cfg, B, half=half, lr=1e-3, device=dev, group=group, world_size=ws, seed=0,
+                    zero=args.zero and ws > 1)
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)
     images = torch.randn(B, cfg.img, cfg.img, cfg.chans, generator=g, device=dev)
@@ -233,7 +234,9 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
         "config": {"model": "ViT-B/16 224x224 (86.6M params, cls token, 1000 classes)", "per_gpu_batch": B,
                    "global_batch": B * ws, "half": vit_half, "loss_scaling": "dynamic, init 2^15",
                    "optimizer": "Adam lr 1e-3 (fused K4, f32 master)", "data": "synthetic N(0,1) images",
-                   "parallelism": f"dp{ws}" + (" (per-block NCCL grad all-reduce overlapped with backward)"
+                   "parallelism": f"dp{ws}" + ((" ZeRO-1 (per-block NCCL reduce-scatter overlapped with backward, "
+                                                "sharded K2/K4, half all-gather)" if args.zero else
+                                                " (per-block NCCL grad all-reduce overlapped with backward)")
                                                if ws > 1 else ""),
                    "execution": "one CUDA graph per step" if use_graph else "eager stream-ordered launches"},
         "roofline": {"bound": "tensor", "achieved": round(tflops, 1), "peak": peak, "unit": "TFLOP/s",
@@ -493,6 +496,7 @@ def main():
     ap.add_argument("--vit-half", choices=["f16", "bf16"], default=None,
                     help="ViT section half format (default: bf16 at 1 GPU = configs[2], f16 at N > 1 = configs[3])")
     ap.add_argument("--no-graph", action="store_true", help="ViT section: eager launches instead of a CUDA graph")
+    ap.add_argument("--zero", action="store_true", help="ViT section at N > 1: ZeRO-1 sharded optimizer step")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -54,20 +54,73 @@ class GradBuckets:
 
 
 class GradExchange:
-    def __init__(self, buckets: GradBuckets, group=None):
+    """All-reduce each bucket as the backward completes it — or, under ZeRO-1
+    (`zero_views`: key -> (whole padded bucket, this rank's chunk)),
+    reduce-scatter it so each rank receives the sum of its chunk only."""
+
+    def __init__(self, buckets: GradBuckets, group=None, zero_views: dict | None = None):
         self.buckets = buckets
         self.group = group
+        self.zero_views = zero_views
         self.pending = []
 
     def ready(self, key: str):
         if self.group is None:
             return
-        self.pending.append(dist.all_reduce(self.buckets.views[key], group=self.group, async_op=True))
+        if self.zero_views is not None:
+            full, mine = self.zero_views[key]
+            self.pending.append(dist.reduce_scatter_tensor(mine, full, group=self.group, async_op=True))
+        else:
+            self.pending.append(dist.all_reduce(self.buckets.views[key], group=self.group, async_op=True))
 
     def wait(self):
         for w in self.pending:
             w.wait()
         self.pending.clear()
+
+
+def _bucket_spans(paths: list[str], offsets: list[int], arena_numel: int) -> list[tuple[str, int, int]]:
+    """(key, lo, hi) per bucket in arena order; hi = the next bucket's start
+    (or the arena end), i.e. including the bucket's alignment padding."""
+    first: dict[str, int] = {}
+    for p, o in zip(paths, offsets):
+        k = bucket_key(p)
+        first[k] = min(first.get(k, o), o)
+    starts = sorted((o, k) for k, o in first.items())
+    return [(k, o, starts[i + 1][0] if i + 1 < len(starts) else arena_numel) for i, (o, k) in enumerate(starts)]
+
+
+def shard_ranges(paths: list[str], offsets: list[int], world: int, rank: int,
+                 arena_numel: int) -> list[tuple[int, int]]:
+    """ZeRO-1: rank `rank`'s (offset, length) chunk of
+    every bucket — each bucket span (padded to a multiple of 8*world by the
+    arena layout) split into `world` equal, 16-byte-aligned chunks."""
+    out = []
+    for _, lo, hi in _bucket_spans(paths, offsets, arena_numel):
+        n = hi - lo
+        if n % (8 * world):
+            raise ValueError(f"bucket at {lo} spans {n} elements, not a multiple of 8*world={8 * world}")
+        c = n // world
+        out.append((lo + rank * c, c))
+    return out
+
+
+def zero_bucket_views(arena: torch.Tensor, ranges: list[tuple[int, int]], world: int, rank: int):
+    """(whole bucket, this rank's chunk) views of `arena` for each bucket: the
+    in-place layouts of reduce_scatter (chunk = sum) and all_gather."""
+    out = []
+    for off, c in ranges:
+        lo = off - rank * c
+        out.append((arena[lo:lo + world * c], arena[off:off + c]))
+    return out
+
+
+def zero_views_by_key(arena: torch.Tensor, paths: list[str], offsets: list[int], world: int, rank: int) -> dict:
+    """bucket key -> (whole padded bucket, this rank's chunk) of `arena`."""
+    spans = _bucket_spans(paths, offsets, arena.numel())
+    ranges = shard_ranges(paths, offsets, world, rank, arena.numel())
+    views = zero_bucket_views(arena, ranges, world, rank)
+    return {k: v for (k, _, _), v in zip(spans, views)}
 
 
 def allreduce_flag_min(flag: torch.Tensor, group=None):

@@ -33,14 +33,21 @@ from .tree import float_leaves, tree_map
 
 
 class FlatArena:
-    """Views of one allocation laid out like a pytree's float leaves."""
+    """Views of one allocation laid out like a pytree's float leaves.
 
-    def __init__(self, leaves, dtype: torch.dtype, device):
+    Every leaf starts on an 8-element (16-byte) boundary; with `groups` (one
+    key per leaf, consecutive equal keys form a group) each group also ends on a
+    multiple of `group_align` elements, so a group splits into equal,
+    aligned chunks (the ZeRO-1 shards of a gradient bucket)."""
+
+    def __init__(self, leaves, dtype: torch.dtype, device, groups=None, group_align: int = 8):
         self.offsets = []
         total = 0
-        for t in leaves:
+        for i, t in enumerate(leaves):
             self.offsets.append(total)
             total += -(-t.numel() // 8) * 8
+            if groups is not None and (i + 1 == len(leaves) or groups[i + 1] != groups[i]):
+                total = -(-total // group_align) * group_align
         self.numel = total
         self.buf = torch.empty(max(total, 8), dtype=dtype, device=device)
         self.views = [self.buf[o:o + t.numel()].view(t.shape) for o, t in zip(self.offsets, leaves)]
@@ -59,7 +66,8 @@ class FusedMPStep:
 
     def __init__(self, params, lr: float, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
                  weight_decay: float = 0.0, half_dtype=F16, scaling: DynamicLossScaling | None = None,
-                 process_group=None):
+                 process_group=None, zero: bool = False, zero_world: int | None = None,
+                 zero_rank: int | None = None):
         self.structure = params
         fl = float_leaves(params)
         if not fl:
@@ -70,11 +78,27 @@ class FusedMPStep:
         dev = leaves[0].device
         self.device = dev
         self.half = as_dtype(half_dtype)
-        self.p32 = FlatArena(leaves, torch.float32, dev)
-        self.m = FlatArena(leaves, torch.float32, dev)
-        self.v = FlatArena(leaves, torch.float32, dev)
-        self.p_half = FlatArena(leaves, self.half.torch, dev)
-        self.grad = FlatArena(leaves, self.half.torch, dev)
+        # ZeRO-1: rank r updates chunk r of every gradient
+        # bucket (K2/K4 on 1/W of the bytes); the half grads arrive by
+        # reduce-scatter and the half working copy leaves by all-gather
+        self.zero = bool(zero)
+        if self.zero:
+            if process_group is not None:
+                zero_world = torch.distributed.get_world_size(process_group)
+                zero_rank = torch.distributed.get_rank(process_group)
+            if zero_world is None or zero_rank is None:
+                raise ValueError("zero=True needs a process group (or zero_world / zero_rank)")
+            self.zero_world, self.zero_rank = int(zero_world), int(zero_rank)
+        else:
+            self.zero_world, self.zero_rank = 1, 0
+        from .dp import bucket_key
+        groups = [bucket_key(p) for p in self.paths] if self.zero else None
+        align = 8 * self.zero_world
+        self.p32 = FlatArena(leaves, torch.float32, dev, groups, align)
+        self.m = FlatArena(leaves, torch.float32, dev, groups, align)
+        self.v = FlatArena(leaves, torch.float32, dev, groups, align)
+        self.p_half = FlatArena(leaves, self.half.torch, dev, groups, align)
+        self.grad = FlatArena(leaves, self.half.torch, dev, groups, align)
         self.p32.buf.zero_()  # alignment pads stay 0 (finite) in every arena
         for dst, src in zip(self.p32.views, leaves):
             dst.copy_(src)
@@ -96,14 +120,24 @@ class FusedMPStep:
 
     # ------------------------------------------------------------------
     def _build_tables(self):
-        one = lambda p: (ctypes.c_void_p * 1)(p)  # noqa: E731
-        self._n = (ctypes.c_int64 * 1)(self.numel)
-        self._g_tab = one(self.grad.ptr())
-        self._p_tab = one(self.p32.ptr())
-        self._pd_tab = (ctypes.c_int32 * 1)(N.MPX_F32)
-        self._m_tab = one(self.m.ptr())
-        self._v_tab = one(self.v.ptr())
-        self._h_tab = one(self.p_half.ptr())
+        # (offset, length) element ranges this rank steps: the whole arena, or
+        # under ZeRO-1 its chunk of every bucket (buckets in arena order)
+        if self.zero:
+            from .dp import shard_ranges
+            self.ranges = shard_ranges(self.paths, self.p32.offsets, self.zero_world, self.zero_rank, self.numel)
+        else:
+            self.ranges = [(0, self.numel)]
+        L = len(self.ranges)
+        tab = lambda arena, es: (ctypes.c_void_p * L)(*[arena.ptr() + o * es for o, _ in self.ranges])  # noqa: E731
+        hs = self.grad.buf.element_size()
+        self._L = L
+        self._n = (ctypes.c_int64 * L)(*[n for _, n in self.ranges])
+        self._g_tab = tab(self.grad, hs)
+        self._p_tab = tab(self.p32, 4)
+        self._pd_tab = (ctypes.c_int32 * L)(*([N.MPX_F32] * L))
+        self._m_tab = tab(self.m, 4)
+        self._v_tab = tab(self.v, 4)
+        self._h_tab = tab(self.p_half, hs)
         self._grad_src = self.grad.ptr()
 
     def tree(self, kind: str):
@@ -127,35 +161,57 @@ class FusedMPStep:
         buffer being filled by a copy engine)."""
         lib = self._lib
         st = stream if stream is not None else K.stream_handle(self.device)
-        g = self._g_tab if grad_ptr is None else (ctypes.c_void_p * 1)(grad_ptr)
+        g = self._grad_table(grad_ptr)
         d_scale = self.scaling.state.data_ptr()
         code = self.half.code
-        N.check(lib.mpx_unscale_finite(N.as_pp(g), None, self._n, 1, code, 1.0, d_scale, self.flag.data_ptr(), 1,
+        L = self._L
+        N.check(lib.mpx_unscale_finite(N.as_pp(g), None, self._n, L, code, 1.0, d_scale, self.flag.data_ptr(), 1,
                                        st), "mpx_unscale_finite")
-        if self.group is not None:
+        if self.group is not None:  # AND over ranks (mandatory under ZeRO-1: shards see different grads)
             torch.distributed.all_reduce(self.flag, op=torch.distributed.ReduceOp.MIN, group=self.group)
         N.check(lib.mpx_optimizer_step(N.as_pp(self._p_tab), self._pd_tab, N.as_pp(self._m_tab),
-                                       N.as_pp(self._v_tab), N.as_pp(g), N.as_pp(self._h_tab), None, self._n, 1,
+                                       N.as_pp(self._v_tab), N.as_pp(g), N.as_pp(self._h_tab), None, self._n, L,
                                        code, code, 0, self.hp, self.bc.data_ptr(), self.bc.numel() // 2,
                                        self.counter.data_ptr(), 1.0, d_scale, self.flag.data_ptr(), st),
                 "mpx_optimizer_step")
         N.check(lib.mpx_scaling_adjust(self.scaling.state.data_ptr(), self.flag.data_ptr(), None,
                                        self.used_scale.data_ptr(), st), "mpx_scaling_adjust")
+        if self.zero and self.group is not None:
+            self.all_gather_half()
+
+    def _grad_table(self, grad_ptr):
+        if grad_ptr is None:
+            return self._g_tab
+        hs = self.grad.buf.element_size()
+        return (ctypes.c_void_p * self._L)(*[grad_ptr + o * hs for o, _ in self.ranges])
+
+    # ZeRO-1 exchange over the bucket layout (also done per bucket by trainer.GradExchange)
+    def reduce_scatter_grads(self):
+        """Sum the half grads over the group into this rank's chunk of every bucket."""
+        from .dp import zero_bucket_views
+        for full, mine in zero_bucket_views(self.grad.buf, self.ranges, self.zero_world, self.zero_rank):
+            torch.distributed.reduce_scatter_tensor(mine, full, group=self.group)
+
+    def all_gather_half(self):
+        """Every rank's updated chunk of the half working copy to every rank."""
+        from .dp import zero_bucket_views
+        for full, mine in zero_bucket_views(self.p_half.buf, self.ranges, self.zero_world, self.zero_rank):
+            torch.distributed.all_gather_into_tensor(full, mine, group=self.group)
 
     # per-kernel entry points (timing / profiling)
     def k2(self, grad_ptr=None, stream=None):
         st = stream if stream is not None else K.stream_handle(self.device)
-        g = self._g_tab if grad_ptr is None else (ctypes.c_void_p * 1)(grad_ptr)
-        N.check(self._lib.mpx_unscale_finite(N.as_pp(g), None, self._n, 1, self.half.code, 1.0,
+        g = self._grad_table(grad_ptr)
+        N.check(self._lib.mpx_unscale_finite(N.as_pp(g), None, self._n, self._L, self.half.code, 1.0,
                                              self.scaling.state.data_ptr(), self.flag.data_ptr(), 1, st), "k2")
 
     def k4(self, grad_ptr=None, stream=None):
         st = stream if stream is not None else K.stream_handle(self.device)
-        g = self._g_tab if grad_ptr is None else (ctypes.c_void_p * 1)(grad_ptr)
+        g = self._grad_table(grad_ptr)
         code = self.half.code
         N.check(self._lib.mpx_optimizer_step(N.as_pp(self._p_tab), self._pd_tab, N.as_pp(self._m_tab),
                                              N.as_pp(self._v_tab), N.as_pp(g), N.as_pp(self._h_tab), None, self._n,
-                                             1, code, code, 0, self.hp, self.bc.data_ptr(), self.bc.numel() // 2,
+                                             self._L, code, code, 0, self.hp, self.bc.data_ptr(), self.bc.numel() // 2,
                                              self.counter.data_ptr(), 1.0, self.scaling.state.data_ptr(),
                                              self.flag.data_ptr(), st), "k4")
 

@@ -30,7 +30,7 @@ from .vit_config import ViTConfig
 class ViTTrainer:
     def __init__(self, cfg: ViTConfig, batch_per_gpu: int, half=F16, lr: float = 1e-3, device=None,
                  group=None, world_size: int = 1, seed: int = 0, loss_scale: float = 2.0 ** 15,
-                 weight_decay: float = 0.0):
+                 weight_decay: float = 0.0, zero: bool = False):
         self.cfg = cfg
         self.B = batch_per_gpu
         self.half = as_dtype(half)
@@ -38,8 +38,12 @@ class ViTTrainer:
         self.group = group
         self.W = world_size
         params = init_params(cfg, self.dev, seed=seed)  # same seed on every rank: replicas start equal
+        # zero=True (ZeRO-1): buckets reduce-scattered during the
+        # backward, K2/K4 on this rank's 1/W chunk, half working copy all-gathered
+        self.zero = bool(zero) and group is not None
         self.mp = FusedMPStep(params, lr, weight_decay=weight_decay, half_dtype=self.half,
-                              scaling=DynamicLossScaling(loss_scale, device=self.dev), process_group=group)
+                              scaling=DynamicLossScaling(loss_scale, device=self.dev), process_group=group,
+                              zero=self.zero)
         del params
         self.engine = ViTEngine(cfg, batch_per_gpu, self.half, self.dev)
         self.paths = self.mp.paths
@@ -51,7 +55,12 @@ class ViTTrainer:
         self.inv_w = torch.full((), 1.0 / world_size, dtype=torch.float32, device=self.dev)
         numels = [v.numel() for v in self.mp.grad.views]
         self.buckets = GradBuckets(self.paths, self.mp.grad.offsets, numels, self.mp.grad.buf)
-        self.exchange = GradExchange(self.buckets, group)
+        zviews = None
+        if self.zero:
+            from .dp import zero_views_by_key
+            zviews = zero_views_by_key(self.mp.grad.buf, self.paths, self.mp.grad.offsets, self.mp.zero_world,
+                                       self.mp.zero_rank)
+        self.exchange = GradExchange(self.buckets, group, zero_views=zviews)
 
     # ------------------------------------------------------------------
     def forward_backward(self, images: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
