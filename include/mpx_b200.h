@@ -70,6 +70,9 @@ typedef struct mpx_adam_hparams {
 const char* mpx_last_error(void);
 int mpx_version(void);
 int mpx_num_sms(int device);
+/* kernels launched by this library so far in this process (every entry
+ * point); bench.py reports its timed regions' launches from it */
+int64_t mpx_launch_count(void);
 
 /* K1 — multi-tensor cast/scale: dst[i] = round_{dst_dtype}(f32(src[i]) * s).
  * Replaces cast_tree/cast_to_* (precision.py:53-85, T.cast tensors.py:529,

@@ -67,6 +67,7 @@ SIGNATURES = {
     "mpx_last_error": (ctypes.c_char_p, []),
     "mpx_version": (ctypes.c_int, []),
     "mpx_num_sms": (ctypes.c_int, [ctypes.c_int]),
+    "mpx_launch_count": (ctypes.c_int64, []),
     "mpx_cast": (ctypes.c_int, [_PP, _PP, _I64P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_double, _P, _P]),
     "mpx_unscale_finite": (ctypes.c_int, [_PP, _PP, _I64P, ctypes.c_int, ctypes.c_int, ctypes.c_double,

@@ -53,6 +53,7 @@ __device__ __forceinline__ void pdl_grid_sync() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 bool pdl_enabled();
+void count_launch();  // every kernel the library launches (mpx_launch_count)
 inline void pdl_attr(cudaLaunchAttribute& a) {
   a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
   a.val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
@@ -70,6 +71,7 @@ inline cudaError_t launch_cfg(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 
   if (!pdl) attr[0].val.programmaticStreamSerializationAllowed = 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  count_launch();
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 // plain stream-ordered launch (the ViT kernels: measured no gain from PDL

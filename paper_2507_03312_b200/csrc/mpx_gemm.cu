@@ -1143,6 +1143,7 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;  // (no PDL for the ViT kernels, see launch_k)
+    count_launch();
     MPX_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, P));
   }
   MPX_LAUNCH_CHECK("gemm_kernel");

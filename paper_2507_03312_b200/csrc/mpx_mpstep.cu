@@ -16,6 +16,7 @@
 // vector accesses, grid sized to resident-blocks x SM count.
 #include "mpx_common.cuh"
 
+#include <atomic>
 #include <cstdlib>
 
 #include <algorithm>
@@ -30,6 +31,9 @@ int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 bool pdl_enabled() {
   static const bool on = !(getenv("MPX_PDL") && getenv("MPX_PDL")[0] == '0');
@@ -507,6 +511,8 @@ static int64_t tiles_of(int64_t n) { return (n + kTile - 1) / kTile; }
 using namespace mpx;
 
 extern "C" {
+
+int64_t mpx_launch_count(void) { return mpx::g_launches.load(std::memory_order_relaxed); }
 
 const char* mpx_last_error(void) { return g_last_error.c_str(); }
 int mpx_version(void) { return 1; }
