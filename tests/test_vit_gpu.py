@@ -59,11 +59,14 @@ CFGS = {
 @pytest.mark.parametrize("name", list(CFGS))
 @pytest.mark.parametrize("half", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("fused", ["1", "0"])
-def test_engine_matches_fp32_reference(cuda, name, half, fused, monkeypatch):
-    """fused = K6 attention kernels; "0" = GEMM + softmax island + GEMM."""
+@pytest.mark.parametrize("B", [4, 1, 3])
+def test_engine_matches_fp32_reference(cuda, name, half, fused, B, monkeypatch):
+    """fused = K6 attention kernels; "0" = GEMM + softmax island + GEMM; odd
+    and single-image batches exercise the GEMM / attention tails."""
+    if B != 4 and (half != torch.bfloat16 or name == "tiny-mean"):
+        pytest.skip("odd batches: bf16 on the cls configs only")
     monkeypatch.setenv("MPX_FUSED_ATTENTION", fused)
     cfg = CFGS[name]
-    B = 4
     p32 = init_params(cfg, cuda, seed=3, std=0.05)
     for k in p32:  # non-trivial LayerNorm parameters
         if k.endswith(".g") or k.endswith(".b"):
