@@ -246,6 +246,10 @@ int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int B, int N, 
 /* image [B,H,W,C] -> patch rows [B*(H/P)*(W/P), P*P*C], order (py, px, c) */
 int mpx_patchify(int dtype, const void* img, void* patches, int B, int H, int W, int C, int P, void* stream);
 /* strided row copy dst[b][r][c] = src[b][r][c] */
+/* dst[c*ld_dst + r] = src[r*ld_src + c] (16-bit): the forward keeps its
+ * weights K-major for the GEMM's B operand (MN-major B costs ~6 %) */
+int mpx_transpose(int dtype, const void* src, int rows, int cols, int64_t ld_src, void* dst, int64_t ld_dst,
+                  void* stream);
 int mpx_copy_rows(int dtype, const void* src, int64_t ld_src, int64_t sb_src, void* dst, int64_t ld_dst,
                   int64_t sb_dst, int rows, int batches, int cols, void* stream);
 /* dst[b*sb + c] = a[c] + b[c] (cls token + its position embedding) */

@@ -102,6 +102,8 @@ SIGNATURES = {
                                          ctypes.c_int, ctypes.c_float, _P, _P, _P, _P, _P, _P]),
     "mpx_patchify": (ctypes.c_int, [ctypes.c_int, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_int, _P]),
+    "mpx_transpose": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _P,
+                                     ctypes.c_int64, _P]),
     "mpx_copy_rows": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, ctypes.c_int64, _P, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]),
     "mpx_rows_add": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P]),

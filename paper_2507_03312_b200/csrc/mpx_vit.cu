@@ -1001,6 +1001,38 @@ __global__ void __launch_bounds__(256) patchify_vec_kernel(const uint4* __restri
   }
 }
 
+// dst[c][r] = src[r][c] for 16-bit elements: 64 x 64 tiles through shared
+// memory (+2-element row pad: conflict-free column reads), 32-bit words on
+// both sides
+__global__ void __launch_bounds__(256) transpose16_kernel(const uint16_t* __restrict__ src, long long ld_src,
+                                                          uint16_t* __restrict__ dst, long long ld_dst, int rows,
+                                                          int cols) {
+  ::mpx::pdl_grid_sync();
+  __shared__ uint16_t tile[64][66];
+  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 column pairs x 8 rows per pass
+  for (int i = ty; i < 64; i += 8) {
+    const int r = r0 + i, c = c0 + 2 * tx;
+    uint16_t a = 0, b = 0;
+    if (r < rows && c < cols) a = src[(long long)r * ld_src + c];
+    if (r < rows && c + 1 < cols) b = src[(long long)r * ld_src + c + 1];
+    tile[i][2 * tx] = a;
+    tile[i][2 * tx + 1] = b;
+  }
+  __syncthreads();
+  for (int i = ty; i < 64; i += 8) {  // dst row = source column c0 + i, 2 source rows per thread
+    const int c = c0 + i, r = r0 + 2 * tx;
+    if (c >= cols) continue;
+    if (r + 1 < rows && ((ld_dst & 1) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 3) == 0)) {
+      const uint32_t w = (uint32_t)tile[2 * tx][i] | ((uint32_t)tile[2 * tx + 1][i] << 16);
+      *reinterpret_cast<uint32_t*>(dst + (long long)c * ld_dst + r) = w;
+    } else {
+      if (r < rows) dst[(long long)c * ld_dst + r] = tile[2 * tx][i];
+      if (r + 1 < rows) dst[(long long)c * ld_dst + r + 1] = tile[2 * tx + 1][i];
+    }
+  }
+}
+
 // strided row copy by 16-byte vectors (cols % 8 == 0, 16-byte aligned rows)
 __global__ void __launch_bounds__(256) copy_rows_vec_kernel(const uint16_t* __restrict__ src, long long ld_src,
                                                             long long sb_src, uint16_t* __restrict__ dst,
@@ -1310,6 +1342,18 @@ int mpx_copy_rows(int dtype, const void* src, int64_t ld_src, int64_t sb_src, vo
   MPX_CUDA_CHECK(::mpx::launch_k(copy_rows_kernel, ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream), static_cast<const uint16_t*>(src), ld_src, sb_src, static_cast<uint16_t*>(dst), ld_dst, sb_dst, rows, batches,
       cols));
   MPX_LAUNCH_CHECK("copy_rows_kernel");
+  return 0;
+}
+
+int mpx_transpose(int dtype, const void* src, int rows, int cols, int64_t ld_src, void* dst, int64_t ld_dst,
+                  void* stream) {
+  if (!half_dtype(dtype)) return fail(MPX_EINVAL, "transpose: f16/bf16 only");
+  if (rows <= 0 || cols <= 0) return 0;
+  if (ld_src < cols || ld_dst < rows) return fail(MPX_EINVAL, "transpose: bad leading dimensions");
+  const dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64));
+  MPX_CUDA_CHECK(::mpx::launch_k(transpose16_kernel, grid, 256, 0, static_cast<cudaStream_t>(stream),
+                                 static_cast<const uint16_t*>(src), (long long)ld_src, static_cast<uint16_t*>(dst),
+                                 (long long)ld_dst, rows, cols));
   return 0;
 }
 

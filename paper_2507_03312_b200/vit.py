@@ -76,6 +76,8 @@ class ViTEngine:
             self.attn_p = [torch.empty(VK.attention_psave_bytes(B, S, H), dtype=torch.uint8, device=self.dev)
                            for _ in range(c.depth)]
         self.O = [e(M, D) for _ in range(c.depth)]
+        # one block's weights transposed (K-major GEMM operands), refilled per block
+        self._wt = {"qkv": e(3 * D, D), "proj": e(D, D), "fc1": e(c.mlp, D), "fc2": e(D, c.mlp)}
         self.xm = [e(M, D) for _ in range(c.depth)]  # after attention residual
         self.bn = [e(M, D) for _ in range(c.depth)]  # LN2 out
         self.pre = [e(M, c.mlp) for _ in range(c.depth)]  # fc1 pre-activation
@@ -179,7 +181,12 @@ class ViTEngine:
             q = f"blocks.{i}."
             x, a, qkv = self.x[i], self.a[i], self.qkv[i]
             self._ln_fwd(x, D, p[q + "ln1.g"], p[q + "ln1.b"], a, D, self.mu1[i], self.rs1[i], M)
-            VK.linear_fwd(a, p[q + "qkv.w"], bias=p[q + "qkv.b"], out=qkv)
+            # the block's four weights, transposed once into K-major copies (the GEMM reads
+            # a K-major B operand ~6 % faster than the MN-major [K, N] layout)
+            wt = self._wt
+            for name in ("qkv", "proj", "fc1", "fc2"):
+                VK.transpose(p[q + name + ".w"], out=wt[name])
+            VK.linear_fwd_t(a, wt["qkv"], bias=p[q + "qkv.b"], out=qkv)
             O = self.O[i]
             if self.fused_attn:
                 VK.attention_fwd(qkv, B, S, H, hd, scale, out=O, p_save=self.attn_p[i])
@@ -193,11 +200,11 @@ class ViTEngine:
                 VK.gemm(P_, qkv[:, 2 * D:], M=S, N=hd, K=S, lda=self.ldS, ldb=3 * D, b_mn=True, nb=(H, B),
                         a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * 3 * D), out=O, ldc=D, c_sb=(hd, S * D))
             xm = self.xm[i]
-            VK.linear_fwd(O, p[q + "proj.w"], bias=p[q + "proj.b"], residual=x, out=xm)
+            VK.linear_fwd_t(O, wt["proj"], bias=p[q + "proj.b"], residual=x, out=xm)
             bn = self.bn[i]
             self._ln_fwd(xm, D, p[q + "ln2.g"], p[q + "ln2.b"], bn, D, self.mu2[i], self.rs2[i], M)
-            VK.linear_fwd(bn, p[q + "fc1.w"], bias=p[q + "fc1.b"], act=VK.ACT_GELU, aux=self.pre[i], out=self.h[i])
-            VK.linear_fwd(self.h[i], p[q + "fc2.w"], bias=p[q + "fc2.b"], residual=xm, out=self.x[i + 1])
+            VK.linear_fwd_t(bn, wt["fc1"], bias=p[q + "fc1.b"], act=VK.ACT_GELU, aux=self.pre[i], out=self.h[i])
+            VK.linear_fwd_t(self.h[i], wt["fc2"], bias=p[q + "fc2.b"], residual=xm, out=self.x[i + 1])
         xl = self.x[c.depth]
         if cls:
             self._ln_fwd(xl, S * D, p["ln_f.g"], p["ln_f.b"], self.fin, D, self.muf, self.rsf, B)

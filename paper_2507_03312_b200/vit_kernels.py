@@ -75,6 +75,26 @@ def linear_fwd(x, w, bias=None, act=ACT_NONE, aux=None, residual=None, out=None,
                 out=out, ldc=N_ if out is not None else None, cta_group=cta_group)
 
 
+def transpose(src, out=None):
+    """out[c, r] = src[r, c] for a 2-D f16/bf16 tensor (mpx_transpose)."""
+    require_cuda([src], "transpose")
+    R, C = src.shape
+    if out is None:
+        out = torch.empty(C, R, dtype=src.dtype, device=src.device)
+    _nat.check(_nat.load().mpx_transpose(_CODE[src.dtype], src.data_ptr(), R, C, src.stride(0), out.data_ptr(),
+                                         out.stride(0), stream_handle(src.device)), "mpx_transpose")
+    return out
+
+
+def linear_fwd_t(x, wt, bias=None, act=ACT_NONE, aux=None, residual=None, out=None, cta_group=0):
+    """y[M,N] = x[M,K] @ wt[N,K]^T — the weight held transposed (K-major B,
+    faster than linear_fwd's MN-major read of w[K,N])."""
+    M, K = x.shape
+    N_ = wt.shape[0]
+    return gemm(x, wt, M=M, N=N_, K=K, lda=K, ldb=K, bias=bias, act=act, aux=aux, residual=residual,
+                out=out, ldc=N_ if out is not None else None, cta_group=cta_group)
+
+
 def linear_dgrad(dy, w, aux=None, out=None, cta_group=0, colsum_out=None, colsum_ws=None):
     """dx[M,K] = dy[M,N] @ w[K,N]^T; with aux (the GELU pre-activation of
     this layer's input) the GELU derivative is applied in the epilogue;
