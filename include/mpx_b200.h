@@ -250,6 +250,9 @@ int mpx_patchify(int dtype, const void* img, void* patches, int B, int H, int W,
  * weights K-major for the GEMM's B operand (MN-major B costs ~6 %) */
 int mpx_transpose(int dtype, const void* src, int rows, int cols, int64_t ld_src, void* dst, int64_t ld_dst,
                   void* stream);
+/* the same for n <= 64 matrices in one launch (the forward's weight copies) */
+int mpx_transpose_batch(int dtype, int n, const void* const* src, void* const* dst, const int* rows,
+                        const int* cols, const int64_t* ld_src, const int64_t* ld_dst, void* stream);
 int mpx_copy_rows(int dtype, const void* src, int64_t ld_src, int64_t sb_src, void* dst, int64_t ld_dst,
                   int64_t sb_dst, int rows, int batches, int cols, void* stream);
 /* dst[b*sb + c] = a[c] + b[c] (cls token + its position embedding) */

@@ -104,6 +104,7 @@ SIGNATURES = {
                                     ctypes.c_int, _P]),
     "mpx_transpose": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _P,
                                      ctypes.c_int64, _P]),
+    "mpx_transpose_batch": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, _P, _P]),
     "mpx_copy_rows": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, ctypes.c_int64, _P, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]),
     "mpx_rows_add": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P]),

@@ -1001,34 +1001,57 @@ __global__ void __launch_bounds__(256) patchify_vec_kernel(const uint4* __restri
   }
 }
 
-// dst[c][r] = src[r][c] for 16-bit elements: 64 x 64 tiles through shared
-// memory (+2-element row pad: conflict-free column reads), 32-bit words on
-// both sides
-__global__ void __launch_bounds__(256) transpose16_kernel(const uint16_t* __restrict__ src, long long ld_src,
-                                                          uint16_t* __restrict__ dst, long long ld_dst, int rows,
-                                                          int cols) {
+// dst[c][r] = src[r][c] for 16-bit elements, many matrices per launch: 64 x 64
+// tiles through shared memory (+2-element row pad), 32-bit words on both sides
+struct TransposeJob {
+  const uint16_t* src;
+  uint16_t* dst;
+  int rows, cols;
+  long long ld_src, ld_dst;
+  int tile_begin, tiles_c;  // first tile index of this job, tiles per tile-row
+};
+constexpr int kMaxTransposeJobs = 64;
+struct TransposeBatch {
+  TransposeJob job[kMaxTransposeJobs];
+  int n;
+};
+
+__global__ void __launch_bounds__(256) transpose16_kernel(const __grid_constant__ TransposeBatch T) {
   ::mpx::pdl_grid_sync();
   __shared__ uint16_t tile[64][66];
-  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  int j = 0;
+  while (j + 1 < T.n && (int)blockIdx.x >= T.job[j + 1].tile_begin) ++j;
+  const TransposeJob& J = T.job[j];
+  const int t = blockIdx.x - J.tile_begin;
+  const int r0 = (t / J.tiles_c) * 64, c0 = (t % J.tiles_c) * 64;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 column pairs x 8 rows per pass
+  const bool wide = (J.cols & 1) == 0 && (J.ld_src & 1) == 0 && (reinterpret_cast<uintptr_t>(J.src) & 3) == 0;
+#pragma unroll 4
   for (int i = ty; i < 64; i += 8) {
     const int r = r0 + i, c = c0 + 2 * tx;
-    uint16_t a = 0, b = 0;
-    if (r < rows && c < cols) a = src[(long long)r * ld_src + c];
-    if (r < rows && c + 1 < cols) b = src[(long long)r * ld_src + c + 1];
-    tile[i][2 * tx] = a;
-    tile[i][2 * tx + 1] = b;
+    uint32_t w = 0;
+    if (r < J.rows && c < J.cols) {
+      if (wide)
+        w = *reinterpret_cast<const uint32_t*>(J.src + (long long)r * J.ld_src + c);
+      else
+        w = (uint32_t)J.src[(long long)r * J.ld_src + c] |
+            (c + 1 < J.cols ? (uint32_t)J.src[(long long)r * J.ld_src + c + 1] << 16 : 0u);
+    }
+    tile[i][2 * tx] = (uint16_t)(w & 0xFFFFu);
+    tile[i][2 * tx + 1] = (uint16_t)(w >> 16);
   }
   __syncthreads();
+  const bool wide_out = (J.ld_dst & 1) == 0 && (reinterpret_cast<uintptr_t>(J.dst) & 3) == 0;
+#pragma unroll 4
   for (int i = ty; i < 64; i += 8) {  // dst row = source column c0 + i, 2 source rows per thread
     const int c = c0 + i, r = r0 + 2 * tx;
-    if (c >= cols) continue;
-    if (r + 1 < rows && ((ld_dst & 1) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 3) == 0)) {
+    if (c >= J.cols) continue;
+    if (r + 1 < J.rows && wide_out) {
       const uint32_t w = (uint32_t)tile[2 * tx][i] | ((uint32_t)tile[2 * tx + 1][i] << 16);
-      *reinterpret_cast<uint32_t*>(dst + (long long)c * ld_dst + r) = w;
+      *reinterpret_cast<uint32_t*>(J.dst + (long long)c * J.ld_dst + r) = w;
     } else {
-      if (r < rows) dst[(long long)c * ld_dst + r] = tile[2 * tx][i];
-      if (r + 1 < rows) dst[(long long)c * ld_dst + r + 1] = tile[2 * tx + 1][i];
+      if (r < J.rows) J.dst[(long long)c * J.ld_dst + r] = tile[2 * tx][i];
+      if (r + 1 < J.rows) J.dst[(long long)c * J.ld_dst + r + 1] = tile[2 * tx + 1][i];
     }
   }
 }
@@ -1345,16 +1368,35 @@ int mpx_copy_rows(int dtype, const void* src, int64_t ld_src, int64_t sb_src, vo
   return 0;
 }
 
+int mpx_transpose_batch(int dtype, int n, const void* const* src, void* const* dst, const int* rows,
+                        const int* cols, const int64_t* ld_src, const int64_t* ld_dst, void* stream) {
+  if (!half_dtype(dtype)) return fail(MPX_EINVAL, "transpose: f16/bf16 only");
+  if (n < 0 || n > kMaxTransposeJobs) return fail(MPX_EINVAL, "transpose: at most 64 matrices per call");
+  TransposeBatch T{};
+  int tiles = 0;
+  for (int i = 0; i < n; ++i) {
+    if (rows[i] <= 0 || cols[i] <= 0) continue;
+    if (ld_src[i] < cols[i] || ld_dst[i] < rows[i]) return fail(MPX_EINVAL, "transpose: bad leading dimensions");
+    TransposeJob& J = T.job[T.n++];
+    J.src = static_cast<const uint16_t*>(src[i]);
+    J.dst = static_cast<uint16_t*>(dst[i]);
+    J.rows = rows[i];
+    J.cols = cols[i];
+    J.ld_src = ld_src[i];
+    J.ld_dst = ld_dst[i];
+    J.tile_begin = tiles;
+    J.tiles_c = (cols[i] + 63) / 64;
+    tiles += ((rows[i] + 63) / 64) * J.tiles_c;
+  }
+  if (tiles == 0) return 0;
+  MPX_CUDA_CHECK(::mpx::launch_k(transpose16_kernel, tiles, 256, 0, static_cast<cudaStream_t>(stream), T));
+  return 0;
+}
+
 int mpx_transpose(int dtype, const void* src, int rows, int cols, int64_t ld_src, void* dst, int64_t ld_dst,
                   void* stream) {
-  if (!half_dtype(dtype)) return fail(MPX_EINVAL, "transpose: f16/bf16 only");
-  if (rows <= 0 || cols <= 0) return 0;
-  if (ld_src < cols || ld_dst < rows) return fail(MPX_EINVAL, "transpose: bad leading dimensions");
-  const dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64));
-  MPX_CUDA_CHECK(::mpx::launch_k(transpose16_kernel, grid, 256, 0, static_cast<cudaStream_t>(stream),
-                                 static_cast<const uint16_t*>(src), (long long)ld_src, static_cast<uint16_t*>(dst),
-                                 (long long)ld_dst, rows, cols));
-  return 0;
+  const int64_t ls = ld_src, ld = ld_dst;
+  return mpx_transpose_batch(dtype, 1, &src, &dst, &rows, &cols, &ls, &ld, stream);
 }
 
 int mpx_rows_add(int dtype, const void* a, const void* b, void* dst, int64_t sb, int B, int D, void* stream) {

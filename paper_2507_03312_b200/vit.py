@@ -76,8 +76,9 @@ class ViTEngine:
             self.attn_p = [torch.empty(VK.attention_psave_bytes(B, S, H), dtype=torch.uint8, device=self.dev)
                            for _ in range(c.depth)]
         self.O = [e(M, D) for _ in range(c.depth)]
-        # one block's weights transposed (K-major GEMM operands), refilled per block
-        self._wt = {"qkv": e(3 * D, D), "proj": e(D, D), "fc1": e(c.mlp, D), "fc2": e(D, c.mlp)}
+        # the blocks' weights transposed (K-major GEMM operands), refreshed every forward
+        self._wt = [{"qkv": e(3 * D, D), "proj": e(D, D), "fc1": e(c.mlp, D), "fc2": e(D, c.mlp)}
+                    for _ in range(c.depth)]
         self.xm = [e(M, D) for _ in range(c.depth)]  # after attention residual
         self.bn = [e(M, D) for _ in range(c.depth)]  # LN2 out
         self.pre = [e(M, c.mlp) for _ in range(c.depth)]  # fc1 pre-activation
@@ -177,15 +178,18 @@ class ViTEngine:
             self._ck(lib.mpx_rows_add(self.code, p["cls"].data_ptr(), p["pos"].data_ptr(), x0.data_ptr(), S * D, B, D,
                                       st), "rows_add")
         scale = 1.0 / math.sqrt(hd)
+        # every block's four weights transposed into K-major copies in one launch (the
+        # GEMM reads a K-major B operand ~6 % faster than the MN-major [K, N] layout)
+        names = ("qkv", "proj", "fc1", "fc2")
+        for i0 in range(0, c.depth, 16):  # <= 64 matrices per launch
+            blocks = range(i0, min(c.depth, i0 + 16))
+            VK.transpose_batch([p[f"blocks.{i}.{n}.w"] for i in blocks for n in names],
+                               [self._wt[i][n] for i in blocks for n in names])
         for i in range(c.depth):
             q = f"blocks.{i}."
             x, a, qkv = self.x[i], self.a[i], self.qkv[i]
             self._ln_fwd(x, D, p[q + "ln1.g"], p[q + "ln1.b"], a, D, self.mu1[i], self.rs1[i], M)
-            # the block's four weights, transposed once into K-major copies (the GEMM reads
-            # a K-major B operand ~6 % faster than the MN-major [K, N] layout)
-            wt = self._wt
-            for name in ("qkv", "proj", "fc1", "fc2"):
-                VK.transpose(p[q + name + ".w"], out=wt[name])
+            wt = self._wt[i]
             VK.linear_fwd_t(a, wt["qkv"], bias=p[q + "qkv.b"], out=qkv)
             O = self.O[i]
             if self.fused_attn:

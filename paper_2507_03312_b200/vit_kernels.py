@@ -86,6 +86,21 @@ def transpose(src, out=None):
     return out
 
 
+def transpose_batch(srcs, outs):
+    """outs[i][c, r] = srcs[i][r, c] for up to 64 2-D f16/bf16 tensors in one launch."""
+    require_cuda(list(srcs), "transpose_batch")
+    n = len(srcs)
+    if n == 0:
+        return outs
+    P, I, L = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+    _nat.check(_nat.load().mpx_transpose_batch(
+        _CODE[srcs[0].dtype], n, (P * n)(*[s.data_ptr() for s in srcs]), (P * n)(*[o.data_ptr() for o in outs]),
+        (I * n)(*[s.shape[0] for s in srcs]), (I * n)(*[s.shape[1] for s in srcs]),
+        (L * n)(*[s.stride(0) for s in srcs]), (L * n)(*[o.stride(0) for o in outs]),
+        stream_handle(srcs[0].device)), "mpx_transpose_batch")
+    return outs
+
+
 def linear_fwd_t(x, wt, bias=None, act=ACT_NONE, aux=None, residual=None, out=None, cta_group=0):
     """y[M,N] = x[M,K] @ wt[N,K]^T — the weight held transposed (K-major B,
     faster than linear_fwd's MN-major read of w[K,N])."""
