@@ -628,19 +628,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           for (int s = 0; s < 4; ++s)  // dP = dO V^T
             umma_f16(tmem, sw128_desc(dO + s * 32, 16, 1024), sw128_desc(v + s * 32, 16, 1024), id_nk, s > 0);
           umma_commit(&bar[4]);
-          mbar_wait(&bar[5], ph);  // dS_t written (dP consumed)
-          if (it == 0) ATRACE(4 + 8 * t);
-          if (t == 0 && it > 0) mbar_wait(&bar[10], (it - 1) & 1);  // last item's dV/dK read out of TMEM
-          tc_fence_after();
-          // dK first (its completion frees Q_t), then dV (frees dO_t), then dQ:
-          // the next tile's Q / dO loads overlap dV, dQ and the dQ readout
-          for (int half = 0; half < halves; ++half) {
-#pragma unroll
-            for (int s = 0; s < 8; ++s)  // over the 128 queries of the tile: dK += dS^T Q
-              umma_f16(tmem + 384 + half * 64, sw128_desc(ds + half * 32768 + s * 2048, 16384, 1024),
-                       sw128_desc(q + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
+          // dV needs only P_t and dO_t: it runs on the tensor pipe while the
+          // softmax warps turn dP into dS (TMEM cols 256-383, disjoint from dP)
+          if (t == 0 && it > 0) {
+            mbar_wait(&bar[10], (it - 1) & 1);  // last item's dV/dK read out of TMEM
+            tc_fence_after();
           }
-          umma_commit(&bar[8]);
           for (int half = 0; half < halves; ++half) {
 #pragma unroll
             for (int s = 0; s < 8; ++s)  // dV += P^T dO
@@ -648,6 +641,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                        sw128_desc(dO + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
           }
           umma_commit(&bar[9]);
+          mbar_wait(&bar[5], ph);  // dS_t written (dP consumed, P_t no longer read by the softmax warps)
+          if (it == 0) ATRACE(4 + 8 * t);
+          tc_fence_after();
+          // dK first (its completion frees Q_t), then dQ: the next tile's Q / dO
+          // loads overlap dQ and the dQ readout
+          for (int half = 0; half < halves; ++half) {
+#pragma unroll
+            for (int s = 0; s < 8; ++s)  // over the 128 queries of the tile: dK += dS^T Q
+              umma_f16(tmem + 384 + half * 64, sw128_desc(ds + half * 32768 + s * 2048, 16384, 1024),
+                       sw128_desc(q + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
+          }
+          umma_commit(&bar[8]);
           for (int s = 0; s < n_chunks; ++s)  // dQ = dS K
             umma_f16(tmem, sw128_desc(ds + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
                      sw128_desc(k + s * 2048, 8192, 1024), id_q, s > 0);
