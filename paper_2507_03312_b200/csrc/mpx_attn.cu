@@ -43,6 +43,10 @@ __device__ long long g_attn_trace[kTraceCtas * kTraceSlots];
   do {               \
   } while (0)
 #endif
+#ifndef MPX_TRACE_IT
+#define MPX_TRACE_IT 0
+#endif
+constexpr int kTraceIt = MPX_TRACE_IT;  // which item of each CTA the trace records
 
 constexpr int kAttnQ = 16384;      // Q tile 128 x 64 half
 constexpr int kAttnKV = 32768;     // K / V 256 x 64 half
@@ -606,13 +610,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (blockIdx.x < P.items) load_item(blockIdx.x);
       for (int item = blockIdx.x; item < P.items; item += gridDim.x, ++it) {
         const int h = item % P.H, b = item / P.H;
-        ATRACE(0);
+        if (it == kTraceIt) ATRACE(0);
+        if (it == kTraceIt + 1) ATRACE(21);
         mbar_wait(&bar[0], it & 1);
-        ATRACE(1);
+        if (it == kTraceIt) ATRACE(1);
         for (int t = 0; t < T; ++t, ++gt) {
           const uint32_t ph = gt & 1;
           mbar_wait(&bar[1], ph);
-          if (it == 0) ATRACE(2 + 8 * t);
+          if (it == kTraceIt) ATRACE(2 + 8 * t);
           if (gt > 0) mbar_wait(&bar[7], ph ^ 1);  // previous dQ drained from TMEM cols 0-63
           tc_fence_after();
           if (!saved) {  // recompute P: S = Q K^T, softmax by the softmax warps
@@ -621,7 +626,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
               umma_f16(tmem, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), id_nk, s > 0);
             umma_commit(&bar[2]);
             mbar_wait(&bar[3], ph);  // P_t written (S consumed)
-            if (it == 0) ATRACE(3 + 8 * t);
+            if (it == kTraceIt) ATRACE(3 + 8 * t);
             tc_fence_after();
           }
 #pragma unroll
@@ -642,7 +647,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           }
           umma_commit(&bar[9]);
           mbar_wait(&bar[5], ph);  // dS_t written (dP consumed, P_t no longer read by the softmax warps)
-          if (it == 0) ATRACE(4 + 8 * t);
+          if (it == kTraceIt) ATRACE(4 + 8 * t);
           tc_fence_after();
           // dK first (its completion frees Q_t), then dQ: the next tile's Q / dO
           // loads overlap dQ and the dQ readout
@@ -700,7 +705,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         float2 st = make_float2(0.f, 0.f);  // the forward's (max, 1/sum), fetched while S is computed
         if (P.stats) st = __ldg(P.stats + ((long long)item * T + t) * 128 + r);
         mbar_wait(&bar[2], ph);
-        if (warp == 4 && lane == 0 && it == 0) ATRACE(5 + 8 * t);
+        if (warp == 4 && lane == 0 && it == kTraceIt) ATRACE(5 + 8 * t);
         tc_fence_after();
         softmax_bwd_p<kSplit>(trow, split, r, qd, P.N, P.scale, P.fmt, red, sP, P.stats ? &st : nullptr);
         fence_async_smem();
@@ -712,7 +717,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       // ---- dS = P * (dP - sum(P * dP)) -> smem; dP rounded to the half
       // format first (the reference's dP is a half GEMM output), kept packed
       mbar_wait(&bar[4], ph);
-      if (warp == 4 && lane == 0 && it == 0) ATRACE(6 + 8 * t);
+      if (warp == 4 && lane == 0 && it == kTraceIt) ATRACE(6 + 8 * t);
       tc_fence_after();
       uint32_t dpk[kMaxC][8];
       float2 tsum2 = f2(0.f);
@@ -763,7 +768,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_arrive(&bar[5]);
       // ---- dQ_t -> dqkv[:, q part]
       mbar_wait(&bar[6], ph);
-      if (warp == 4 && lane == 0 && it == 0) ATRACE(7 + 8 * t);
+      if (warp == 4 && lane == 0 && it == kTraceIt) ATRACE(7 + 8 * t);
       tc_fence_after();
       const int qrow = t * 128 + r;
       uint16_t* o = static_cast<uint16_t*>(P.dqkv) + ((long long)b * P.N + qrow) * P.ld + (long long)h * P.hd;
@@ -792,7 +797,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&bar[7]);
-      if (warp == 4 && lane == 0 && it == 0) ATRACE(8 + 8 * t);
+      if (warp == 4 && lane == 0 && it == kTraceIt) ATRACE(8 + 8 * t);
     }
     // ---- dV, dK (keys r and 128 + r of this head): 4 (half, which) combos split over the warps
     float kvsum[4] = {0.f, 0.f, 0.f, 0.f};  // per chunk: column col16(lane), this warp's 32 keys
@@ -850,6 +855,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // dV/dK (and the scratch) consumed: the next item may accumulate into TMEM cols 256-511
     tc_fence_before();
     mbar_arrive(&bar[10]);
+    if (warp == 4 && lane == 0 && it == kTraceIt) ATRACE(20);
     }
   }
   tc_fence_before();

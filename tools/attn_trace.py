@@ -1,6 +1,7 @@
 """Phase timeline of the fused attention backward (needs the -DMPX_TRACE
 build: python paper_2507_03312_b200/_build.py -DMPX_TRACE -o abl/libmpx_trace.so).
-Prints, per phase, the median over the first 64 CTAs of cycles since slot 0."""
+Prints, per phase, the median over the first 64 CTAs of cycles since slot 0
+(the item traced is -DMPX_TRACE_IT=k, default the first)."""
 import ctypes
 import os
 import sys
@@ -29,7 +30,7 @@ buf = (ctypes.c_longlong * (64 * 32))()
 assert lib.mpx_debug_attn_trace(buf) == 0
 a = np.frombuffer(buf, dtype=np.int64).reshape(64, 32).astype(np.float64)
 a = a - a[:, :1]
-names = {0: "mma: item start (last item)", 1: "mma: K,V landed (last item)", 30: "end"}
+names = {0: "mma: item start", 1: "mma: K,V landed", 20: "smx: dV/dK read out", 21: "mma: next item start", 30: "end"}
 for t in range(2):
     names.update({2 + 8 * t: f"t{t} mma: Q,dO landed", 3 + 8 * t: f"t{t} mma: P ready", 4 + 8 * t: f"t{t} mma: dS ready",
                   5 + 8 * t: f"t{t} smx: S ready", 6 + 8 * t: f"t{t} smx: dP ready", 7 + 8 * t: f"t{t} smx: dQ ready",
