@@ -52,12 +52,9 @@ constexpr int kAttnQ = 16384;      // Q tile 128 x 64 half
 constexpr int kAttnKV = 32768;     // K / V 256 x 64 half
 constexpr int kAttnP = 65536;      // P 128 x 256 half (4 K-major chunks of 64 keys)
 constexpr int kSplit = 4;          // backward: softmax warps per TMEM lane quarter (column split)
-constexpr int kSplitF = 4;         // forward (40 registers: 2 CTAs x 640 threads per SM)
+constexpr int kSplitF = 7;         // forward: 28 softmax warps + 4 control warps = 1024 threads (64 registers)
 constexpr int kAttnThreads = 128 + 128 * kSplit;  // warps 0-3 control, then 4*kSplit softmax warps
 constexpr int kAttnThreadsF = 128 + 128 * kSplitF;
-// forward smem: P (64 KB) overwrites the dead Q (16 KB) + K (32 KB) tiles once
-// S = Q K^T has been computed, so two CTAs fit on one SM
-constexpr size_t kAttnSmem = 1024 + kAttnP + kAttnKV + 2 * kSplitF * 128 * 4 + 256;
 
 struct AttnParams {
   int N, H, hd, m_tiles;
@@ -67,6 +64,7 @@ struct AttnParams {
   long long ldo;  // O row stride (elements); head h at column h*hd
   float2* stats;  // optional [(b*H + h)*m_tiles*128 + row] = (row max, 1 / row sum) for the backward
   uint8_t* psave;  // optional: P (rounded, as the P V MMA read it) to [B*H][N][16 ceil(N/16)] for the backward
+  int items;       // B * H (image, head) items, walked by a persistent grid
 };
 
 __device__ __forceinline__ float h2f(uint16_t h, int fmt) { return fmt ? to_f32<MPX_BF16>(h) : to_f32<MPX_F16>(h); }
@@ -76,83 +74,12 @@ __device__ __forceinline__ void quarter_sync(int q) {  // the NS warps sharing T
   asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * NS) : "memory");
 }
 
-// row r's softmax statistics over the keys this split handles, combined over
-// the kSplit warps of the quarter through smem: returns (m, 1/l)
-template <int NS>
-__device__ __forceinline__ void softmax_stats(uint32_t trow, int split, int r, int q, int N, float scale, int fmt,
-                                              float* red, float& m_out, float& inv_out) {
-  const int n_chunks = (N + 15) / 16;
-  float m = -INFINITY, l = 0.f;
-  for (int c = split; c < n_chunks; c += NS) {
-    uint32_t a[16];
-    tmem_ld16(trow + c * 16, a);
-    tmem_ld_wait();
-    float sv[16], cm = -INFINITY;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      sv[i] = c * 16 + i < N ? h2f(f2h(__uint_as_float(a[i]) * scale, fmt), fmt) : -INFINITY;
-      cm = fmaxf(cm, sv[i]);
-    }
-    const float nm = fmaxf(m, cm);
-    float add = 0.f;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) add += sv[i] == -INFINITY ? 0.f : __expf(sv[i] - nm);
-    l = (m == -INFINITY ? 0.f : l * __expf(m - nm)) + add;
-    m = nm;
-  }
-  red[split * 128 + r] = m;
-  red[NS * 128 + split * 128 + r] = l;
-  quarter_sync<NS>(q);
-  float M = -INFINITY;
-#pragma unroll
-  for (int j = 0; j < NS; ++j) M = fmaxf(M, red[j * 128 + r]);
-  float L = 0.f;
-#pragma unroll
-  for (int j = 0; j < NS; ++j) {
-    const float mj = red[j * 128 + r];
-    if (mj != -INFINITY) L += red[NS * 128 + j * 128 + r] * __expf(mj - M);
-  }
-  quarter_sync<NS>(q);  // red[] may be reused afterwards
-  m_out = M;
-  inv_out = 1.f / L;
-}
-
 // P chunk c (keys 16c..16c+15) of row r into the K-major SW128 P tile
 __device__ __forceinline__ void store_p_chunk(uint8_t* sP, int c, int r, const uint32_t* pk) {
   uint8_t* rowp = sP + (c >> 2) * 16384 + r * 128;
   const int u0 = (c & 3) * 2, sw = r & 7;
   *reinterpret_cast<uint4*>(rowp + ((u0 ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
   *reinterpret_cast<uint4*>(rowp + (((u0 + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-}
-
-// P = exp(round(s*scale) - m) * inv for the chunks of this split (zeros past N)
-template <int NS>
-__device__ __forceinline__ void softmax_write_p(uint32_t trow, int split, int r, int N, float scale, int fmt, float m,
-                                                float inv, uint8_t* sP) {
-  const int n_chunks = (N + 15) / 16;
-  for (int c = split; c < 16; c += NS) {
-    uint32_t pk[8];
-    if (c < n_chunks) {
-      uint32_t a[16];
-      tmem_ld16(trow + c * 16, a);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float e[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int col = c * 16 + 2 * i + j;
-          const float sv = h2f(f2h(__uint_as_float(a[2 * i + j]) * scale, fmt), fmt);
-          e[j] = col < N ? __expf(sv - m) * inv : 0.f;
-        }
-        pk[i] = pack2_fmt(e[0], e[1], fmt);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) pk[i] = 0u;
-    }
-    store_p_chunk(sP, c, r, pk);
-  }
 }
 
 __device__ __forceinline__ void unpack2(uint32_t pk, int fmt, float& lo, float& hi) {
@@ -191,101 +118,118 @@ __device__ __forceinline__ void grid_scores16(const uint32_t* a, const ScoreGrid
             sv[2 * i], sv[2 * i + 1]);
 }
 
-// Forward softmax of row r over the chunks c = split, split + NS, ... < n_chunks,
-// two TMEM passes (TMEM reads bound this kernel: 64 B/clk per SM):
-//   pass 1  online: running max m, e = exp(s - m) written back into the same
-//           TMEM columns, running sum rescaled when m grows; m kept per chunk
-//   pass 2  P = e * exp(m_chunk - M) / L rounded to half, into the K-major P tile
-// Full chunks run unpredicated; only the last chunk masks keys >= N.
-template <int NS>
-__device__ __forceinline__ void softmax_fwd_p(uint32_t trow, int split, int r, int q, int N, float scale, int fmt,
-                                              float* red, uint8_t* sP, float2* stats) {
+// Forward softmax of row r, one TMEM pass: the thread's chunks c = split +
+// NS j (< n_chunks) stay in registers (scores on the half grid, then e); the
+// row max is exchanged through red_m, e = 2^(sv sl - M log2 e), and the row
+// sum L is the chunk sums (pairs accumulated in order, then .x + .y) added in
+// chunk order — the canonical order the backward's recompute follows, so its
+// P is bit-identical.  Keys past N in the tail chunk are masked (e = 0); full
+// chunks run unpredicated.  Returns (M, 1/L); softmax_store_p then writes P.
+template <int FMT>
+__device__ __forceinline__ uint32_t pack2T(float a, float b) {
+  return FMT ? pack2<MPX_BF16>(a, b) : pack2<MPX_F16>(a, b);
+}
+template <int FMT>
+__device__ __forceinline__ float2 unpack2T(uint32_t pk) {
+  if (FMT) return make_float2(__uint_as_float(pk << 16), __uint_as_float(pk & 0xFFFF0000u));
+  return __half22float2(*reinterpret_cast<const __half2*>(&pk));
+}
+template <int NS, int KC, int FMT>
+__device__ __forceinline__ float2 softmax_fwd_regs(uint32_t trow, int split, int r, int q, int N, const ScoreGrid& G,
+                                                   float* red_m, float* red_l, uint32_t (&a)[KC][16]) {
   constexpr float kLog2e = 1.4426950408889634f;
-  constexpr int kMaxC = (16 + NS - 1) / NS;
-  const ScoreGrid G(scale, fmt);
   const int n_chunks = (N + 15) / 16;
   const int tail = N - (n_chunks - 1) * 16;  // valid keys in the last chunk (1..16)
-  float m = -INFINITY, l = 0.f;  // running max (scaled score units) and sum
-  float mc[kMaxC];               // running max used for each of this thread's chunks
-  auto pass1 = [&](uint32_t* a, auto masked) {
-    constexpr bool kMasked = decltype(masked)::value;
-    float sv[16];
-    grid_scores16(a, G, fmt, sv);
-    float cm = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (!kMasked || i < tail) cm = fmaxf(cm, sv[i]);
-    cm *= G.ms;
-    if (cm > m) {
-      if (m != -INFINITY) l *= ex2_approx((m - cm) * kLog2e);
-      m = cm;
+  for (int j = 0; j < KC; ++j)
+    if (split + NS * j < n_chunks) tmem_ld16(trow + (split + NS * j) * 16, a[j]);
+  tmem_ld_wait();
+  float mloc = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < KC; ++j) {
+    const int c = split + NS * j;
+    if (c < n_chunks) {
+      if (G.pre != 1.f) {  // scores onto the half grid (pre = 1 when the scale is folded: x * 1 == x)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) a[j][i] = __float_as_uint(__uint_as_float(a[j][i]) * G.pre);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float2 s2 = unpack2T<FMT>(pack2T<FMT>(__uint_as_float(a[j][2 * i]), __uint_as_float(a[j][2 * i + 1])));
+        a[j][2 * i] = __float_as_uint(s2.x);
+        a[j][2 * i + 1] = __float_as_uint(s2.y);
+      }
+      if (c == n_chunks - 1 && tail < 16) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i < tail) mloc = fmaxf(mloc, __uint_as_float(a[j][i]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) mloc = fmaxf(mloc, __uint_as_float(a[j][i]));
+      }
     }
-    const float ml = m * kLog2e;
-    float2 acc = f2(0.f);  // even / odd column partial sums (the backward recomputes them alike)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float2 arg = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), f2(G.sl), f2(-ml));
-      const float e0 = (!kMasked || 2 * i < tail) ? ex2_approx(arg.x) : 0.f;
-      const float e1 = (!kMasked || 2 * i + 1 < tail) ? ex2_approx(arg.y) : 0.f;
-      acc = __fadd2_rn(acc, make_float2(e0, e1));
-      a[2 * i] = __float_as_uint(e0);
-      a[2 * i + 1] = __float_as_uint(e1);
-    }
-    l += acc.x + acc.y;
-  };
-#pragma unroll
-  for (int j = 0; j < kMaxC; ++j) {
-    const int c = split + j * NS;
-    mc[j] = -INFINITY;
-    if (c >= n_chunks) continue;
-    uint32_t a[16];
-    tmem_ld16(trow + c * 16, a);
-    tmem_ld_wait();
-    if (c == n_chunks - 1 && tail < 16)
-      pass1(a, std::true_type{});
-    else
-      pass1(a, std::false_type{});
-    mc[j] = m;
-    tmem_st16(trow + c * 16, a);
   }
-  red[split * 128 + r] = m;
-  red[NS * 128 + split * 128 + r] = l;
+  red_m[split * 128 + r] = mloc * G.ms;
   quarter_sync<NS>(q);
   float M = -INFINITY;
 #pragma unroll
-  for (int j = 0; j < NS; ++j) M = fmaxf(M, red[j * 128 + r]);
-  float L = 0.f;
-#pragma unroll
-  for (int j = 0; j < NS; ++j) {
-    const float mj = red[j * 128 + r];
-    if (mj != -INFINITY) L += red[NS * 128 + j * 128 + r] * ex2_approx((mj - M) * kLog2e);
-  }
-  const float inv = 1.f / L;
-  if (stats != nullptr && split == 0) *stats = make_float2(M, inv);
-  tmem_st_wait();
-#pragma unroll
-  for (int j = 0; j < kMaxC; ++j) {
-    const int c = split + j * NS;
-    if (c >= n_chunks) continue;
-    uint32_t a[16];
-    tmem_ld16(trow + c * 16, a);
-    tmem_ld_wait();
-    const float f = ex2_approx((mc[j] - M) * kLog2e) * inv;
-    uint32_t pk[8];
+  for (int j = 0; j < NS; ++j) M = fmaxf(M, red_m[j * 128 + r]);
+  const float ml = M * kLog2e;
+  auto expc = [&](uint32_t* x, auto masked) {  // e in place, returns the chunk sum
+    constexpr bool kMasked = decltype(masked)::value;
+    float2 acc = f2(0.f);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float2 p2 = __fmul2_rn(make_float2(__uint_as_float(a[2 * i]), __uint_as_float(a[2 * i + 1])), f2(f));
-      pk[i] = pack2_fmt(p2.x, p2.y, fmt);
+      const float2 arg = __ffma2_rn(make_float2(__uint_as_float(x[2 * i]), __uint_as_float(x[2 * i + 1])), f2(G.sl),
+                                    f2(-ml));
+      const float e0 = (!kMasked || 2 * i < tail) ? ex2_approx(arg.x) : 0.f;
+      const float e1 = (!kMasked || 2 * i + 1 < tail) ? ex2_approx(arg.y) : 0.f;
+      acc = __fadd2_rn(acc, make_float2(e0, e1));
+      x[2 * i] = __float_as_uint(e0);
+      x[2 * i + 1] = __float_as_uint(e1);
     }
-    store_p_chunk(sP, c, r, pk);
+    return acc.x + acc.y;
+  };
+#pragma unroll
+  for (int j = 0; j < KC; ++j) {
+    const int c = split + NS * j;
+    if (c < n_chunks)
+      red_l[c * 128 + r] = (c == n_chunks - 1 && tail < 16) ? expc(a[j], std::true_type{}) : expc(a[j], std::false_type{});
+  }
+  quarter_sync<NS>(q);
+  float L = 0.f;
+  for (int c = 0; c < n_chunks; ++c) L += red_l[c * 128 + r];
+  return make_float2(M, 1.f / L);
+}
+
+// P = e * (1/L) rounded to half, the thread's chunks into the K-major P tile
+template <int NS, int KC, int FMT>
+__device__ __forceinline__ void softmax_store_p(int split, int r, int N, float inv, const uint32_t (&a)[KC][16],
+                                                uint8_t* sP) {
+  const int n_chunks = (N + 15) / 16;
+#pragma unroll
+  for (int j = 0; j < KC; ++j) {
+    const int c = split + NS * j;
+    if (c < n_chunks) {
+      uint32_t pk[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float2 p2 = __fmul2_rn(make_float2(__uint_as_float(a[j][2 * i]), __uint_as_float(a[j][2 * i + 1])),
+                                     f2(inv));
+        pk[i] = pack2T<FMT>(p2.x, p2.y);
+      }
+      store_p_chunk(sP, c, r, pk);
+    }
   }
 }
 
 // Backward: P_t of row r recomputed from the forward's (M, 1/L) when given,
-// else from statistics recomputed here in the forward's order (same bits).
+// else from statistics recomputed here in the forward's canonical order (exact
+// row max; chunk sums, each as softmax_fwd_regs forms it, added in chunk order
+// through `lsc` [16 chunks][128 rows]) — the same bits as the forward.
 template <int NS>
 __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, int q, int N, float scale, int fmt,
-                                              float* red, uint8_t* sP, const float2* stats) {
+                                              float* red, float* lsc, uint8_t* sP, const float2* stats) {
   constexpr float kLog2e = 1.4426950408889634f;
   const ScoreGrid G(scale, fmt);
   const int n_chunks = (N + 15) / 16;
@@ -295,57 +239,46 @@ __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, i
     const float2 st = *stats;
     M = st.x;
     inv = st.y;
-  } else {  // the forward's statistics, recomputed in its order (online max / rescaled sum)
-    float m = -INFINITY, l = 0.f;
-    auto stat = [&](const uint32_t* a, auto masked) {
-      constexpr bool kMasked = decltype(masked)::value;
-      float sv[16];
-      grid_scores16(a, G, fmt, sv);
-      float cm = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (!kMasked || i < tail) cm = fmaxf(cm, sv[i]);
-      cm *= G.ms;
-      if (cm > m) {
-        if (m != -INFINITY) l *= ex2_approx((m - cm) * kLog2e);
-        m = cm;
-      }
-      const float mlc = m * kLog2e;
-      float2 acc = f2(0.f);  // as the forward's pass 1
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float2 arg = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), f2(G.sl), f2(-mlc));
-        const float e0 = (!kMasked || 2 * i < tail) ? ex2_approx(arg.x) : 0.f;
-        const float e1 = (!kMasked || 2 * i + 1 < tail) ? ex2_approx(arg.y) : 0.f;
-        acc = __fadd2_rn(acc, make_float2(e0, e1));
-      }
-      l += acc.x + acc.y;
-    };
+  } else {
+    float mloc = -INFINITY;
     for (int c = split; c < n_chunks; c += NS) {
       uint32_t a[16];
       tmem_ld16(trow + c * 16, a);
       tmem_ld_wait();
-      if (c == n_chunks - 1 && tail < 16)
-        stat(a, std::true_type{});
-      else
-        stat(a, std::false_type{});
+      float sv[16];
+      grid_scores16(a, G, fmt, sv);
+      const int nv = c == n_chunks - 1 ? tail : 16;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (i < nv) mloc = fmaxf(mloc, sv[i]);
     }
-    red[split * 128 + r] = m;
+    red[split * 128 + r] = mloc * G.ms;
     quarter_sync<NS>(q);
     M = -INFINITY;
 #pragma unroll
     for (int j = 0; j < NS; ++j) M = fmaxf(M, red[j * 128 + r]);
-    float mj[NS];
+    const float mlc = M * kLog2e;
+    for (int c = split; c < n_chunks; c += NS) {
+      uint32_t a[16];
+      tmem_ld16(trow + c * 16, a);
+      tmem_ld_wait();
+      float sv[16];
+      grid_scores16(a, G, fmt, sv);
+      const int nv = c == n_chunks - 1 ? tail : 16;
+      float2 acc = f2(0.f);
 #pragma unroll
-    for (int j = 0; j < NS; ++j) mj[j] = red[j * 128 + r];
-    quarter_sync<NS>(q);  // one scratch row set (the backward's smem is full)
-    red[split * 128 + r] = l;
+      for (int i = 0; i < 8; ++i) {
+        const float2 arg = __ffma2_rn(make_float2(sv[2 * i], sv[2 * i + 1]), f2(G.sl), f2(-mlc));
+        const float e0 = 2 * i < nv ? ex2_approx(arg.x) : 0.f;
+        const float e1 = 2 * i + 1 < nv ? ex2_approx(arg.y) : 0.f;
+        acc = __fadd2_rn(acc, make_float2(e0, e1));
+      }
+      lsc[c * 128 + r] = acc.x + acc.y;
+    }
     quarter_sync<NS>(q);
     float L = 0.f;
-#pragma unroll
-    for (int j = 0; j < NS; ++j)
-      if (mj[j] != -INFINITY) L += red[j * 128 + r] * ex2_approx((mj[j] - M) * kLog2e);
-    quarter_sync<NS>(q);  // red[] is reused by the caller
+    for (int c = 0; c < n_chunks; ++c) L += lsc[c * 128 + r];
+    quarter_sync<NS>(q);  // red[] / lsc[] are reused by the caller
     inv = 1.f / L;
   }
   const float ml = M * kLog2e;
@@ -375,40 +308,57 @@ __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, i
   }
 }
 
-__global__ void __launch_bounds__(kAttnThreadsF, 2)
+// ===========================================================================
+// Forward: persistent, one CTA per SM walking the (image, head) items; per
+// item K, V and every 128-query tile's Q are loaded once.  The CTA's tiles
+// g = 0, 1, ... (item-major) alternate between two TMEM buffers (cols
+// 256 (g & 1) ..): S_g = Q K^T there, then O_g = P_g V over the consumed S_g.
+//   28 softmax warps (kSplitF column splits per lane quarter), software-
+//   pipelined one tile deep: softmax(S_g) in registers (softmax_fwd_regs, one
+//   TMEM pass), then the readout of O_{g-1} (its P V ran during that
+//   softmax), then P_g into the K-major SW128 P tile
+//   issuer (warp 0, one thread): S_{g+1} as soon as O_{g-1} is read out of its
+//   buffer, P_g V once P_g is written, the TMA stores of the rounded P tiles
+//   (psave), TMA loads — the next item's K and Q once this item's S MMAs have
+//   read them, V once its last P V has
+// smem: K, V (256 key rows, zero-filled past N), Q_0, Q_1, P, row-exchange
+// scratch.  Barriers: 0 K+Q landed, 1 V landed, 2/3 S in buffer 0/1, 4 P
+// written, 5/6 O in buffer 0/1, 7/8 buffer 0/1 read out, 9 P tile's TMA store
+// has read it
+// ===========================================================================
+constexpr size_t kAttnSmemF = 1024 + 2 * kAttnKV + 2 * kAttnQ + kAttnP + (kSplitF + 16) * 128 * 4 + 128;
+
+template <int KC, int FMT>
+__global__ void __launch_bounds__(kAttnThreadsF, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmP,
                     const __grid_constant__ AttnParams P) {
   extern __shared__ uint8_t smem_raw[];
-  // 1 KB-aligned by indexing the __shared__ array (not via an integer cast), so
-  // derived pointers stay in the shared window: STS/LDS, 32-bit addressing
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sP = smem;               // P, aliasing Q (0-16K) and K (16K-48K) after MMA1
-  uint8_t* sQ = smem;
-  uint8_t* sK = smem + kAttnQ;
-  uint8_t* sV = smem + kAttnP;
-  float* red = reinterpret_cast<float*>(sV + kAttnKV);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * kSplitF * 128);  // 0 load, 1 S, 2 P, 3 O
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 4);
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + kAttnKV;
+  uint8_t* sQ = sV + kAttnKV;  // Q_0, Q_1
+  uint8_t* sP = sQ + 2 * kAttnQ;
+  float* red_m = reinterpret_cast<float*>(sP + kAttnP);
+  float* red_l = red_m + kSplitF * 128;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red_l + 16 * 128);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tile = blockIdx.x;
-  const int mt = tile % P.m_tiles;
-  const int bh = tile / P.m_tiles;
-  const int h = bh % P.H, b = bh / P.H;
-  const int m0 = mt * 128;
+  const int T = P.m_tiles;
+  const int n_chunks = (P.N + 15) / 16;
+  // this CTA's items blockIdx.x, + gridDim.x, ...; tiles g = item index * T + t
+  const int n_items = P.items > (int)blockIdx.x ? (P.items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int G = n_items * T;
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_init(&bar[2], 128 * kSplitF);
-    mbar_init(&bar[3], 1);
+    for (int i = 0; i < 10; ++i) mbar_init(&bar[i], (i == 4 || i == 7 || i == 8) ? 128 * kSplitF : 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -416,75 +366,150 @@ __global__ void __launch_bounds__(kAttnThreadsF, 2)
   ::mpx::pdl_grid_sync();  // prologue done: wait for the predecessor's outputs
 
   if (warp == 0) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(&bar[0], kAttnQ + 2 * kAttnKV);
-      tma_load_4d(sQ, &tmQ, &bar[0], 0, m0, h, b);
-      tma_load_4d(sK, &tmK, &bar[0], 0, 0, h, b);
-      tma_load_4d(sV, &tmV, &bar[0], 0, 0, h, b);
-      mbar_wait(&bar[0], 0);
-      tc_fence_after();
-      const int n_chunks = (P.N + 15) / 16;
-      const uint32_t idesc1 = idesc_f16(P.fmt, 128, 16 * n_chunks, 0, 0);  // keys past N: never computed
-      const uint32_t q = smem_u32(sQ), k = smem_u32(sK);
+    if (lane == 0 && G > 0) {
+      auto item_of = [&](int i) { return (int)blockIdx.x + i * (int)gridDim.x; };
+      auto load_kq = [&](int i) {
+        const int item = item_of(i), hh = item % P.H, bb = item / P.H;
+        mbar_arrive_expect_tx(&bar[0], kAttnKV + T * kAttnQ);
+        tma_load_4d(sK, &tmK, &bar[0], 0, 0, hh, bb);
+        for (int t = 0; t < T; ++t) tma_load_4d(sQ + t * kAttnQ, &tmQ, &bar[0], 0, t * 128, hh, bb);
+      };
+      auto load_v = [&](int i) {
+        const int item = item_of(i);
+        mbar_arrive_expect_tx(&bar[1], kAttnKV);
+        tma_load_4d(sV, &tmV, &bar[1], 0, 0, item % P.H, item / P.H);
+      };
+      load_kq(0);
+      load_v(0);
+      const uint32_t idesc1 = idesc_f16(FMT, 128, 16 * n_chunks, 0, 0);  // keys past N: never computed
+      const uint32_t idesc2 = idesc_f16(FMT, 128, 64, 0, 1);
+      const uint32_t k = smem_u32(sK), v = smem_u32(sV), p = smem_u32(sP);
+      auto issue_s = [&](int gs) {  // S_gs = Q_t K^T into buffer gs & 1
+        const int i = gs / T, t = gs - i * T, buf = gs & 1;
+        if (t == 0) mbar_wait(&bar[0], i & 1);                            // the item's K and Q landed
+        if (gs >= 2) mbar_wait(&bar[7 + buf], ((gs >> 1) - 1) & 1);       // O_{gs-2} read out of the buffer
+        tc_fence_after();
+        const uint32_t q = smem_u32(sQ + t * kAttnQ);
 #pragma unroll
-      for (int s = 0; s < 4; ++s)  // S = Q K^T into TMEM cols 0-255
-        umma_f16(tmem, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), idesc1, s > 0);
-      umma_commit(&bar[1]);
-      mbar_wait(&bar[2], 0);
-      tc_fence_after();
-      if (P.psave) {  // the rounded P tile as the MMAs read it (rows < N, keys < 16 n_chunks)
-        for (int blk = 0; blk * 4 < n_chunks; ++blk) tma_store_4d(&tmP, sP + blk * 16384, blk * 64, m0, bh, 0);
-      }
-      const uint32_t idesc2 = idesc_f16(P.fmt, 128, 64, 0, 1);
-      const uint32_t p = smem_u32(sP), v = smem_u32(sV);
-      for (int s = 0; s < n_chunks; ++s)  // O = P V into TMEM cols 0-63 (S is consumed)
-        umma_f16(tmem, sw128_desc(p + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
-                 sw128_desc(v + s * 2048, 8192, 1024), idesc2, s > 0);
-      umma_commit(&bar[3]);
-      if (P.psave) {
-        bulk_commit();
-        bulk_wait_read0();  // P read out of smem before the CTA may exit
+        for (int s = 0; s < 4; ++s)
+          umma_f16(tmem + 256 * buf, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), idesc1,
+                   s > 0);
+        umma_commit(&bar[2 + buf]);
+        if (t == T - 1 && i + 1 < n_items) {  // K and the Q tiles are free once these S MMAs completed
+          mbar_wait(&bar[2 + buf], (gs >> 1) & 1);
+          load_kq(i + 1);
+        }
+      };
+      issue_s(0);
+      for (int g = 0; g < G; ++g) {
+        if (g % T == 0 && g / T == kTraceIt) ATRACE(0);
+        if (g % T == 0 && g / T == kTraceIt + 1) ATRACE(20);
+        if (g + 1 < G) issue_s(g + 1);
+        const int i = g / T, t = g - i * T, buf = g & 1;
+        if (t == 0) mbar_wait(&bar[1], i & 1);  // V landed
+        mbar_wait(&bar[4], g & 1);              // P_g written (S_g consumed)
+        tc_fence_after();
+        if (P.psave) {  // the rounded P tile as the MMAs read it (rows < N, keys < 16 n_chunks)
+          for (int blk = 0; blk * 4 < n_chunks; ++blk)
+            tma_store_4d(&tmP, sP + blk * 16384, blk * 64, t * 128, item_of(i), 0);
+          bulk_commit();
+        }
+        for (int s = 0; s < n_chunks; ++s)  // O_g = P_g V
+          umma_f16(tmem + 256 * buf, sw128_desc(p + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
+                   sw128_desc(v + s * 2048, 8192, 1024), idesc2, s > 0);
+        umma_commit(&bar[5 + buf]);
+        if (P.psave) bulk_wait_read0();
+        mbar_arrive(&bar[9]);
+        if (t == T - 1 && i + 1 < n_items) {  // V is free once this P V completed
+          mbar_wait(&bar[5 + buf], (g >> 1) & 1);
+          load_v(i + 1);
+        }
       }
     }
   } else if (warp >= 4) {
     const int q = warp & 3, split = (warp - 4) >> 2;
     const int r = q * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    mbar_wait(&bar[1], 0);
-    tc_fence_after();
-    // a lane quarter whose 32 query rows are all padding (rows >= N of the last
-    // tile) skips the softmax: its P rows stay whatever finite bytes the tile
-    // held, feed only O rows that are never stored, and are clipped from the saved P
-    if (m0 + q * 32 < P.N) {
-      float2* st = P.stats ? P.stats + ((long long)bh * P.m_tiles + mt) * 128 + r : nullptr;
-      softmax_fwd_p<kSplitF>(trow, split, r, q, P.N, P.scale, P.fmt, red, sP, st);
-    }
-    fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
-    tc_fence_before();
-    mbar_arrive(&bar[2]);
-    mbar_wait(&bar[3], 0);
-    tc_fence_after();
-    const int qrow = m0 + r;
-    uint16_t* o = static_cast<uint16_t*>(P.O) + ((long long)b * P.N + qrow) * P.ldo + (long long)h * P.hd;
-    for (int c = split; c < 4 && m0 + q * 32 < P.N; c += kSplitF) {
-      uint32_t a[16];
-      tmem_ld16(trow + c * 16, a);
-      tmem_ld_wait();
-      if (qrow < P.N) {
-        uint32_t pk[8];
+    const ScoreGrid G2(P.scale, FMT);
+    // tile bookkeeping advanced incrementally (no divisions per tile): the
+    // current tile (t, item = b H + h) and the previous one, whose O is read out
+    const int hstep = (int)gridDim.x % P.H, bstep = (int)gridDim.x / P.H;
+    int t = 0, item = blockIdx.x, h = item % P.H, b = item / P.H;
+    int pt = 0, ph_ = 0, pb = 0;
+    // O rows of the previous tile -> O (one 16-column chunk per split 0-3, two 8-column loads)
+    auto drain = [&](int g) {
+      const int buf = g & 1;
+      mbar_wait(&bar[5 + buf], (g >> 1) & 1);
+      tc_fence_after();
+      const int qrow = pt * 128 + r;
+      if (split < 4 && pt * 128 + q * 32 < P.N) {
+        uint16_t* o = static_cast<uint16_t*>(P.O) + ((long long)pb * P.N + qrow) * P.ldo + (long long)ph_ * P.hd +
+                      split * 16;
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          pk[i] = pack2_fmt(__uint_as_float(a[2 * i]), __uint_as_float(a[2 * i + 1]), P.fmt);
-        *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t o32[8];
+          tmem_ld8(trow + 256 * buf + split * 16 + hh * 8, o32);
+          tmem_ld_wait();
+          if (qrow < P.N)
+            *reinterpret_cast<uint4*>(o + hh * 8) =
+                make_uint4(pack2T<FMT>(__uint_as_float(o32[0]), __uint_as_float(o32[1])),
+                           pack2T<FMT>(__uint_as_float(o32[2]), __uint_as_float(o32[3])),
+                           pack2T<FMT>(__uint_as_float(o32[4]), __uint_as_float(o32[5])),
+                           pack2T<FMT>(__uint_as_float(o32[6]), __uint_as_float(o32[7])));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bar[7 + buf]);
+    };
+    for (int g = 0; g < G; ++g) {
+      const int buf = g & 1;
+      // a lane quarter whose 32 query rows are all padding (rows >= N of the last
+      // tile) skips the softmax: its P rows keep whatever finite bytes the tile
+      // held, feed only O rows that are never stored, and are clipped from the saved P
+      const bool live = t * 128 + q * 32 < P.N;
+      mbar_wait(&bar[2 + buf], (g >> 1) & 1);
+      const bool tr = warp == 4 && lane == 0 && (g / T) == kTraceIt;
+      if (tr) ATRACE(1 + 8 * t);
+      tc_fence_after();
+      uint32_t a[KC][16];
+      float2 st = make_float2(0.f, 0.f);
+      if (live) st = softmax_fwd_regs<kSplitF, KC, FMT>(trow + 256 * buf, split, r, q, P.N, G2, red_m, red_l, a);
+      if (tr) ATRACE(2 + 8 * t);
+      if (g > 0) {
+        drain(g - 1);                     // O_{g-1}: its P V also means the P tile is no longer read by MMAs
+        if (tr) ATRACE(3 + 8 * t);
+        mbar_wait(&bar[9], (g - 1) & 1);  // ... and its TMA store has read it
+      }
+      if (tr) ATRACE(4 + 8 * t);
+      if (live) {
+        softmax_store_p<kSplitF, KC, FMT>(split, r, P.N, st.y, a, sP);
+        if (P.stats != nullptr && split == 0) P.stats[((long long)item * T + t) * 128 + r] = st;
+      }
+      fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core / TMA
+      tc_fence_before();
+      mbar_arrive(&bar[4]);
+      if (tr) ATRACE(5 + 8 * t);
+      pt = t;
+      ph_ = h;
+      pb = b;
+      if (++t == T) {
+        t = 0;
+        item += gridDim.x;
+        h += hstep;
+        b += bstep;
+        if (h >= P.H) {
+          h -= P.H;
+          ++b;
+        }
       }
     }
+    if (G > 0) drain(G - 1);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<256>(tmem);
+    tmem_dealloc<512>(tmem);
   }
 }
 
@@ -707,7 +732,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mbar_wait(&bar[2], ph);
         if (warp == 4 && lane == 0 && it == kTraceIt) ATRACE(5 + 8 * t);
         tc_fence_after();
-        softmax_bwd_p<kSplit>(trow, split, r, qd, P.N, P.scale, P.fmt, red, sP, P.stats ? &st : nullptr);
+        softmax_bwd_p<kSplit>(trow, split, r, qd, P.N, P.scale, P.fmt, red, reinterpret_cast<float*>(sdS), sP,
+                              P.stats ? &st : nullptr);
         fence_async_smem();
         tc_fence_before();
         mbar_arrive(&bar[3]);
@@ -953,14 +979,24 @@ extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H
   P.ldo = ldo;
   P.stats = reinterpret_cast<float2*>(row_stats);
   P.psave = static_cast<uint8_t*>(p_save);
+  P.items = B * H;
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmem);
+    const void* ks[4] = {(const void*)attn_fwd_kernel<2, 0>, (const void*)attn_fwd_kernel<2, 1>,
+                         (const void*)attn_fwd_kernel<3, 0>, (const void*)attn_fwd_kernel<3, 1>};
+    for (const void* kf : ks)
+      if (err == cudaSuccess) err = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmemF);
   });
   if (err != cudaSuccess) return fail((int)err, "cudaFuncSetAttribute(attn_fwd_kernel)");
-  const long long grid = (long long)B * H * P.m_tiles;
-  MPX_CUDA_CHECK(::mpx::launch_k(attn_fwd_kernel, (unsigned)grid, kAttnThreadsF, kAttnSmem, static_cast<cudaStream_t>(stream), tq, tk, tv, tp, P));
+  // persistent: one CTA per SM walks the (image, head) items; KC = score chunks
+  // per softmax thread (2 up to N = 224)
+  const unsigned grid = (unsigned)std::min(B * H, current_num_sms());
+  const int kc3 = (N + 15) / 16 > 2 * kSplitF;
+  auto kern = kc3 ? (fmt ? attn_fwd_kernel<3, 1> : attn_fwd_kernel<3, 0>)
+                  : (fmt ? attn_fwd_kernel<2, 1> : attn_fwd_kernel<2, 0>);
+  MPX_CUDA_CHECK(::mpx::launch_k(kern, grid, kAttnThreadsF, kAttnSmemF, static_cast<cudaStream_t>(stream), tq, tk,
+                                 tv, tp, P));
   MPX_LAUNCH_CHECK("attn_fwd_kernel");
   return 0;
 }
