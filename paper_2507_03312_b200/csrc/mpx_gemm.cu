@@ -163,7 +163,9 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, long long t
 // per 256-row tile: each CTA stages its 128 A rows and half of the BN B
 // columns, the leader issues tcgen05.mma.cta_group::2 (M = 256), so each SM
 // streams 2/3 of the bytes per FLOP of the 1-CTA tile.
-template <int CG, int XO>
+// FMT: the A/B (and 16-bit C, bias, residual, aux) format, 0 f16 / 1 bf16,
+// compiled in so the epilogue carries one conversion path
+template <int CG, int XO, int FMT>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
@@ -350,15 +352,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t u[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          o[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), P.ab_fmt);
-          o[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), P.ab_fmt);
+          o[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), FMT);
+          o[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), FMT);
         }
       };
       // ---- softmax modes: row statistics over this warp's column groups,
       // combined with the partner warp (same TMEM lane quarter) through smem
       float row_m = 0.f, row_inv = 1.f, row_t = 0.f;
       const bool smx = XO == XOP_NONE && (P.act == ACT_SOFTMAX || P.act == ACT_SOFTMAX_BWD);
-      auto round_half = [&](float x) { return half_to_f32(f32_to_half(x, P.ab_fmt), P.ab_fmt); };
+      auto round_half = [&](float x) { return half_to_f32(f32_to_half(x, FMT), FMT); };
       if (smx) {
         float m = -INFINITY, l = 0.f, tacc = 0.f;
         for (int g = h; g * 64 < P.BN; g += kEpiPerQ) {
@@ -388,8 +390,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
-                pv[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), P.ab_fmt);
-                pv[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), P.ab_fmt);
+                pv[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), FMT);
+                pv[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), FMT);
               }
 #pragma unroll
               for (int i = 0; i < 16; ++i)
@@ -433,7 +435,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             } else {
 #pragma unroll
               for (int i = 0; i < 16; ++i)
-                bb[i] = col + i < P.N ? half_to_f32(static_cast<const uint16_t*>(P.bias)[col + i], P.ab_fmt) : 0.f;
+                bb[i] = col + i < P.N ? half_to_f32(static_cast<const uint16_t*>(P.bias)[col + i], FMT) : 0.f;
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -483,7 +485,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           } else {  // ragged tail: the bias has exactly N entries
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              bb[i] = col + i < P.N ? half_to_f32(static_cast<const uint16_t*>(P.bias)[col + i], P.ab_fmt) : 0.f;
+              bb[i] = col + i < P.N ? half_to_f32(static_cast<const uint16_t*>(P.bias)[col + i], FMT) : 0.f;
           }
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += bb[i];
@@ -496,10 +498,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint32_t pk[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], P.ab_fmt);
+              pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], FMT);
               const uint16_t lo = (uint16_t)(pk[i] & 0xFFFFu), hi = (uint16_t)(pk[i] >> 16);
-              v[2 * i] = half_to_f32(lo, P.ab_fmt);  // GELU of the rounded pre-activation
-              v[2 * i + 1] = half_to_f32(hi, P.ab_fmt);
+              v[2 * i] = half_to_f32(lo, FMT);  // GELU of the rounded pre-activation
+              v[2 * i + 1] = half_to_f32(hi, FMT);
             }
             *reinterpret_cast<uint4*>(ax) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             if (ncols == 16) *reinterpret_cast<uint4*>(ax + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
@@ -544,7 +546,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         constexpr bool kAuxOut = XO == XOP_AUX_OUT;
         const bool f32out = P.split > 1 || P.c_dtype == MPX_F32;
         const int GW = (f32out || kAuxOut) ? 32 : 64;
-        const int cf = P.c_dtype == MPX_BF16 ? 1 : 0;
+        constexpr int cf = FMT;  // 16-bit C has the A/B format (checked on the host)
         const int n_groups = (P.BN + GW - 1) / GW;
         const int my_groups = n_groups > h ? (n_groups - h + kEpiPerQ - 1) / kEpiPerQ : 0;
         auto buf = [&](uint32_t c) { return obuf + (c % kBufPerWarp) * 4096; };
@@ -600,9 +602,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 uint32_t pa[8], pc[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                  pa[i] = pack2_fmt(v[2 * i], v[2 * i + 1], P.ab_fmt);
-                  const float a = half_to_f32((uint16_t)(pa[i] & 0xFFFFu), P.ab_fmt);
-                  const float b = half_to_f32((uint16_t)(pa[i] >> 16), P.ab_fmt);
+                  pa[i] = pack2_fmt(v[2 * i], v[2 * i + 1], FMT);
+                  const float a = half_to_f32((uint16_t)(pa[i] & 0xFFFFu), FMT);
+                  const float b = half_to_f32((uint16_t)(pa[i] >> 16), FMT);
                   const float2 y = gelu2(make_float2(a, b));  // GELU of the rounded pre-activation
                   pc[i] = pack2_fmt(y.x, y.y, cf);
                 }
@@ -624,8 +626,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                  xv[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), P.ab_fmt);
-                  xv[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), P.ab_fmt);
+                  xv[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), FMT);
+                  xv[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), FMT);
                 }
               }
               if (row_ok && col < P.N_store) epi(v, col, min(16, P.N_store - col), xv);
@@ -745,7 +747,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int i = 0; i < ncols; i += 4)
               *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
           } else {
-            const int f = P.c_dtype == MPX_BF16 ? 1 : 0;
+            constexpr int f = FMT;
             uint32_t pk[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i)
@@ -1018,6 +1020,8 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   P.c_sb1 = g->c_sb1;
   P.c_sb2 = g->c_sb2;
   P.c_dtype = g->c_dtype;
+  if (split == 1 && g->c_dtype != MPX_F32 && g->c_dtype != g->ab_dtype)
+    return fail(MPX_EINVAL, "mpx_gemm: a 16-bit C must have the A/B format");
   P.bias = g->bias;
   P.res = g->residual;
   P.ldr = g->ldr;
@@ -1101,17 +1105,22 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
 
   using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
                            const GemmParams);
-  static const KernelFn kernels[2][5] = {
-      {gemm_kernel<1, XOP_NONE>, gemm_kernel<1, XOP_RES_IN>, gemm_kernel<1, XOP_AUX_IN>, gemm_kernel<1, XOP_AUX_OUT>,
-       gemm_kernel<1, XOP_PLAIN>},
-      {gemm_kernel<2, XOP_NONE>, gemm_kernel<2, XOP_RES_IN>, gemm_kernel<2, XOP_AUX_IN>, gemm_kernel<2, XOP_AUX_OUT>,
-       gemm_kernel<2, XOP_PLAIN>}};
+  static const KernelFn kernels[2][2][5] = {
+      {{gemm_kernel<1, XOP_NONE, 0>, gemm_kernel<1, XOP_RES_IN, 0>, gemm_kernel<1, XOP_AUX_IN, 0>,
+        gemm_kernel<1, XOP_AUX_OUT, 0>, gemm_kernel<1, XOP_PLAIN, 0>},
+       {gemm_kernel<2, XOP_NONE, 0>, gemm_kernel<2, XOP_RES_IN, 0>, gemm_kernel<2, XOP_AUX_IN, 0>,
+        gemm_kernel<2, XOP_AUX_OUT, 0>, gemm_kernel<2, XOP_PLAIN, 0>}},
+      {{gemm_kernel<1, XOP_NONE, 1>, gemm_kernel<1, XOP_RES_IN, 1>, gemm_kernel<1, XOP_AUX_IN, 1>,
+        gemm_kernel<1, XOP_AUX_OUT, 1>, gemm_kernel<1, XOP_PLAIN, 1>},
+       {gemm_kernel<2, XOP_NONE, 1>, gemm_kernel<2, XOP_RES_IN, 1>, gemm_kernel<2, XOP_AUX_IN, 1>,
+        gemm_kernel<2, XOP_AUX_OUT, 1>, gemm_kernel<2, XOP_PLAIN, 1>}}};
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
-    for (int c = 0; c < 2 && attr_err == cudaSuccess; ++c)
-      for (int x = 0; x < 5 && attr_err == cudaSuccess; ++x)
-        attr_err = cudaFuncSetAttribute(kernels[c][x], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+    for (int f = 0; f < 2 && attr_err == cudaSuccess; ++f)
+      for (int c = 0; c < 2 && attr_err == cudaSuccess; ++c)
+        for (int x = 0; x < 5 && attr_err == cudaSuccess; ++x)
+          attr_err = cudaFuncSetAttribute(kernels[f][c][x], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
   });
   if (attr_err != cudaSuccess) return fail((int)attr_err, "cudaFuncSetAttribute(gemm_kernel)");
   // fused column sum: in the staged lean epilogues (16-bit C, one batch), else a separate pass
@@ -1124,7 +1133,7 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
                                                            : GemmSmem<XOP_AUX_IN>::kBufPerWarp);
     if (csum_fused) P.csum = g->colsum_ws;
   }
-  const KernelFn kern = kernels[CG - 1][P.xop];
+  const KernelFn kern = kernels[fmt][CG - 1][P.xop];
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (CG == 1) {
     const long long grid = std::min<long long>(P.total_tiles, current_num_sms());

@@ -52,11 +52,14 @@ __device__ __forceinline__ float warp_max(float v) {
 // ===========================================================================
 // K7 LayerNorm forward: y = (x - mean) * rstd * g + b over the last dim (f32)
 // ===========================================================================
-template <int V>  // V = 16-byte vectors per lane (D = 256 * V); V = 0: generic
+// V = 16-byte vectors per lane (D = 256 * V); V = 0: generic.  FMT (0 f16, 1
+// bf16) is a template parameter so only one conversion path is compiled.
+template <int V, int FMT>
 __global__ void __launch_bounds__(256) ln_fwd_kernel(const void* __restrict__ x, long long ldx,
                                                      const void* __restrict__ g, const void* __restrict__ b,
                                                      void* __restrict__ y, long long ldy, float* __restrict__ mean,
-                                                     float* __restrict__ rstd, int rows, int D, float eps, int fmt) {
+                                                     float* __restrict__ rstd, int rows, int D, float eps, int) {
+  constexpr int fmt = FMT;
   ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -235,14 +238,14 @@ __global__ void __launch_bounds__(256) ln_dx_kernel(const void* __restrict__ x, 
 // 4 warps per block, fixed row assignment).  The block's warps are combined
 // in a fixed order; ws layout [3][gridDim.x][D] for partials_reduce3_kernel.
 // ===========================================================================
-template <int V>
-__global__ void __launch_bounds__(128) ln_bwd_fused_kernel(const void* __restrict__ x, long long ldx,
+template <int V, int FMT>  // FMT (0 f16, 1 bf16) compiled in: one conversion path
+__global__ void __launch_bounds__(128, 4) ln_bwd_fused_kernel(const void* __restrict__ x, long long ldx,
                                                            const void* __restrict__ g, const float* __restrict__ mean,
                                                            const float* __restrict__ rstd, const void* __restrict__ dy,
                                                            long long lddy, const void* __restrict__ dres,
                                                            long long ldres, void* __restrict__ dx, long long lddx,
-                                                           float* __restrict__ ws, int rows, int D, int nsum,
-                                                           int fmt) {
+                                                           float* __restrict__ ws, int rows, int D, int nsum, int) {
+  constexpr int fmt = FMT;
   ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
   extern __shared__ float acc_sh[];  // [4 warps][3 sums][V][4 column pairs][32 lanes] float2
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1137,14 +1140,15 @@ int mpx_layernorm_fwd(int dtype, const void* x, int64_t ldx, const void* gain, c
                                                          reinterpret_cast<uintptr_t>(gain) |
                                                          reinterpret_cast<uintptr_t>(bias)) % 16 == 0);
   const int f = fmt_of(dtype);
+  auto launch = [&](auto k) { return ::mpx::launch_k(k, grid, 256, 0, st, x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f); };
   if (vec && D == 768)
-    MPX_CUDA_CHECK(::mpx::launch_k(ln_fwd_kernel<3>, grid, 256, 0, st, x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f));
+    MPX_CUDA_CHECK(f ? launch(ln_fwd_kernel<3, 1>) : launch(ln_fwd_kernel<3, 0>));
   else if (vec && D == 1024)
-    MPX_CUDA_CHECK(::mpx::launch_k(ln_fwd_kernel<4>, grid, 256, 0, st, x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f));
+    MPX_CUDA_CHECK(f ? launch(ln_fwd_kernel<4, 1>) : launch(ln_fwd_kernel<4, 0>));
   else if (vec && D == 512)
-    MPX_CUDA_CHECK(::mpx::launch_k(ln_fwd_kernel<2>, grid, 256, 0, st, x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f));
+    MPX_CUDA_CHECK(f ? launch(ln_fwd_kernel<2, 1>) : launch(ln_fwd_kernel<2, 0>));
   else
-    MPX_CUDA_CHECK(::mpx::launch_k(ln_fwd_kernel<0>, grid, 256, 0, st, x, ldx, gain, bias, y, ldy, mean, rstd, rows, D, eps, f));
+    MPX_CUDA_CHECK(f ? launch(ln_fwd_kernel<0, 1>) : launch(ln_fwd_kernel<0, 0>));
   MPX_LAUNCH_CHECK("ln_fwd_kernel");
   return 0;
 }
@@ -1224,17 +1228,19 @@ int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, 
     const size_t shb = (size_t)4 * 3 * D * sizeof(float);  // per-warp accumulator slabs
     static std::once_flag attr;
     std::call_once(attr, [] {
-      cudaFuncSetAttribute(ln_bwd_fused_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
-      cudaFuncSetAttribute(ln_bwd_fused_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
-      cudaFuncSetAttribute(ln_bwd_fused_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
+      const void* ks[6] = {(const void*)ln_bwd_fused_kernel<1, 0>, (const void*)ln_bwd_fused_kernel<2, 0>,
+                           (const void*)ln_bwd_fused_kernel<3, 0>, (const void*)ln_bwd_fused_kernel<1, 1>,
+                           (const void*)ln_bwd_fused_kernel<2, 1>, (const void*)ln_bwd_fused_kernel<3, 1>};
+      for (const void* k : ks) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
     });
+    auto launch = [&](auto k) {
+      return ::mpx::launch_k(k, blocks, 128, shb, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx,
+                             workspace, rows, D, nsum, f);
+    };
     switch (D / 256) {
-      case 1: MPX_CUDA_CHECK(::mpx::launch_k(ln_bwd_fused_kernel<1>, blocks, 128, shb, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx,
-                                                               workspace, rows, D, nsum, f)); break;
-      case 2: MPX_CUDA_CHECK(::mpx::launch_k(ln_bwd_fused_kernel<2>, blocks, 128, shb, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx,
-                                                               workspace, rows, D, nsum, f)); break;
-      default: MPX_CUDA_CHECK(::mpx::launch_k(ln_bwd_fused_kernel<3>, blocks, 128, shb, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx,
-                                                                lddx, workspace, rows, D, nsum, f)); break;
+      case 1: MPX_CUDA_CHECK(f ? launch(ln_bwd_fused_kernel<1, 1>) : launch(ln_bwd_fused_kernel<1, 0>)); break;
+      case 2: MPX_CUDA_CHECK(f ? launch(ln_bwd_fused_kernel<2, 1>) : launch(ln_bwd_fused_kernel<2, 0>)); break;
+      default: MPX_CUDA_CHECK(f ? launch(ln_bwd_fused_kernel<3, 1>) : launch(ln_bwd_fused_kernel<3, 0>)); break;
     }
     MPX_LAUNCH_CHECK("ln_bwd_fused_kernel");
     MPX_CUDA_CHECK(::mpx::launch_k(partials_reduce3_kernel, dim3((D + 31) / 32, nsum), 1024, 0, st, workspace, blocks, D, dgain, dbias, dxsum, f));
