@@ -560,6 +560,7 @@ __device__ __forceinline__ int col16(int lane) {
   return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
 }
 
+template <int FMT>  // 0 f16, 1 bf16: one conversion path compiled
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -627,9 +628,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const int n_chunks = (P.N + 15) / 16;
       const int halves = P.N > 128 ? 2 : 1;
       // [128 x 16 n_chunks] = X[128 x 64] Y[keys x 64]^T: keys past N are never computed
-      const uint32_t id_nk = idesc_f16(P.fmt, 128, 16 * n_chunks, 0, 0);
-      const uint32_t id_kv = idesc_f16(P.fmt, 128, 64, 1, 1);   // dV / dK halves: A, B MN-major
-      const uint32_t id_q = idesc_f16(P.fmt, 128, 64, 0, 1);    // dQ: A K-major, B MN-major
+      const uint32_t id_nk = idesc_f16(FMT, 128, 16 * n_chunks, 0, 0);
+      const uint32_t id_kv = idesc_f16(FMT, 128, 64, 1, 1);   // dV / dK halves: A, B MN-major
+      const uint32_t id_q = idesc_f16(FMT, 128, 64, 0, 1);    // dQ: A K-major, B MN-major
       uint32_t gt = 0;  // tiles so far (barrier phases)
       int it = 0;       // items so far
       if (blockIdx.x < P.items) load_item(blockIdx.x);
@@ -714,7 +715,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint4 w1 = *reinterpret_cast<const uint4*>(rowp + (((u0 + 1) ^ sw) << 4));
       const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) unpack2(u[i], P.fmt, pv[2 * i], pv[2 * i + 1]);
+      for (int i = 0; i < 8; ++i) unpack2(u[i], FMT, pv[2 * i], pv[2 * i + 1]);
     };
     constexpr int kMaxC = 16 / kSplit;  // chunks per thread
     static_assert(kSplit == 4, "dQ readout: one chunk per split");
@@ -732,7 +733,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mbar_wait(&bar[2], ph);
         if (warp == 4 && lane == 0 && it == kTraceIt) ATRACE(5 + 8 * t);
         tc_fence_after();
-        softmax_bwd_p<kSplit>(trow, split, r, qd, P.N, P.scale, P.fmt, red, reinterpret_cast<float*>(sdS), sP,
+        softmax_bwd_p<kSplit>(trow, split, r, qd, P.N, P.scale, FMT, red, reinterpret_cast<float*>(sdS), sP,
                               P.stats ? &st : nullptr);
         fence_async_smem();
         tc_fence_before();
@@ -758,9 +759,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            dpk[j][i] = pack2_fmt(__uint_as_float(a[2 * i]), __uint_as_float(a[2 * i + 1]), P.fmt);
+            dpk[j][i] = pack2_fmt(__uint_as_float(a[2 * i]), __uint_as_float(a[2 * i + 1]), FMT);
             float d0, d1;
-            unpack2(dpk[j][i], P.fmt, d0, d1);
+            unpack2(dpk[j][i], FMT, d0, d1);
             tsum2 = __ffma2_rn(make_float2(pv[2 * i], pv[2 * i + 1]), make_float2(d0, d1), tsum2);
           }
         }
@@ -781,10 +782,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             float d0, d1;
-            unpack2(dpk[j][i], P.fmt, d0, d1);
+            unpack2(dpk[j][i], FMT, d0, d1);
             const float2 ds = __fmul2_rn(make_float2(pv[2 * i], pv[2 * i + 1]),
                                          __fadd2_rn(make_float2(d0, d1), f2(-tsum)));
-            pk[i] = pack2_fmt(ds.x, ds.y, P.fmt);
+            pk[i] = pack2_fmt(ds.x, ds.y, FMT);
           }
           store_p_chunk(sdS, c, r, pk);
         }
@@ -806,7 +807,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         uint32_t pk[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * P.scale, __uint_as_float(a[2 * i + 1]) * P.scale, P.fmt);
+          pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * P.scale, __uint_as_float(a[2 * i + 1]) * P.scale, FMT);
         if (qrow < P.N) {
           *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
@@ -815,7 +816,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           float v[16];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            unpack2(pk[i], P.fmt, v[2 * i], v[2 * i + 1]);
+            unpack2(pk[i], FMT, v[2 * i], v[2 * i + 1]);
             if (qrow >= P.N) v[2 * i] = v[2 * i + 1] = 0.f;
           }
           qsum += warp_colsum16(v, lane);
@@ -840,7 +841,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         uint32_t pk[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * mul, __uint_as_float(a[2 * i + 1]) * mul, P.fmt);
+          pk[i] = pack2_fmt(__uint_as_float(a[2 * i]) * mul, __uint_as_float(a[2 * i + 1]) * mul, FMT);
         if (key < P.N) {
           *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
@@ -849,7 +850,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           float v[16];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            unpack2(pk[i], P.fmt, v[2 * i], v[2 * i + 1]);
+            unpack2(pk[i], FMT, v[2 * i], v[2 * i + 1]);
             if (key >= P.N) v[2 * i] = v[2 * i + 1] = 0.f;
           }
           kvsum[c] = warp_colsum16(v, lane);
@@ -1038,12 +1039,14 @@ extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnBwdSmem);
+    err = cudaFuncSetAttribute(attn_bwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnBwdSmem);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(attn_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnBwdSmem);
   });
   if (err != cudaSuccess) return fail((int)err, "cudaFuncSetAttribute(attn_bwd_kernel)");
   P.items = B * H;  // persistent: one CTA per SM walks the (image, head) items
   const unsigned grid = (unsigned)std::min(B * H, current_num_sms());
-  MPX_CUDA_CHECK(::mpx::launch_k(attn_bwd_kernel, grid, kAttnThreads, kAttnBwdSmem, static_cast<cudaStream_t>(stream),
+  MPX_CUDA_CHECK(::mpx::launch_k(fmt ? attn_bwd_kernel<1> : attn_bwd_kernel<0>, grid, kAttnThreads, kAttnBwdSmem, static_cast<cudaStream_t>(stream),
                                  tq, tk, tv, tdo, tp, P));
   MPX_LAUNCH_CHECK("attn_bwd_kernel");
   if (colsum_out) {  // the qkv bias gradient: sum the per-image partials [B][3D]
