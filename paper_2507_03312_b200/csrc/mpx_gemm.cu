@@ -73,6 +73,7 @@ struct GemmParams {
   int m_blocks, n_blocks, k_blocks, kb_per_split;
   long long total_tiles;
   uint32_t idesc;
+  uint32_t idesc2;  // WN variant: the N = 128 second MMA of each K step
   int ab_fmt;  // 0 = f16, 1 = bf16 (also the dtype of bias/residual/aux)
   // epilogue
   void* C;
@@ -164,17 +165,25 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, long long t
 // columns, the leader issues tcgen05.mma.cta_group::2 (M = 256), so each SM
 // streams 2/3 of the bytes per FLOP of the 1-CTA tile.
 // FMT: the A/B (and 16-bit C, bias, residual, aux) format, 0 f16 / 1 bf16,
-// compiled in so the epilogue carries one conversion path
-template <int CG, int XO, int FMT>
+// compiled in so the epilogue carries one conversion path.
+// WN = 1: the wide weight-gradient tile — CTA pair, 256 x 384, MN-major B, one
+// accumulator (384 TMEM columns; the split-K units are one tile each, so there
+// is no next tile to overlap): per K step an N = 256 and an N = 128 MMA share
+// the A tile; each CTA stages B column chunks {2r, 2r+1, 4+r} (64 columns
+// each) so both MMAs' halves land in column order.  Bytes per MAC from L2 are
+// 5/6 of the 256 x 256 tile's, the feed the long wgrad mainloops are bound by.
+template <int CG, int XO, int FMT, int WN = 0>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
                 const __grid_constant__ GemmParams P) {
+  static_assert(!WN || (CG == 2 && XO == XOP_PLAIN), "the wide tile is a CTA-pair plain-epilogue variant");
   using SM = GemmSmem<XO>;
-  constexpr int S = CG == 1 ? SM::kStages1 : SM::kStages2;  // smem ring depth (48 / 32 KB stages)
+  constexpr int BT = (WN ? 384 * kBK * 2 : kBTileBytes) / CG;  // B bytes per stage per CTA
+  // smem ring depth: 48 / 32 KB stages; wide: 40 KB stages in the same 224 KB budget
+  constexpr int S = WN ? (224 - SM::kStageKB) * 1024 / (kATileBytes + BT) : CG == 1 ? SM::kStages1 : SM::kStages2;
   constexpr int kBufPerWarp = SM::kBufPerWarp;
   constexpr int kEpiStage = SM::kEpiStage;
-  constexpr int BT = kBTileBytes / CG;         // B bytes per stage per CTA
   extern __shared__ uint8_t smem_raw[];
   // 1 KB-aligned by indexing the __shared__ array (not via an integer cast), so
   // derived pointers stay in the shared window: STS/LDS, 32-bit addressing
@@ -239,7 +248,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const TileCoord tc = tile_coord(P, t);
         const int b1 = tc.z % P.nb1, b2 = tc.z / P.nb1;
         const int m0 = tc.m_blk * (kBM * CG) + (int)rank * kBM;
-        const int n0 = tc.n_blk * P.BN + (int)rank * bn_cta;
+        const int n0 = tc.n_blk * P.BN + (WN ? 0 : (int)rank * bn_cta);
         const int kb0 = tc.s * P.kb_per_split;
         const int kb1 = min(P.k_blocks, kb0 + P.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -262,7 +271,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             load(a, &tmA, m0, k0, ab1, ab2);
             load(a + 8192, &tmA, m0 + 64, k0, ab1, ab2);
           }
-          if (!P.b_mn) {
+          if (WN) {  // chunks 2r, 2r + 1 (the N = 256 MMA's half) and 4 + r (the N = 128 MMA's)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              load(b + c * 8192, &tmB, n0 + 64 * (c < 2 ? 2 * (int)rank + c : 4 + (int)rank), k0, bb1, bb2);
+          } else if (!P.b_mn) {
             load(b, &tmB, k0, n0, bb1, bb2);
           } else {
             for (int c = 0; c < bn_cta / 64; ++c) load(b + c * 8192, &tmB, n0 + 64 * c, k0, bb1, bb2);
@@ -287,7 +300,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int kb1 = min(P.k_blocks, kb0 + P.kb_per_split);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * 256;
+        const uint32_t d = tmem_base + (WN ? 0u : (uint32_t)acc * 256);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -297,10 +310,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ad = P.a_mn ? sw128_desc(a + k * 2048, 8192, 1024) : sw128_desc(a + k * 32, 16, 1024);
             const uint64_t bd = P.b_mn ? sw128_desc(b + k * 2048, 8192, 1024) : sw128_desc(b + k * 32, 16, 1024);
-            if (CG == 2)
+            if (WN) {
               umma_f16_2sm(d, ad, bd, P.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-            else
+              umma_f16_2sm(d + 256, ad, sw128_desc(b + 2 * 8192 + k * 2048, 8192, 1024), P.idesc2,
+                           (kb > kb0 || k > 0) ? 1u : 0u);
+            } else if (CG == 2) {
+              umma_f16_2sm(d, ad, bd, P.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            } else {
               umma_f16(d, ad, bd, P.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
           }
           // smem slot free (in both CTAs) once these MMAs have read it
           if (CG == 2)
@@ -316,7 +334,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           umma_commit_2sm_mc(&tfull[acc], 3);  // accumulator ready for both epilogues
         else
           umma_commit(&tfull[acc]);
-        acc ^= 1;
+        if (!WN) acc ^= 1;  // (wide: one accumulator, its phase flips every tile)
         if (acc == 0) acc_phase ^= 1;
       }
     }
@@ -344,7 +362,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const bool row_ok = row < P.M;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
+      const uint32_t taddr = tmem_base + (WN ? 0u : (uint32_t)acc * 256) + ((uint32_t)(q * 32) << 16);
 
       // bias / activation / residual on 16 consecutive columns of this row
       auto load8 = [&](const void* base, long long idx, float* o) {
@@ -765,7 +783,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         else
           mbar_arrive(&tempty[acc]);
       }
-      acc ^= 1;
+      if (!WN) acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
     if (P.tma_store && lane == 0) bulk_wait0();
@@ -842,8 +860,11 @@ __global__ void __launch_bounds__(256) splitk_reduce4_kernel(const float* __rest
   const int n4 = N / 4;
   const long long mn = (long long)M * N;
   const long long total = (long long)M * n4;
+  // 32-bit index math when the output fits (every ViT shape): one 32-bit divide per 4 columns
+  const bool small = total < (1ll << 31);
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const int row = (int)(i / n4), c4 = (int)(i - (long long)row * n4);
+    const int row = small ? (int)((unsigned)i / (unsigned)n4) : (int)(i / n4);
+    const int c4 = (int)(i - (long long)row * n4);
     const long long e = (long long)row * N + 4 * c4;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
     int k = 0;
@@ -955,7 +976,10 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   int BN = g->block_n;
   if (BN <= 0) BN = g->N >= kBNMax ? kBNMax : ((g->N + 15) / 16) * 16;
   if (g->b_mn_major) BN = ((BN + 63) / 64) * 64;
-  if (BN > kBNMax || BN % 16) return fail(MPX_EINVAL, "mpx_gemm: bad block_n");
+  const bool wide = BN == 384;  // the wide weight-gradient tile (WN variant)
+  if (wide && (!g->b_mn_major || g->act != ACT_NONE || g->residual || g->aux || g->M < 256))
+    return fail(MPX_EINVAL, "mpx_gemm: block_n 384 is the MN-major-B plain-epilogue pair tile");
+  if ((BN > kBNMax && !wide) || BN % 16) return fail(MPX_EINVAL, "mpx_gemm: bad block_n");
   const int split = g->split_k > 1 ? g->split_k : 1;
   if (split > 1 && (nb1 * nb2 != 1 || !g->workspace)) return fail(MPX_EINVAL, "mpx_gemm: split-K needs batch 1 + workspace");
   if (split > 1 && g->act != ACT_NONE) return fail(MPX_EINVAL, "mpx_gemm: split-K supports no activation");
@@ -968,8 +992,9 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   }
   // CTA pair (M = 256 tiles) for the large problems; single CTA otherwise
   int CG = g->cta_group;
-  const bool pair_ok = (BN == 256 || BN == 128) && (!g->b_mn_major || BN % 128 == 0);
-  if (CG == 0) CG = (pair_ok && g->M >= 512) ? 2 : 1;
+  const bool pair_ok = (BN == 256 || BN == 128 || wide) && (!g->b_mn_major || BN % 128 == 0);
+  if (CG == 0) CG = (pair_ok && (g->M >= 512 || wide)) ? 2 : 1;
+  if (wide && CG != 2) return fail(MPX_EINVAL, "mpx_gemm: block_n 384 needs the CTA pair");
   if (CG != 1 && CG != 2) return fail(MPX_EINVAL, "mpx_gemm: cta_group must be 0, 1 or 2");
   if (CG == 2 && !pair_ok) return fail(MPX_EINVAL, "mpx_gemm: cta_group 2 needs BN 128/256");
 
@@ -1013,7 +1038,8 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   P.k_blocks = (g->K + kBK - 1) / kBK;
   P.kb_per_split = (P.k_blocks + split - 1) / split;
   P.total_tiles = (long long)P.nbatch * split * P.m_blocks * P.n_blocks;
-  P.idesc = ptx::idesc_f16(fmt, kBM * CG, BN, g->a_mn_major, g->b_mn_major);
+  P.idesc = ptx::idesc_f16(fmt, kBM * CG, wide ? 256 : BN, g->a_mn_major, g->b_mn_major);
+  P.idesc2 = ptx::idesc_f16(fmt, kBM * CG, 128, g->a_mn_major, g->b_mn_major);
   P.ab_fmt = fmt;
   P.C = g->C;
   P.ldc = g->ldc;
@@ -1114,13 +1140,17 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
         gemm_kernel<1, XOP_AUX_OUT, 1>, gemm_kernel<1, XOP_PLAIN, 1>},
        {gemm_kernel<2, XOP_NONE, 1>, gemm_kernel<2, XOP_RES_IN, 1>, gemm_kernel<2, XOP_AUX_IN, 1>,
         gemm_kernel<2, XOP_AUX_OUT, 1>, gemm_kernel<2, XOP_PLAIN, 1>}}};
+  static const KernelFn wide_kernels[2] = {gemm_kernel<2, XOP_PLAIN, 0, 1>, gemm_kernel<2, XOP_PLAIN, 1, 1>};
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
-    for (int f = 0; f < 2 && attr_err == cudaSuccess; ++f)
+    for (int f = 0; f < 2 && attr_err == cudaSuccess; ++f) {
       for (int c = 0; c < 2 && attr_err == cudaSuccess; ++c)
         for (int x = 0; x < 5 && attr_err == cudaSuccess; ++x)
           attr_err = cudaFuncSetAttribute(kernels[f][c][x], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+      if (attr_err == cudaSuccess)
+        attr_err = cudaFuncSetAttribute(wide_kernels[f], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+    }
   });
   if (attr_err != cudaSuccess) return fail((int)attr_err, "cudaFuncSetAttribute(gemm_kernel)");
   // fused column sum: in the staged lean epilogues (16-bit C, one batch), else a separate pass
@@ -1133,7 +1163,9 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
                                                            : GemmSmem<XOP_AUX_IN>::kBufPerWarp);
     if (csum_fused) P.csum = g->colsum_ws;
   }
-  const KernelFn kern = kernels[fmt][CG - 1][P.xop];
+  if (wide && P.xop != XOP_PLAIN)
+    return fail(MPX_EINVAL, "mpx_gemm: block_n 384 needs the TMA-store plain epilogue (aligned C / workspace)");
+  const KernelFn kern = wide ? wide_kernels[fmt] : kernels[fmt][CG - 1][P.xop];
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (CG == 1) {
     const long long grid = std::min<long long>(P.total_tiles, current_num_sms());

@@ -4,6 +4,7 @@ memory and streams; every arithmetic op runs in libmpx_b200.so."""
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 
@@ -140,10 +141,10 @@ def auto_cta_group(M: int, N: int, b_mn: bool) -> int:
     return 2 if pair_ok and M >= 512 else 1
 
 
-def auto_split_k(M: int, N: int, K: int, cg: int, sms: int) -> int:
+def auto_split_k(M: int, N: int, K: int, cg: int, sms: int, bn: int = 0) -> int:
     """Split-K factor that fills the machine in whole waves (wgrad: M, N are
     the weight dims, K the token count)."""
-    bn = 256 if N >= 256 else -(-N // 16) * 16
+    bn = bn or (256 if N >= 256 else -(-N // 16) * 16)
     tiles = -(-M // (128 * cg)) * -(-N // bn)
     slots = sms // cg
     kb = -(-K // 64)
@@ -159,15 +160,25 @@ def auto_split_k(M: int, N: int, K: int, cg: int, sms: int) -> int:
     return best_s
 
 
-def linear_wgrad(x, dy, out=None, split_k=None, cta_group=0):
-    """dw[K,N] = x[M,K]^T @ dy[M,N] (reduction over the M tokens)."""
+# the wide 256 x 384 weight-gradient tile (mpx_gemm block_n = 384); MPX_WGRAD_WIDE=0 for A/B
+_WGRAD_WIDE = os.environ.get("MPX_WGRAD_WIDE", "1") != "0"
+
+
+def linear_wgrad(x, dy, out=None, split_k=None, cta_group=0, wide=None):
+    """dw[K,N] = x[M,K]^T @ dy[M,N] (reduction over the M tokens).  Weight
+    shapes with N % 384 == 0 and K >= 256 use the wide CTA-pair tile (one
+    accumulator, 5/6 of the L2 bytes per MAC of the 256 x 256 tile)."""
     M, K = x.shape
     N_ = dy.shape[1]
+    if wide is None:
+        wide = _WGRAD_WIDE and N_ % 384 == 0 and K >= 256 and cta_group in (0, 2)
+    bn = 384 if wide else 0
     if split_k is None:
-        cg = cta_group or auto_cta_group(K, N_, True)
-        split_k = auto_split_k(K, N_, M, cg, _num_sms(x.device))
+        cg = 2 if wide else (cta_group or auto_cta_group(K, N_, True))
+        split_k = auto_split_k(K, N_, M, cg, _num_sms(x.device), bn)
     return gemm(x, dy, M=K, N=N_, K=M, lda=K, ldb=N_, a_mn=True, b_mn=True, out=out,
-                ldc=N_ if out is not None else None, split_k=split_k, cta_group=cta_group)
+                ldc=N_ if out is not None else None, split_k=split_k, cta_group=2 if wide else cta_group,
+                block_n=bn)
 
 
 def attention_stats_numel(B: int, N: int, H: int) -> int:

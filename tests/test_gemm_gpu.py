@@ -201,3 +201,20 @@ def test_fused_colsum(cuda, dt, shape):
     y = VK.gemm(x, w, M=M, N=N, K=K, lda=K, ldb=K, split_k=2, colsum_out=cs)
     want = y.float().sum(0)
     assert torch.allclose(cs.float(), want, rtol=1e-2, atol=1e-2 * want.abs().max().item())
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("shape", [(4096, 768, 2304), (1000, 320, 384), (777, 256, 768), (8192, 3072, 768)])
+def test_wide_wgrad(cuda, dt, shape):
+    """The 256 x 384 weight-gradient tile (block_n 384, one accumulator, B chunks
+    staged {2r, 2r+1, 4+r} per CTA) against fp32 and the 256 x 256 path, with
+    and without split-K, including row counts that are not tile multiples."""
+    T, K, N = shape
+    g = torch.Generator(device=cuda).manual_seed(T + K)
+    x = torch.randn(T, K, device=cuda, generator=g).to(dt)
+    dy = torch.randn(T, N, device=cuda, generator=g).to(dt)
+    want = x.float().t() @ dy.float()
+    for split in (None, 1, 3):
+        w = VK.linear_wgrad(x, dy, split_k=split, wide=True)
+        close(w, want, rel=1e-2)
+    close(VK.linear_wgrad(x, dy, wide=False), want, rel=1e-2)
