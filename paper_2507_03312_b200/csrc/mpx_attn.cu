@@ -675,8 +675,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           mbar_wait(&bar[5], ph);  // dS_t written (dP consumed, P_t no longer read by the softmax warps)
           if (it == kTraceIt) ATRACE(4 + 8 * t);
           tc_fence_after();
-          // dK first (its completion frees Q_t), then dQ: the next tile's Q / dO
-          // loads overlap dQ and the dQ readout
+          // dQ first, so the softmax warps read it out while dK runs; dK's
+          // completion (bar 8: every MMA of the tile) frees Q_t, dS_t and K
+          for (int s = 0; s < n_chunks; ++s)  // dQ = dS K
+            umma_f16(tmem, sw128_desc(ds + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
+                     sw128_desc(k + s * 2048, 8192, 1024), id_q, s > 0);
+          umma_commit(&bar[6]);
           for (int half = 0; half < halves; ++half) {
 #pragma unroll
             for (int s = 0; s < 8; ++s)  // over the 128 queries of the tile: dK += dS^T Q
@@ -684,10 +688,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                        sw128_desc(q + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
           }
           umma_commit(&bar[8]);
-          for (int s = 0; s < n_chunks; ++s)  // dQ = dS K
-            umma_f16(tmem, sw128_desc(ds + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
-                     sw128_desc(k + s * 2048, 8192, 1024), id_q, s > 0);
-          umma_commit(&bar[6]);
           if (t + 1 < T) {  // next tile's Q / dO (/ P) as soon as this tile's MMAs have read them
             mbar_arrive_expect_tx(&bar[1], qtx);
             mbar_wait(&bar[8], ph);
@@ -695,8 +695,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             mbar_wait(&bar[9], ph);  // dV done: dO and P free
             tma_load_4d(sdO, &tmdO, &bar[1], 0, (t + 1) * 128, h, b);
             if (saved) load_p(item, t + 1);
-          } else if (item + (int)gridDim.x < P.items) {  // next item, once every tile has been read
-            mbar_wait(&bar[6], ph);
+          } else if (item + (int)gridDim.x < P.items) {  // next item, once every MMA has read its tiles
+            mbar_wait(&bar[8], ph);
             load_item(item + gridDim.x);
           }
         }
@@ -826,7 +826,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_arrive(&bar[7]);
       if (warp == 4 && lane == 0 && it == kTraceIt) ATRACE(8 + 8 * t);
     }
-    // ---- dV, dK (keys r and 128 + r of this head): 4 (half, which) combos split over the warps
+    // ---- dV, dK (keys r and 128 + r of this head): 4 (half, which) combos split over the warps,
+    // once the last tile's dK MMAs (issued after its dQ) have completed
+    mbar_wait(&bar[8], (gt - 1) & 1);
+    tc_fence_after();
     float kvsum[4] = {0.f, 0.f, 0.f, 0.f};  // per chunk: column col16(lane), this warp's 32 keys
     const int half = split >> 1, which = split & 1;  // kSplit == 4: one combo per split
     {
