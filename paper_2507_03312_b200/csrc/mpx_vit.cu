@@ -1027,6 +1027,29 @@ __global__ void __launch_bounds__(256) transpose16_kernel(const __grid_constant_
   const TransposeJob& J = T.job[j];
   const int t = blockIdx.x - J.tile_begin;
   const int r0 = (t / J.tiles_c) * 64, c0 = (t % J.tiles_c) * 64;
+  // full 64 x 64 tiles with 16-byte aligned rows on both sides: 16-byte loads
+  // (8 columns of a row) and 16-byte stores (8 rows of a column), through a
+  // tile padded to 72 columns (a column's 8 rows fall in 8 distinct banks)
+  if (r0 + 64 <= J.rows && c0 + 64 <= J.cols && ((J.ld_src | J.ld_dst) & 7) == 0 &&
+      ((reinterpret_cast<uintptr_t>(J.src) | reinterpret_cast<uintptr_t>(J.dst)) & 15) == 0) {
+    __shared__ __align__(16) uint16_t tv[64][72];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {  // 512 vectors: row = v / 8, 8-column group = v % 8
+      const int v = threadIdx.x + 256 * k, rr = v >> 3, cg = (v & 7) * 8;
+      *reinterpret_cast<uint4*>(&tv[rr][cg]) =
+          *reinterpret_cast<const uint4*>(J.src + (long long)(r0 + rr) * J.ld_src + c0 + cg);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {  // 512 vectors: dst row = source column v / 8, 8-row group = v % 8
+      const int v = threadIdx.x + 256 * k, cc = v >> 3, rg = (v & 7) * 8;
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) w[e] = (uint32_t)tv[rg + 2 * e][cc] | ((uint32_t)tv[rg + 2 * e + 1][cc] << 16);
+      *reinterpret_cast<uint4*>(J.dst + (long long)(c0 + cc) * J.ld_dst + r0 + rg) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    return;
+  }
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 column pairs x 8 rows per pass
   const bool wide = (J.cols & 1) == 0 && (J.ld_src & 1) == 0 && (reinterpret_cast<uintptr_t>(J.src) & 3) == 0;
 #pragma unroll 4

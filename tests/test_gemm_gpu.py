@@ -218,3 +218,20 @@ def test_wide_wgrad(cuda, dt, shape):
         w = VK.linear_wgrad(x, dy, split_k=split, wide=True)
         close(w, want, rel=1e-2)
     close(VK.linear_wgrad(x, dy, wide=False), want, rel=1e-2)
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+def test_transpose_batch(cuda, dt):
+    """mpx_transpose_batch (the forward's K-major weight copies): full 64 x 64
+    tiles on the 16-byte path, ragged edges, odd widths and padded rows."""
+    g = torch.Generator(device=cuda).manual_seed(5)
+    shapes = [(768, 2304), (3072, 768), (100, 37), (64, 64), (129, 200), (1, 9)]
+    srcs = [torch.randn(r, c, device=cuda, generator=g).to(dt) for r, c in shapes]
+    outs = [torch.empty(c, r, device=cuda, dtype=dt) for r, c in shapes]
+    VK.transpose_batch(srcs, outs)
+    for s_, o in zip(srcs, outs):
+        assert torch.equal(o, s_.t())
+    big = torch.randn(256, 136, device=cuda, generator=g).to(dt)[:, :128]  # ld 136, 16-byte rows
+    out = torch.empty(128, 264, device=cuda, dtype=dt)[:, :256]
+    VK.transpose_batch([big], [out])
+    assert torch.equal(out, big.t())
