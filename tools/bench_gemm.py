@@ -1,5 +1,6 @@
 """Time the K5 tcgen05 GEMM on the ViT-B/16 (bs 256) linear shapes, fwd /
-dgrad / wgrad, against torch.matmul (cuBLAS) on the same operands."""
+dgrad / wgrad, against torch.matmul (cuBLAS) on the same operands (the
+forward as the engine runs it: on the K-major weight copy)."""
 import json
 import sys
 from pathlib import Path
@@ -30,13 +31,15 @@ def main():
     for name, K, N in [("qkv", 768, 2304), ("proj", 768, 768), ("fc1", 768, 3072), ("fc2", 3072, 768)]:
         x = torch.randn(M, K, device="cuda").to(dt)
         w = torch.randn(K, N, device="cuda").to(dt) * 0.03
+        wt = w.t().contiguous()
         dy = torch.randn(M, N, device="cuda").to(dt)
         y = torch.empty(M, N, device="cuda", dtype=dt)
         dx = torch.empty(M, K, device="cuda", dtype=dt)
         dw = torch.empty(K, N, device="cuda", dtype=dt)
         fl = 2.0 * M * N * K
         for kind, ours, ref in [
-            ("fwd", lambda: VK.linear_fwd(x, w, out=y), lambda: torch.matmul(x, w, out=y)),
+            # the engine's forward reads K-major weight copies (linear_fwd_t)
+            ("fwd", lambda: VK.linear_fwd_t(x, wt, out=y), lambda: torch.matmul(x, w, out=y)),
             ("dgrad", lambda: VK.linear_dgrad(dy, w, out=dx), lambda: torch.matmul(dy, w.t(), out=dx)),
             ("wgrad", lambda: VK.linear_wgrad(x, dy, out=dw), lambda: torch.matmul(x.t(), dy, out=dw)),
         ]:
