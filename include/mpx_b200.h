@@ -142,8 +142,9 @@ int mpx_optimizer_step(void* const* h_p, const int32_t* h_p_dtype, float* const*
  * Epilogue (fused, per element, f32): + bias[n]; act GELU (aux receives the
  * rounded pre-activation) or GELU-backward (multiplies by gelu'(aux[m,n]));
  * + residual[m,n]; store as c_dtype (f32/f16/bf16).  bias/residual/aux share
- * ab_dtype.  split_k > 1 (batch 1, no act) reduces through `workspace`
- * (split*M*N f32) with a second deterministic pass. */
+ * ab_dtype; a 16-bit C must have the A/B format (f32 C any).  split_k > 1
+ * (batch 1, no act) reduces through `workspace` (split*M*N f32) with a second
+ * deterministic pass. */
 typedef struct mpx_gemm_desc {
   int ab_dtype; /* MPX_F16 / MPX_BF16 */
   int M, N, K;
@@ -167,7 +168,9 @@ typedef struct mpx_gemm_desc {
                   (whole rows: N <= 256 in one tile), 4 softmax backward: C = P*(alpha*acc -
                   rowsum(P*alpha*acc)) with aux = P (ld_aux >= round_up(N, 16)); aux is
                   addressed with C's batch strides */
-  int block_n; /* 0 = auto */
+  int block_n; /* 0 = auto (<= 256); 384 = the wide weight-gradient tile: CTA pair, 256 x 384,
+                  one accumulator, MN-major B, no act / residual / aux, TMA-store epilogue
+                  (aligned C or workspace) */
   int split_k; /* <= 1: none */
   void* workspace;
   int cta_group; /* 0 = auto, 1 = one CTA per 128-row tile, 2 = CTA pair per 256-row tile */
