@@ -52,7 +52,15 @@ __device__ __forceinline__ void pdl_grid_sync() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// a non-persistent kernel (many waves of blocks) lets its successor launch only
+// from its last wave: the successor's CTAs then fill the SMs its tail frees
+// instead of taking them from its remaining waves
+__device__ __forceinline__ void pdl_wait_only() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 bool pdl_enabled();
+bool pdl_all();       // MPX_PDL_ALL=1: the plain (launch_k) launches use PDL too
 void count_launch();  // every kernel the library launches (mpx_launch_count)
 inline void pdl_attr(cudaLaunchAttribute& a) {
   a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -79,7 +87,7 @@ inline cudaError_t launch_cfg(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                             Args&&... args) {
-  return launch_cfg(false, kern, grid, block, smem, st, std::forward<Args>(args)...);
+  return launch_cfg(pdl_all(), kern, grid, block, smem, st, std::forward<Args>(args)...);
 }
 // PDL launch (the MP-step chain K2 -> K4 -> K3: +0.8 %)
 template <typename... KArgs, typename... Args>

@@ -39,6 +39,10 @@ bool pdl_enabled() {
   static const bool on = !(getenv("MPX_PDL") && getenv("MPX_PDL")[0] == '0');
   return on;
 }
+bool pdl_all() {
+  static const bool on = getenv("MPX_PDL_ALL") && getenv("MPX_PDL_ALL")[0] == '1';
+  return on;
+}
 
 int current_num_sms() {
   int dev = 0;

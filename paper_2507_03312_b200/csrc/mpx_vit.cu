@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const void* __restrict__ x,
                                                      void* __restrict__ y, long long ldy, float* __restrict__ mean,
                                                      float* __restrict__ rstd, int rows, int D, float eps, int) {
   constexpr int fmt = FMT;
-  ::mpx::pdl_grid_sync();  // programmatic dependent launch: inputs are final past here
+  ::mpx::pdl_wait_only();  // programmatic dependent launch: inputs are final past here
   const int lane = threadIdx.x & 31;
   const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -1020,7 +1020,7 @@ struct TransposeBatch {
 };
 
 __global__ void __launch_bounds__(256) transpose16_kernel(const __grid_constant__ TransposeBatch T) {
-  ::mpx::pdl_grid_sync();
+  ::mpx::pdl_wait_only();  // many waves: the successor launches when the last one ends
   __shared__ uint16_t tile[64][66];
   int j = 0;
   while (j + 1 < T.n && (int)blockIdx.x >= T.job[j + 1].tile_begin) ++j;
