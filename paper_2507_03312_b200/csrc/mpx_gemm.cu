@@ -812,13 +812,12 @@ __global__ void __launch_bounds__(1024) colsum_parts_kernel(const float* __restr
   if (c < N) {
     const float* w = parts + c;
     int k = kl;
-    for (; k + 96 < nparts; k += 128) {
-      const float v0 = w[(long long)k * N], v1 = w[(long long)(k + 32) * N], v2 = w[(long long)(k + 64) * N],
-                  v3 = w[(long long)(k + 96) * N];
-      a += v0;
-      a += v1;
-      a += v2;
-      a += v3;
+    for (; k + 224 < nparts; k += 256) {  // 8 partial rows in flight, summed in row order
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = w[(long long)(k + 32 * u) * N];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a += v[u];
     }
     for (; k < nparts; k += 32) a += w[(long long)k * N];
   }

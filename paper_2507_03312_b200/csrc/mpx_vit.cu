@@ -440,13 +440,12 @@ __global__ void __launch_bounds__(1024) partials_reduce3_kernel(const float* __r
   if (c < D) {
     const float* w = ws + (long long)q * nb * D + c;
     int k = kl;
-    for (; k + 96 < nb; k += 128) {
-      const float v0 = w[(long long)k * D], v1 = w[(long long)(k + 32) * D], v2 = w[(long long)(k + 64) * D],
-                  v3 = w[(long long)(k + 96) * D];
-      a += v0;
-      a += v1;
-      a += v2;
-      a += v3;
+    for (; k + 224 < nb; k += 256) {  // 8 partial rows in flight, summed in row order
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = w[(long long)(k + 32 * u) * D];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a += v[u];
     }
     for (; k < nb; k += 32) a += w[(long long)k * D];
   }
