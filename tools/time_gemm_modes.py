@@ -1,6 +1,8 @@
 """Time the fc1-shaped GEMM (M=50432, K=768, N=3072, bf16) in each epilogue
 mode the ViT uses: bare, bias+GELU with aux out, GELU' with aux in (fc2
-dgrad), bias+residual (fc2 forward)."""
+dgrad), bias+residual (fc2 forward) — forward modes on K-major weight copies
+as the engine runs them — and the fc1 weight gradient on the wide 256x384
+tile (K = 50432 tokens, split-K)."""
 import json
 import sys
 from pathlib import Path
@@ -21,11 +23,14 @@ dy = torch.randn(M, K, device="cuda").to(bf)
 w2 = (torch.randn(N, K, device="cuda") * 0.03).to(bf)
 res = torch.randn(M, K, device="cuda").to(bf)
 out_k = torch.empty(M, K, device="cuda", dtype=bf)
+wt, w2t = w.t().contiguous(), w2.t().contiguous()
+dw = torch.empty(K, N, device="cuda", dtype=bf)
 modes = {
-    "bare": lambda: VK.linear_fwd(x, w, out=y),
-    "gelu_aux_out": lambda: VK.linear_fwd(x, w, bias=b, act=VK.ACT_GELU, aux=aux, out=y),
+    "bare": lambda: VK.linear_fwd_t(x, wt, out=y),
+    "gelu_aux_out": lambda: VK.linear_fwd_t(x, wt, bias=b, act=VK.ACT_GELU, aux=aux, out=y),
     "gelu_bwd_aux_in": lambda: VK.linear_dgrad(dy, w2, aux=aux, out=y),
-    "bias_residual": lambda: VK.linear_fwd(y, w2, bias=b[:K], residual=res, out=out_k),
+    "bias_residual": lambda: VK.linear_fwd_t(y, w2t, bias=b[:K], residual=res, out=out_k),
+    "wgrad_wide": lambda: VK.linear_wgrad(x, aux, out=dw),
 }
 only = sys.argv[1:]  # optional subset (for ncu)
 res_ = {}
