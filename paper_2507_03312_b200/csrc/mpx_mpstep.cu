@@ -71,9 +71,19 @@ static int blocks_per_sm(const void* fn) {
   return b;
 }
 
+// streaming grids.  A one-wave grid-stride (persistent) launch streams HBM at
+// ~5.95 TB/s, a grid of a few tiles per block at the 6.55 TB/s copy peak
+// (tools/hbm_streams.cu; K4 at ViT-B size: 5.84 -> 6.36 TB/s with ~3 tiles per
+// block, 12 waves of resident blocks — 1 tile per block is slow again, the
+// per-block setup no longer amortized).  MPX_STREAM_WAVES=k forces k waves.
+static int stream_waves() {
+  static const int w = getenv("MPX_STREAM_WAVES") ? std::max(1, atoi(getenv("MPX_STREAM_WAVES"))) : 0;
+  return w;
+}
 template <class K>
 static int grid_for(K kernel, int64_t n_tiles) {
-  int64_t g = (int64_t)current_num_sms() * blocks_per_sm(reinterpret_cast<const void*>(kernel));
+  const int64_t resident = (int64_t)current_num_sms() * blocks_per_sm(reinterpret_cast<const void*>(kernel));
+  int64_t g = stream_waves() ? resident * stream_waves() : std::max(resident, n_tiles / 3);
   if (n_tiles < g) g = n_tiles;
   return (int)std::max<int64_t>(g, 1);
 }
