@@ -152,16 +152,16 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
 
     cfg, B = VIT_B16, args.vit_batch
     # configs[2] is bf16 on one GPU, configs[3] fp16 data-parallel: auto picks by world size
-    vit_half = args.vit_half or ("bf16" if ws == 1 else "f16")
+    vit_half = args.vit_half or ("bf16" if group is None else "f16")
     half = as_dtype(vit_half)
     tr = ViTTrainer(cfg, B, half=half, lr=1e-3, device=dev, group=group, world_size=ws, seed=0,
-                    zero=args.zero and ws > 1)
+                    zero=args.zero and group is not None)
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)
     images = torch.randn(B, cfg.img, cfg.img, cfg.chans, generator=g, device=dev)
     labels = torch.randint(0, cfg.classes, (B,), generator=g, device=dev).to(torch.int32)
     stream = torch.cuda.current_stream(dev)
-    use_graph = ws == 1 and not args.no_graph
+    use_graph = group is None and not args.no_graph
     from paper_2507_03312_b200 import _native
     lib = _native.load()
     n0 = lib.mpx_launch_count()
@@ -243,7 +243,7 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
                    "parallelism": f"dp{ws}" + ((" ZeRO-1 (per-block NCCL reduce-scatter overlapped with backward, "
                                                 "sharded K2/K4, half all-gather)" if args.zero else
                                                 " (per-block NCCL grad all-reduce overlapped with backward)")
-                                               if ws > 1 else ""),
+                                               if group is not None else ""),
                    "execution": "one CUDA graph per step" if use_graph else "eager stream-ordered launches"},
         "roofline": {"bound": "tensor", "achieved": round(tflops, 1), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(tflops / peak, 4), "flops_per_image": cfg.flops_per_image(),
@@ -270,7 +270,12 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
-    if ws > 1:
+    if ws > 1 or args.dp_path:
+        if args.dp_path and ws == 1:  # validation: the data-parallel code path through NCCL, world size 1
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
     half = as_dtype(args.half)
@@ -412,7 +417,7 @@ def run_gpu(args):
                                "(p32,m,v,p_half) -> K3 adjust",
                    "params": n, "half": args.half, "grad_arena_bytes": grad_bytes,
                    "l2": "working set 2.6 GB >> 126 MB L2: no flush needed",
-                   "parallelism": f"dp{ws} replicas + finite-flag MIN all-reduce" if ws > 1 else "single GPU",
+                   "parallelism": f"dp{ws} replicas + finite-flag MIN all-reduce" if group is not None else "single GPU",
                    "skipped_steps": n_skip},
         "roofline": {"bound": "hbm", "kernel": "optimizer_kernel (K4)", "achieved": round(achieved, 1),
                      "peak": hbm, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / hbm, 4),
@@ -506,6 +511,8 @@ def main():
                     help="ViT section half format (default: bf16 at 1 GPU = configs[2], f16 at N > 1 = configs[3])")
     ap.add_argument("--no-graph", action="store_true", help="ViT section: eager launches instead of a CUDA graph")
     ap.add_argument("--zero", action="store_true", help="ViT section at N > 1: ZeRO-1 sharded optimizer step")
+    ap.add_argument("--dp-path", action="store_true",
+                    help="validation: run the N > 1 code path (NCCL group, eager ViT steps, f16) at world size 1")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -513,6 +520,9 @@ def main():
         run_reference(args)
     else:
         run_gpu(args)
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            dist.destroy_process_group()
 
 
 if __name__ == "__main__":
