@@ -161,7 +161,9 @@ def vit_section(args, dev, ws, rank, group, barrier, max_over_ranks):
     images = torch.randn(B, cfg.img, cfg.img, cfg.chans, generator=g, device=dev)
     labels = torch.randint(0, cfg.classes, (B,), generator=g, device=dev).to(torch.int32)
     stream = torch.cuda.current_stream(dev)
-    use_graph = group is None and not args.no_graph
+    # data parallel: eager by default; --dp-graph captures the step with its NCCL
+    # collectives (tested at world size 1: tests/test_dp_nccl_gpu.py)
+    use_graph = (group is None or args.dp_graph) and not args.no_graph
     from paper_2507_03312_b200 import _native
     lib = _native.load()
     n0 = lib.mpx_launch_count()
@@ -511,6 +513,8 @@ def main():
                     help="ViT section half format (default: bf16 at 1 GPU = configs[2], f16 at N > 1 = configs[3])")
     ap.add_argument("--no-graph", action="store_true", help="ViT section: eager launches instead of a CUDA graph")
     ap.add_argument("--zero", action="store_true", help="ViT section at N > 1: ZeRO-1 sharded optimizer step")
+    ap.add_argument("--dp-graph", action="store_true",
+                    help="ViT section at N > 1: capture the data-parallel step (NCCL collectives included) as a CUDA graph")
     ap.add_argument("--dp-path", action="store_true",
                     help="validation: run the N > 1 code path (NCCL group, eager ViT steps, f16) at world size 1")
     args = ap.parse_args()

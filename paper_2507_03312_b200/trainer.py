@@ -90,8 +90,9 @@ class ViTTrainer:
     # Python/ctypes launches (and their host-side tensor-map encodes).
     def capture(self, images: torch.Tensor, labels: torch.Tensor, warmup: int = 2):
         """Capture step() reading from the given (static) device buffers."""
-        if self.group is not None:
-            raise RuntimeError("graph capture is single-process only (NCCL exchange runs eagerly)")
+        # with a process group the NCCL collectives (bucket all-reduce / reduce-scatter,
+        # flag MIN, ZeRO all-gather) are captured into the graph too; every rank
+        # captures the same sequence, so replays stay matched across ranks
         s = torch.cuda.Stream(self.dev)
         s.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(s):
