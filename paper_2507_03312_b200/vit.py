@@ -98,6 +98,9 @@ class ViTEngine:
         # backward scratch (reused across blocks)
         self.dX = e(M, D)
         self.dXm = e(M, D)
+        # cls pooling: the top block's input gradient is nonzero only on the cls rows,
+        # which the LN_f backward rewrites every step — zeroed once here, not per step
+        self.dX_top = e(M, D).zero_() if c.pool == "cls" else None
         self.dO = e(M, D)
         self.dqkv = e(M, 3 * D)
         self.dP = e(B * H * S, self.ldS) if not self.fused_attn else None
@@ -267,11 +270,10 @@ class ViTEngine:
         self._colsum(self.dlogits, self.ldl, B, c.classes, g["head.b"])
         dfeat = self.dfin if cls else self.dpool
         VK.gemm(self.dlogits, hw, M=B, N=D, K=c.classes, lda=self.ldl, ldb=ldhw, out=dfeat, ldc=D)
-        dX = self.dX
+        dX = self.dX_top if cls else self.dX
         xl = self.x[c.depth]
         top_fc2b = g[f"blocks.{c.depth - 1}.fc2.b"] if c.depth else None
         if cls:
-            dX.zero_()
             # only the cls rows carry gradient: colsum over them = colsum(dX) = the top fc2.b grad
             self._ln_bwd2(xl, S * D, p["ln_f.g"], self.muf, self.rsf, dfeat, D, None, dX, S * D, g["ln_f.g"],
                           g["ln_f.b"], top_fc2b, B)
@@ -311,8 +313,9 @@ class ViTEngine:
             VK.linear_wgrad(self.a[i], dqkv, out=g[q + "qkv.w"])
             VK.linear_dgrad(dqkv, p[q + "qkv.w"], out=self.dA)
             # LN1 (+ residual): dX = LN1'(dA) + dXm; colsum(dX) = fc2.b grad of the block below
-            self._ln_bwd2(self.x[i], D, p[q + "ln1.g"], self.mu1[i], self.rs1[i], self.dA, D, dXm, dX, D,
+            self._ln_bwd2(self.x[i], D, p[q + "ln1.g"], self.mu1[i], self.rs1[i], self.dA, D, dXm, self.dX, D,
                           g[q + "ln1.g"], g[q + "ln1.b"], g[f"blocks.{i - 1}.fc2.b"] if i > 0 else None, M)
+            dX = self.dX
             ready(f"blocks.{i}")
         # embedding: tokens = patches @ Wp + bp + pos (+ cls row)
         self._colsum(dX, S * D, B, S * D, g["pos"])  # sum over the batch
