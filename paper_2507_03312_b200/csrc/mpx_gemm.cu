@@ -47,7 +47,7 @@ constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // TMA warp, MMA warp, epilog
 // the others one buffer per warp (32 KB) and a 6-deep ring (measured: plain
 // epilogue 209 -> 205 us, operand-in variants 250 -> 262 us with one buffer).
 template <int XO> struct GemmSmem {
-  static constexpr int kStageKB = (XO == 1 || XO == 2) ? 64 : 32;  // XOP_RES_IN, XOP_AUX_IN
+  static constexpr int kStageKB = (XO == 1 || XO == 2 || XO == 3) ? 64 : 32;  // RES_IN, AUX_IN, AUX_OUT
   static constexpr int kEpiStage = kStageKB * 1024;
   static constexpr int kStages2 = (192 - kStageKB) / 32 + 1;  // CTA-pair ring depth (32 KB stages)
   static constexpr int kStages1 = (kStages2 * 2) / 3;          // single-CTA ring depth (48 KB stages)
@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         constexpr bool kXin = XO == XOP_RES_IN || XO == XOP_AUX_IN;
         constexpr bool kAuxOut = XO == XOP_AUX_OUT;
         const bool f32out = P.split > 1 || P.c_dtype == MPX_F32;
-        const int GW = (f32out || kAuxOut) ? 32 : 64;
+        const int GW = f32out ? 32 : 64;
         constexpr int cf = FMT;  // 16-bit C has the A/B format (checked on the host)
         const int n_groups = (P.BN + GW - 1) / GW;
         const int my_groups = n_groups > h ? (n_groups - h + kEpiPerQ - 1) / kEpiPerQ : 0;
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 continue;
               }
               const int col = n0 + g * GW + k * 16;
-              if (kAuxOut) {  // aux (rounded pre-activation) at bb, C = GELU(aux) at bb + 2 KB; SW64
+              if (kAuxOut) {  // aux (rounded pre-activation) in the warp's buffer 0, C = GELU(aux) in buffer 1; SW128
                 if (row_ok && col < P.N_store) epi(v, col, min(16, P.N_store - col), v);
                 uint32_t pa[8], pc[8];
 #pragma unroll
@@ -626,13 +626,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   const float2 y = gelu2(make_float2(a, b));  // GELU of the rounded pre-activation
                   pc[i] = pack2_fmt(y.x, y.y, cf);
                 }
-                const int s64 = (lane >> 1) & 3;
-                uint8_t* ra = bb + lane * 64;
-                uint8_t* rc = ra + 2048;
-                *reinterpret_cast<uint4*>(ra + (((2 * k) ^ s64) << 4)) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
-                *reinterpret_cast<uint4*>(ra + (((2 * k + 1) ^ s64) << 4)) = make_uint4(pa[4], pa[5], pa[6], pa[7]);
-                *reinterpret_cast<uint4*>(rc + (((2 * k) ^ s64) << 4)) = make_uint4(pc[0], pc[1], pc[2], pc[3]);
-                *reinterpret_cast<uint4*>(rc + (((2 * k + 1) ^ s64) << 4)) = make_uint4(pc[4], pc[5], pc[6], pc[7]);
+                const int s128 = lane & 7;
+                uint8_t* ra = obuf + lane * 128;
+                uint8_t* rc = ra + 4096;
+                *reinterpret_cast<uint4*>(ra + (((2 * k) ^ s128) << 4)) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+                *reinterpret_cast<uint4*>(ra + (((2 * k + 1) ^ s128) << 4)) = make_uint4(pa[4], pa[5], pa[6], pa[7]);
+                *reinterpret_cast<uint4*>(rc + (((2 * k) ^ s128) << 4)) = make_uint4(pc[0], pc[1], pc[2], pc[3]);
+                *reinterpret_cast<uint4*>(rc + (((2 * k + 1) ^ s128) << 4)) = make_uint4(pc[4], pc[5], pc[6], pc[7]);
                 continue;
               }
               uint8_t* rowp = bb + lane * 128;
@@ -661,8 +661,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (P.split > 1) {
             tma_store_4d(&tmC, bb, n0 + g * GW, row0, tc.s, 0);
           } else if (kAuxOut) {
-            tma_store_4d(&tmX, bb, n0 + g * GW, row0, b1, b2);
-            tma_store_4d(&tmC, bb + 2048, n0 + g * GW, row0, b1, b2);
+            tma_store_4d(&tmX, obuf, n0 + g * GW, row0, b1, b2);
+            tma_store_4d(&tmC, obuf + 4096, n0 + g * GW, row0, b1, b2);
           } else {
             tma_store_4d(&tmC, bb, n0 + g * GW, row0, b1, b2);
           }
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // one proxy fence and one bulk group per tile — the previous tile's
         // stores had a whole tile of MMA time to drain.  Otherwise (f32 / GELU-
         // aux-out groups, > 2 groups) ping-pong the buffers group by group.
-        const bool batched = my_groups <= kBufPerWarp;
+        const bool batched = !kAuxOut && my_groups <= kBufPerWarp;  // GELU-aux-out: both buffers per group
         if (batched) {
           if (lane == 0) {
             bulk_wait_read0();
@@ -698,7 +698,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               eph ^= 1u;
             }
           } else if (!batched) {
-            if (lane == 0) bulk_wait_read<kBufPerWarp - 1>();  // the store that last used this buffer has read it
+            if (lane == 0) {  // the store that last used this buffer (both, for GELU-aux-out) has read it
+              if (kAuxOut)
+                bulk_wait_read0();
+              else
+                bulk_wait_read<kBufPerWarp - 1>();
+            }
             __syncwarp();
           }
           stage_group(g, nch, bb, j == my_groups - 1);
@@ -1103,17 +1108,17 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
         (nb1 == 1 || (g->c_sb1 > 0 && g->c_sb1 % 8 == 0)) && (nb2 == 1 || (g->c_sb2 > 0 && g->c_sb2 % 8 == 0))) {
       const uint64_t s_m = (uint64_t)g->ld_aux * es2;
       P.xop = g->act == ACT_GELU ? XOP_AUX_OUT : XOP_AUX_IN;
-      // GELU out: aux and C leave as 32-column SW64 tiles sharing one staging buffer
+      // GELU out: aux and C leave as 64-column SW128 tiles, one 4 KB staging buffer each
       const bool out2 = P.xop == XOP_AUX_OUT;
-      const CUtensorMapSwizzle swz = out2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+      const CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B;
       rc = make_map(&tx, g->aux, fmt, g->N, g->M, nb1, nb2, s_m, nb1 > 1 ? (uint64_t)g->c_sb1 * es2 : s_m * g->M,
-                    nb2 > 1 ? (uint64_t)g->c_sb2 * es2 : s_m * g->M, out2 ? 32 : 64, 32, swz);
+                    nb2 > 1 ? (uint64_t)g->c_sb2 * es2 : s_m * g->M, 64, 32, swz);
       if (rc) return rc;
       if (out2) {
         const uint64_t s_c = (uint64_t)g->ldc * es2;
         rc = make_map(&tc, g->C, g->c_dtype == MPX_BF16 ? 1 : 0, g->N, g->M, nb1, nb2, s_c,
                       nb1 > 1 ? (uint64_t)g->c_sb1 * es2 : s_c * g->M, nb2 > 1 ? (uint64_t)g->c_sb2 * es2 : s_c * g->M,
-                      32, 32, swz);
+                      64, 32, swz);
         if (rc) return rc;
       }
     } else if (g->act == ACT_NONE && g->residual && al16(g->residual) && g->ldr % 8 == 0 &&
