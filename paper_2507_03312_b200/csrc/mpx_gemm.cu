@@ -73,7 +73,7 @@ struct GemmParams {
   int m_blocks, n_blocks, k_blocks, kb_per_split;
   long long total_tiles;
   uint32_t idesc;
-  uint32_t idesc2;  // WN variant: the N = 128 second MMA of each K step
+  uint32_t idesc2;  // WN variants: the second MMA of each K step (N = 128 at 384 wide, 256 at 512)
   int ab_fmt;  // 0 = f16, 1 = bf16 (also the dtype of bias/residual/aux)
   // epilogue
   void* C;
@@ -166,12 +166,13 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, long long t
 // streams 2/3 of the bytes per FLOP of the 1-CTA tile.
 // FMT: the A/B (and 16-bit C, bias, residual, aux) format, 0 f16 / 1 bf16,
 // compiled in so the epilogue carries one conversion path.
-// WN = 1: the wide weight-gradient tile — CTA pair, 256 x 384, MN-major B, one
-// accumulator (384 TMEM columns; the split-K units are one tile each, so there
-// is no next tile to overlap): per K step an N = 256 and an N = 128 MMA share
-// the A tile; each CTA stages B column chunks {2r, 2r+1, 4+r} (64 columns
-// each) so both MMAs' halves land in column order.  Bytes per MAC from L2 are
-// 5/6 of the 256 x 256 tile's, the feed the long wgrad mainloops are bound by.
+// WN = 1 / 2: the wide weight-gradient tiles — CTA pair, 256 x 384 / 256 x 512,
+// MN-major B, one accumulator (384 / 512 TMEM columns; the split-K units are one
+// tile each, so there is no next tile to overlap): per K step an N = 256 MMA and
+// an N = 128 / 256 one share the A tile; each CTA stages the B column chunks
+// {2r, 2r+1, 4+r} / {2r, 2r+1, 4+2r, 5+2r} (64 columns each) so every MMA's
+// per-CTA halves land in column order.  Bytes per MAC from L2 are 5/6 / 3/4 of
+// the 256 x 256 tile's, the feed the long wgrad mainloops are bound by.
 template <int CG, int XO, int FMT, int WN = 0>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -179,7 +180,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const __grid_constant__ GemmParams P) {
   static_assert(!WN || (CG == 2 && XO == XOP_PLAIN), "the wide tile is a CTA-pair plain-epilogue variant");
   using SM = GemmSmem<XO>;
-  constexpr int BT = (WN ? 384 * kBK * 2 : kBTileBytes) / CG;  // B bytes per stage per CTA
+  constexpr int kBNw = WN == 2 ? 512 : WN == 1 ? 384 : kBNMax;  // tile width
+  constexpr int BT = kBNw * kBK * 2 / CG;  // B bytes per stage per CTA
   // smem ring depth: 48 / 32 KB stages; wide: 40 KB stages in the same 224 KB budget
   constexpr int S = WN ? (224 - SM::kStageKB) * 1024 / (kATileBytes + BT) : CG == 1 ? SM::kStages1 : SM::kStages2;
   constexpr int kBufPerWarp = SM::kBufPerWarp;
@@ -271,10 +273,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             load(a, &tmA, m0, k0, ab1, ab2);
             load(a + 8192, &tmA, m0 + 64, k0, ab1, ab2);
           }
-          if (WN) {  // chunks 2r, 2r + 1 (the N = 256 MMA's half) and 4 + r (the N = 128 MMA's)
+          if (WN) {  // chunks 2r, 2r + 1 (the first N = 256 MMA's half), then 4 + r (384: the N = 128
+                     // MMA's half) or 4 + 2r, 5 + 2r (512: the second N = 256 MMA's half)
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-              load(b + c * 8192, &tmB, n0 + 64 * (c < 2 ? 2 * (int)rank + c : 4 + (int)rank), k0, bb1, bb2);
+            for (int c = 0; c < (WN == 2 ? 4 : 3); ++c) {
+              const int chunk = c < 2 ? 2 * (int)rank + c : (WN == 2 ? 4 + 2 * (int)rank + (c - 2) : 4 + (int)rank);
+              load(b + c * 8192, &tmB, n0 + 64 * chunk, k0, bb1, bb2);
+            }
           } else if (!P.b_mn) {
             load(b, &tmB, k0, n0, bb1, bb2);
           } else {
@@ -980,9 +985,10 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   int BN = g->block_n;
   if (BN <= 0) BN = g->N >= kBNMax ? kBNMax : ((g->N + 15) / 16) * 16;
   if (g->b_mn_major) BN = ((BN + 63) / 64) * 64;
-  const bool wide = BN == 384;  // the wide weight-gradient tile (WN variant)
+  const bool wide = BN == 384 || BN == 512;  // the wide weight-gradient tiles (WN variants)
+  const int wn = BN == 512 ? 2 : BN == 384 ? 1 : 0;
   if (wide && (!g->b_mn_major || g->act != ACT_NONE || g->residual || g->aux || g->M < 256))
-    return fail(MPX_EINVAL, "mpx_gemm: block_n 384 is the MN-major-B plain-epilogue pair tile");
+    return fail(MPX_EINVAL, "mpx_gemm: block_n 384 / 512 is the MN-major-B plain-epilogue pair tile");
   if ((BN > kBNMax && !wide) || BN % 16) return fail(MPX_EINVAL, "mpx_gemm: bad block_n");
   const int split = g->split_k > 1 ? g->split_k : 1;
   if (split > 1 && (nb1 * nb2 != 1 || !g->workspace)) return fail(MPX_EINVAL, "mpx_gemm: split-K needs batch 1 + workspace");
@@ -998,7 +1004,7 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   int CG = g->cta_group;
   const bool pair_ok = (BN == 256 || BN == 128 || wide) && (!g->b_mn_major || BN % 128 == 0);
   if (CG == 0) CG = (pair_ok && (g->M >= 512 || wide)) ? 2 : 1;
-  if (wide && CG != 2) return fail(MPX_EINVAL, "mpx_gemm: block_n 384 needs the CTA pair");
+  if (wide && CG != 2) return fail(MPX_EINVAL, "mpx_gemm: block_n 384 / 512 needs the CTA pair");
   if (CG != 1 && CG != 2) return fail(MPX_EINVAL, "mpx_gemm: cta_group must be 0, 1 or 2");
   if (CG == 2 && !pair_ok) return fail(MPX_EINVAL, "mpx_gemm: cta_group 2 needs BN 128/256");
 
@@ -1043,7 +1049,7 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   P.kb_per_split = (P.k_blocks + split - 1) / split;
   P.total_tiles = (long long)P.nbatch * split * P.m_blocks * P.n_blocks;
   P.idesc = ptx::idesc_f16(fmt, kBM * CG, wide ? 256 : BN, g->a_mn_major, g->b_mn_major);
-  P.idesc2 = ptx::idesc_f16(fmt, kBM * CG, 128, g->a_mn_major, g->b_mn_major);
+  P.idesc2 = ptx::idesc_f16(fmt, kBM * CG, wn == 2 ? 256 : 128, g->a_mn_major, g->b_mn_major);
   P.ab_fmt = fmt;
   P.C = g->C;
   P.ldc = g->ldc;
@@ -1144,7 +1150,8 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
         gemm_kernel<1, XOP_AUX_OUT, 1>, gemm_kernel<1, XOP_PLAIN, 1>},
        {gemm_kernel<2, XOP_NONE, 1>, gemm_kernel<2, XOP_RES_IN, 1>, gemm_kernel<2, XOP_AUX_IN, 1>,
         gemm_kernel<2, XOP_AUX_OUT, 1>, gemm_kernel<2, XOP_PLAIN, 1>}}};
-  static const KernelFn wide_kernels[2] = {gemm_kernel<2, XOP_PLAIN, 0, 1>, gemm_kernel<2, XOP_PLAIN, 1, 1>};
+  static const KernelFn wide_kernels[2][2] = {{gemm_kernel<2, XOP_PLAIN, 0, 1>, gemm_kernel<2, XOP_PLAIN, 1, 1>},
+                                              {gemm_kernel<2, XOP_PLAIN, 0, 2>, gemm_kernel<2, XOP_PLAIN, 1, 2>}};
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [] {
@@ -1152,8 +1159,8 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
       for (int c = 0; c < 2 && attr_err == cudaSuccess; ++c)
         for (int x = 0; x < 5 && attr_err == cudaSuccess; ++x)
           attr_err = cudaFuncSetAttribute(kernels[f][c][x], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-      if (attr_err == cudaSuccess)
-        attr_err = cudaFuncSetAttribute(wide_kernels[f], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+      for (int w = 0; w < 2 && attr_err == cudaSuccess; ++w)
+        attr_err = cudaFuncSetAttribute(wide_kernels[w][f], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
     }
   });
   if (attr_err != cudaSuccess) return fail((int)attr_err, "cudaFuncSetAttribute(gemm_kernel)");
@@ -1168,8 +1175,8 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
     if (csum_fused) P.csum = g->colsum_ws;
   }
   if (wide && P.xop != XOP_PLAIN)
-    return fail(MPX_EINVAL, "mpx_gemm: block_n 384 needs the TMA-store plain epilogue (aligned C / workspace)");
-  const KernelFn kern = wide ? wide_kernels[fmt] : kernels[fmt][CG - 1][P.xop];
+    return fail(MPX_EINVAL, "mpx_gemm: block_n 384 / 512 needs the TMA-store plain epilogue (aligned C / workspace)");
+  const KernelFn kern = wide ? wide_kernels[wn - 1][fmt] : kernels[fmt][CG - 1][P.xop];
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (CG == 1) {
     const long long grid = std::min<long long>(P.total_tiles, current_num_sms());

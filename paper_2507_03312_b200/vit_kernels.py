@@ -160,19 +160,29 @@ def auto_split_k(M: int, N: int, K: int, cg: int, sms: int, bn: int = 0) -> int:
     return best_s
 
 
-# the wide 256 x 384 weight-gradient tile (mpx_gemm block_n = 384); MPX_WGRAD_WIDE=0 for A/B
-_WGRAD_WIDE = os.environ.get("MPX_WGRAD_WIDE", "1") != "0"
+# the wide weight-gradient tiles (mpx_gemm block_n = 512 / 384); MPX_WGRAD_WIDE=0 turns
+# them off, =384 / =512 restricts them to one width (A/B runs)
+_WGRAD_WIDE = os.environ.get("MPX_WGRAD_WIDE", "1")
 
 
 def linear_wgrad(x, dy, out=None, split_k=None, cta_group=0, wide=None):
     """dw[K,N] = x[M,K]^T @ dy[M,N] (reduction over the M tokens).  Weight
-    shapes with N % 384 == 0 and K >= 256 use the wide CTA-pair tile (one
-    accumulator, 5/6 of the L2 bytes per MAC of the 256 x 256 tile)."""
+    shapes with N % 512 (or 384) == 0 and K >= 256 use a wide CTA-pair tile
+    (one accumulator, 3/4 (5/6) of the L2 bytes per MAC of the 256 x 256 tile).
+    wide: None = auto, False = 256 x 256, True = a wide tile (512 when N allows), 384 / 512 = that width."""
     M, K = x.shape
     N_ = dy.shape[1]
-    if wide is None:
-        wide = _WGRAD_WIDE and N_ % 384 == 0 and K >= 256 and cta_group in (0, 2)
-    bn = 384 if wide else 0
+    bn = 0
+    if wide in (384, 512) and wide is not True:  # an explicit width
+        bn = int(wide)
+    elif wide is None or wide:
+        for w in (512, 384):
+            if N_ % w == 0 and K >= 256 and cta_group in (0, 2) and (wide or _WGRAD_WIDE in ("1", str(w))):
+                bn = w
+                break
+        if wide and not bn:
+            bn = 384
+    wide = bn > 0
     if split_k is None:
         cg = 2 if wide else (cta_group or auto_cta_group(K, N_, True))
         split_k = auto_split_k(K, N_, M, cg, _num_sms(x.device), bn)

@@ -204,7 +204,8 @@ def test_fused_colsum(cuda, dt, shape):
 
 
 @pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
-@pytest.mark.parametrize("shape", [(4096, 768, 2304), (1000, 320, 384), (777, 256, 768), (8192, 3072, 768)])
+@pytest.mark.parametrize("shape", [(4096, 768, 2304), (1000, 320, 384), (777, 256, 768), (8192, 3072, 768),
+                                   (4096, 1024, 1024), (1000, 320, 512), (2048, 768, 3072)])
 def test_wide_wgrad(cuda, dt, shape):
     """The 256 x 384 weight-gradient tile (block_n 384, one accumulator, B chunks
     staged {2r, 2r+1, 4+r} per CTA) against fp32 and the 256 x 256 path, with
@@ -214,9 +215,11 @@ def test_wide_wgrad(cuda, dt, shape):
     x = torch.randn(T, K, device=cuda, generator=g).to(dt)
     dy = torch.randn(T, N, device=cuda, generator=g).to(dt)
     want = x.float().t() @ dy.float()
-    for split in (None, 1, 3):
-        w = VK.linear_wgrad(x, dy, split_k=split, wide=True)
-        close(w, want, rel=1e-2)
+    widths = [384] + ([512] if N % 512 == 0 else [])
+    for width in widths:
+        for split in (None, 1, 3):
+            w = VK.linear_wgrad(x, dy, split_k=split, wide=width)
+            close(w, want, rel=1e-2)
     close(VK.linear_wgrad(x, dy, wide=False), want, rel=1e-2)
 
 

@@ -24,12 +24,12 @@ def t(fn, it=20):
 
 
 M = 256 * 197
-tot = {"wide": 0.0, "narrow": 0.0, "cublas": 0.0}
+tot = {"auto": 0.0, "narrow": 0.0, "cublas": 0.0}
 for name, K, N in [("qkv", 768, 2304), ("proj", 768, 768), ("fc1", 768, 3072), ("fc2", 3072, 768)]:
     x = torch.randn(M, K, device="cuda").bfloat16()
     dy = torch.randn(M, N, device="cuda").bfloat16()
     dw = torch.empty(K, N, device="cuda", dtype=torch.bfloat16)
-    row = {"gemm": name + ".wgrad", "wide_us": round(t(lambda: VK.linear_wgrad(x, dy, out=dw, wide=True)), 1),
+    row = {"gemm": name + ".wgrad", "wide384_us": round(t(lambda: VK.linear_wgrad(x, dy, out=dw, wide=384)), 1), "wide512_us": round(t(lambda: VK.linear_wgrad(x, dy, out=dw, wide=512)), 1) if N % 512 == 0 else None, "auto_us": round(t(lambda: VK.linear_wgrad(x, dy, out=dw)), 1),
            "narrow_us": round(t(lambda: VK.linear_wgrad(x, dy, out=dw, wide=False)), 1),
            "cublas_us": round(t(lambda: torch.matmul(x.t(), dy, out=dw)), 1)}
     for k in tot:
