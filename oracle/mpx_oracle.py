@@ -196,8 +196,11 @@ def _balanced_shards(sizes, n_shards):
 class ThreadedStep:
     """In-place (buffer-reusing) variant of mp_step for timing on many cores."""
 
-    def __init__(self, params, m, v, n_threads: int, lr: float, beta1=0.9, beta2=0.999, eps=1e-8):
+    def __init__(self, params, m, v, n_threads: int, lr: float, beta1=0.9, beta2=0.999, eps=1e-8,
+                 half_fmt=None):
         self.params, self.m, self.v = params, m, v
+        self.half_fmt = half_fmt  # also produce the next step's half working copy (cast_tree, precision.py:209)
+        self.half = [None] * len(params)
         self.lr, self.beta1, self.beta2, self.eps = lr, beta1, beta2, eps
         self.shards = _balanced_shards([p.size for p in params], max(1, n_threads))
         self.pool = ThreadPoolExecutor(max_workers=max(1, n_threads))
@@ -221,6 +224,8 @@ class ThreadedStep:
                 pn, m1, v1, _ = adam_leaf(self.params[i], F32, self.m[i], self.v[i], g, t, self.lr,
                                           self.beta1, self.beta2, self.eps)
                 self.params[i], self.m[i], self.v[i] = pn, m1, v1
+                if self.half_fmt:
+                    self.half[i] = quantize(pn, self.half_fmt)
             return True
 
         list(self.pool.map(upd, self.shards))

@@ -984,21 +984,14 @@ extern "C" int mpx_attention_fwd(int dtype, const void* qkv, int B, int N, int H
   P.stats = reinterpret_cast<float2*>(row_stats);
   P.psave = static_cast<uint8_t*>(p_save);
   P.items = B * H;
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
-    const void* ks[4] = {(const void*)attn_fwd_kernel<2, 0>, (const void*)attn_fwd_kernel<2, 1>,
-                         (const void*)attn_fwd_kernel<3, 0>, (const void*)attn_fwd_kernel<3, 1>};
-    for (const void* kf : ks)
-      if (err == cudaSuccess) err = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnSmemF);
-  });
+  const int kc3 = (N + 15) / 16 > 2 * kSplitF;
+  auto kern = kc3 ? (fmt ? attn_fwd_kernel<3, 1> : attn_fwd_kernel<3, 0>)
+                  : (fmt ? attn_fwd_kernel<2, 1> : attn_fwd_kernel<2, 0>);
+  cudaError_t err = ensure_smem_attr((const void*)kern, (int)kAttnSmemF);
   if (err != cudaSuccess) return fail((int)err, "cudaFuncSetAttribute(attn_fwd_kernel)");
   // persistent: one CTA per SM walks the (image, head) items; KC = score chunks
   // per softmax thread (2 up to N = 224)
   const unsigned grid = (unsigned)std::min(B * H, current_num_sms());
-  const int kc3 = (N + 15) / 16 > 2 * kSplitF;
-  auto kern = kc3 ? (fmt ? attn_fwd_kernel<3, 1> : attn_fwd_kernel<3, 0>)
-                  : (fmt ? attn_fwd_kernel<2, 1> : attn_fwd_kernel<2, 0>);
   MPX_CUDA_CHECK(::mpx::launch_k(kern, grid, kAttnThreadsF, kAttnSmemF, static_cast<cudaStream_t>(stream), tq, tk,
                                  tv, tp, P));
   MPX_LAUNCH_CHECK("attn_fwd_kernel");
@@ -1039,13 +1032,7 @@ extern "C" int mpx_attention_bwd(int dtype, const void* qkv, const void* dO, int
   if ((colsum_ws == nullptr) != (colsum_out == nullptr))
     return fail(MPX_EINVAL, "attention_bwd: colsum_ws and colsum_out go together");
   P.csum = colsum_ws;
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
-    err = cudaFuncSetAttribute(attn_bwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnBwdSmem);
-    if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(attn_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAttnBwdSmem);
-  });
+  cudaError_t err = ensure_smem_attr((const void*)(fmt ? attn_bwd_kernel<1> : attn_bwd_kernel<0>), (int)kAttnBwdSmem);
   if (err != cudaSuccess) return fail((int)err, "cudaFuncSetAttribute(attn_bwd_kernel)");
   P.items = B * H;  // persistent: one CTA per SM walks the (image, head) items
   const unsigned grid = (unsigned)std::min(B * H, current_num_sms());

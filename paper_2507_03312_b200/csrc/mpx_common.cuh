@@ -38,6 +38,12 @@ int fail(int code, const std::string& msg);
   } while (0)
 
 int current_num_sms();
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the CURRENT device
+// (the attribute is per device: a process driving two GPUs sets it on each),
+// remembered per (kernel, device) so the call is cheap on every launch
+cudaError_t ensure_smem_attr(const void* fn, int bytes);
+// the whole 32-bit word *d_flag = value, stream-ordered
+cudaError_t set_flag_word(uint32_t* d_flag, uint32_t value, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // Programmatic dependent launch (PDL).  Every kernel starts with

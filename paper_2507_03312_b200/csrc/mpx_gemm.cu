@@ -1152,18 +1152,6 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
         gemm_kernel<2, XOP_AUX_OUT, 1>, gemm_kernel<2, XOP_PLAIN, 1>}}};
   static const KernelFn wide_kernels[2][2] = {{gemm_kernel<2, XOP_PLAIN, 0, 1>, gemm_kernel<2, XOP_PLAIN, 1, 1>},
                                               {gemm_kernel<2, XOP_PLAIN, 0, 2>, gemm_kernel<2, XOP_PLAIN, 1, 2>}};
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [] {
-    for (int f = 0; f < 2 && attr_err == cudaSuccess; ++f) {
-      for (int c = 0; c < 2 && attr_err == cudaSuccess; ++c)
-        for (int x = 0; x < 5 && attr_err == cudaSuccess; ++x)
-          attr_err = cudaFuncSetAttribute(kernels[f][c][x], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-      for (int w = 0; w < 2 && attr_err == cudaSuccess; ++w)
-        attr_err = cudaFuncSetAttribute(wide_kernels[w][f], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-    }
-  });
-  if (attr_err != cudaSuccess) return fail((int)attr_err, "cudaFuncSetAttribute(gemm_kernel)");
   // fused column sum: in the staged lean epilogues (16-bit C, one batch), else a separate pass
   bool csum_fused = false;
   if (g->colsum_out) {
@@ -1177,6 +1165,8 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   if (wide && P.xop != XOP_PLAIN)
     return fail(MPX_EINVAL, "mpx_gemm: block_n 384 / 512 needs the TMA-store plain epilogue (aligned C / workspace)");
   const KernelFn kern = wide ? wide_kernels[wn - 1][fmt] : kernels[fmt][CG - 1][P.xop];
+  const cudaError_t attr_err = ensure_smem_attr((const void*)kern, (int)kGemmSmem);
+  if (attr_err != cudaSuccess) return fail((int)attr_err, "cudaFuncSetAttribute(gemm_kernel)");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (CG == 1) {
     const long long grid = std::min<long long>(P.total_tiles, current_num_sms());

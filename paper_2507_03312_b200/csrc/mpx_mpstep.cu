@@ -16,11 +16,14 @@
 // vector accesses, grid sized to resident-blocks x SM count.
 #include "mpx_common.cuh"
 
+#include <cudaTypedefs.h>
+
 #include <atomic>
 #include <cstdlib>
 
 #include <algorithm>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 namespace mpx {
@@ -42,6 +45,37 @@ bool pdl_enabled() {
 bool pdl_all() {
   static const bool on = getenv("MPX_PDL_ALL") && getenv("MPX_PDL_ALL")[0] == '1';
   return on;
+}
+
+cudaError_t ensure_smem_attr(const void* fn, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::vector<std::tuple<const void*, int, int>> done;  // (kernel, device, bytes)
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& t : done)
+    if (std::get<0>(t) == fn && std::get<1>(t) == dev && std::get<2>(t) >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.emplace_back(fn, dev, bytes);
+  return e;
+}
+
+// the whole 32-bit flag word set on the stream (cuMemsetD32Async): a byte
+// memset would leave whatever the upper bytes held, which a MIN all-reduce or
+// an `== 1` test reads (a freshly allocated flag is uninitialised)
+cudaError_t set_flag_word(uint32_t* d_flag, uint32_t value, cudaStream_t st) {
+  static PFN_cuMemsetD32Async_v3020 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemsetD32Async", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuMemsetD32Async_v3020>(p);
+  });
+  if (!fn) return cudaErrorNotSupported;
+  return fn((CUdeviceptr)d_flag, value, 1, (CUstream)st) == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
 }
 
 int current_num_sms() {
@@ -577,8 +611,7 @@ int mpx_unscale_finite(const void* const* h_g, float* const* h_out, const int64_
   if (!valid_dtype(g_dtype)) return fail(MPX_EINVAL, "mpx_unscale_finite: bad dtype");
   if (!d_flag) return fail(MPX_EINVAL, "mpx_unscale_finite: null flag");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // the flag word is only ever 0 or 1, so setting its low byte to 1 sets it to 1
-  if (reset_flag) MPX_CUDA_CHECK(cudaMemsetAsync(d_flag, 1, 1, st));
+  if (reset_flag) MPX_CUDA_CHECK(set_flag_word(d_flag, 1u, st));
   // fast path: one contiguous half leaf, flag only (the gradient arena)
   if (n_leaves == 1 && (!h_out || !h_out[0]) && g_dtype != MPX_F32 && h_numel[0] > 0 &&
       (reinterpret_cast<uintptr_t>(h_g[0]) % 16) == 0) {

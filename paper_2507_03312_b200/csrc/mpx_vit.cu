@@ -1192,23 +1192,16 @@ int mpx_layernorm_bwd(int dtype, const void* x, int64_t ldx, const void* gain, c
   const int nb = mpx_layernorm_bwd_blocks(rows);
   const size_t sh = (size_t)8 * 2 * D * sizeof(float);
   if (sh > 48 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      MPX_CUDA_CHECK(cudaFuncSetAttribute(ln_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+    MPX_CUDA_CHECK(ensure_smem_attr((const void*)ln_bwd_kernel, 200 * 1024));
   }
   const int f = fmt_of(dtype);
   const bool vec = ldx % 8 == 0 && lddy % 8 == 0 && lddx % 8 == 0 && (!dres || ldres % 8 == 0) &&
                    ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(dx) |
                      reinterpret_cast<uintptr_t>(gain) | reinterpret_cast<uintptr_t>(dres)) % 16 == 0);
   if (sh > 48 * 1024) {
-    static bool attr_vec = false;
-    if (!attr_vec) {
-      MPX_CUDA_CHECK(cudaFuncSetAttribute(ln_bwd_vec_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      MPX_CUDA_CHECK(cudaFuncSetAttribute(ln_bwd_vec_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr_vec = true;
-    }
+    MPX_CUDA_CHECK(ensure_smem_attr((const void*)ln_bwd_vec_kernel<1>, 200 * 1024));
+    MPX_CUDA_CHECK(ensure_smem_attr((const void*)ln_bwd_vec_kernel<3>, 200 * 1024));
+    MPX_CUDA_CHECK(ensure_smem_attr((const void*)ln_bwd_vec_kernel<4>, 200 * 1024));
   }
   if (vec && D == 768)
     MPX_CUDA_CHECK(::mpx::launch_k(ln_bwd_vec_kernel<3>, nb, 256, sh, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx, workspace,
@@ -1252,13 +1245,10 @@ int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, 
     int blocks = current_num_sms() * 4;
     while ((long long)nsum * blocks * D > workspace_floats && blocks > 1) blocks /= 2;
     const size_t shb = (size_t)4 * 3 * D * sizeof(float);  // per-warp accumulator slabs
-    static std::once_flag attr;
-    std::call_once(attr, [] {
-      const void* ks[6] = {(const void*)ln_bwd_fused_kernel<1, 0>, (const void*)ln_bwd_fused_kernel<2, 0>,
-                           (const void*)ln_bwd_fused_kernel<3, 0>, (const void*)ln_bwd_fused_kernel<1, 1>,
-                           (const void*)ln_bwd_fused_kernel<2, 1>, (const void*)ln_bwd_fused_kernel<3, 1>};
-      for (const void* k : ks) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
-    });
+    const void* ks[6] = {(const void*)ln_bwd_fused_kernel<1, 0>, (const void*)ln_bwd_fused_kernel<2, 0>,
+                         (const void*)ln_bwd_fused_kernel<3, 0>, (const void*)ln_bwd_fused_kernel<1, 1>,
+                         (const void*)ln_bwd_fused_kernel<2, 1>, (const void*)ln_bwd_fused_kernel<3, 1>};
+    for (const void* k : ks) MPX_CUDA_CHECK(ensure_smem_attr(k, 48 * 1024));
     auto launch = [&](auto k) {
       return ::mpx::launch_k(k, blocks, 128, shb, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx,
                              workspace, rows, D, nsum, f);

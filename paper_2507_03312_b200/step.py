@@ -56,6 +56,32 @@ class FlatArena:
         return self.buf.data_ptr()
 
 
+class ShardArena:
+    """ZeRO-1 master weights / moments: only this rank's chunk of every
+    gradient bucket, concatenated in bucket order — 1/W of the f32 state per
+    GPU.  `ranges` are (arena offset, length) pairs of the full layout."""
+
+    def __init__(self, ranges, dtype: torch.dtype, device):
+        self.ranges = list(ranges)
+        self.starts, total = [], 0
+        for _, n in self.ranges:
+            self.starts.append(total)
+            total += n
+        self.numel = total
+        self.buf = torch.empty(max(total, 8), dtype=dtype, device=device)
+
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    def chunks(self):
+        """[(full-arena offset, chunk view)] in bucket order."""
+        return [(o, self.buf[s:s + n]) for (o, n), s in zip(self.ranges, self.starts)]
+
+    def fill_from(self, full: torch.Tensor):
+        for (o, n), s in zip(self.ranges, self.starts):
+            self.buf[s:s + n].copy_(full[o:o + n])
+
+
 class FusedMPStep:
     """Master weights, Adam moments, half working copy and half grads of a
     parameter tree, resident in flat device arenas, stepped by K2/K4/K3.
@@ -94,20 +120,35 @@ class FusedMPStep:
         from .dp import bucket_key
         groups = [bucket_key(p) for p in self.paths] if self.zero else None
         align = 8 * self.zero_world
-        self.p32 = FlatArena(leaves, torch.float32, dev, groups, align)
-        self.m = FlatArena(leaves, torch.float32, dev, groups, align)
-        self.v = FlatArena(leaves, torch.float32, dev, groups, align)
+        p32 = FlatArena(leaves, torch.float32, dev, groups, align)
         self.p_half = FlatArena(leaves, self.half.torch, dev, groups, align)
         self.grad = FlatArena(leaves, self.half.torch, dev, groups, align)
-        self.p32.buf.zero_()  # alignment pads stay 0 (finite) in every arena
-        for dst, src in zip(self.p32.views, leaves):
+        self.offsets = p32.offsets
+        p32.buf.zero_()  # alignment pads stay 0 (finite) in every arena
+        for dst, src in zip(p32.views, leaves):
             dst.copy_(src)
-        self.m.buf.zero_()
-        self.v.buf.zero_()
         self.grad.buf.zero_()
         self.n_params = sum(t.numel() for t in leaves)
-        self.numel = self.p32.numel  # padded arena length (pads stay 0 / finite)
-        K.cast_into([self.p32.buf], [self.p_half.buf])
+        self.numel = p32.numel  # padded arena length (pads stay 0 / finite)
+        K.cast_into([p32.buf], [self.p_half.buf])
+        if self.zero:
+            # ZeRO-1: p32 / m / v exist only for this rank's chunks (the optimizer
+            # state is sharded, not just the update); the full layout's offsets
+            # still address the gradient and half arenas
+            from .dp import shard_ranges
+            self.ranges = shard_ranges(self.paths, self.offsets, self.zero_world, self.zero_rank, self.numel)
+            self.p32 = ShardArena(self.ranges, torch.float32, dev)
+            self.p32.fill_from(p32.buf)
+            del p32
+            self.m = ShardArena(self.ranges, torch.float32, dev)
+            self.v = ShardArena(self.ranges, torch.float32, dev)
+        else:
+            self.ranges = [(0, self.numel)]
+            self.p32 = p32
+            self.m = FlatArena(leaves, torch.float32, dev, groups, align)
+            self.v = FlatArena(leaves, torch.float32, dev, groups, align)
+        self.m.buf.zero_()
+        self.v.buf.zero_()
         self.scaling = scaling if scaling is not None else DynamicLossScaling(2.0 ** 15, device=dev)
         self.flag = torch.ones((), dtype=torch.int32, device=dev)
         self.counter = torch.zeros(2, dtype=torch.int64, device=dev)
@@ -122,29 +163,54 @@ class FusedMPStep:
     def _build_tables(self):
         # (offset, length) element ranges this rank steps: the whole arena, or
         # under ZeRO-1 its chunk of every bucket (buckets in arena order)
-        if self.zero:
-            from .dp import shard_ranges
-            self.ranges = shard_ranges(self.paths, self.p32.offsets, self.zero_world, self.zero_rank, self.numel)
-        else:
-            self.ranges = [(0, self.numel)]
         L = len(self.ranges)
         tab = lambda arena, es: (ctypes.c_void_p * L)(*[arena.ptr() + o * es for o, _ in self.ranges])  # noqa: E731
+        if self.zero:  # the f32 state is compact: chunk r starts at its running offset
+            ftab = lambda arena: (ctypes.c_void_p * L)(*[arena.ptr() + s * 4 for s in arena.starts])  # noqa: E731
+        else:
+            ftab = lambda arena: tab(arena, 4)  # noqa: E731
         hs = self.grad.buf.element_size()
         self._L = L
         self._n = (ctypes.c_int64 * L)(*[n for _, n in self.ranges])
         self._g_tab = tab(self.grad, hs)
-        self._p_tab = tab(self.p32, 4)
+        self._p_tab = ftab(self.p32)
         self._pd_tab = (ctypes.c_int32 * L)(*([N.MPX_F32] * L))
-        self._m_tab = tab(self.m, 4)
-        self._v_tab = tab(self.v, 4)
+        self._m_tab = ftab(self.m)
+        self._v_tab = ftab(self.v)
         self._h_tab = tab(self.p_half, hs)
         self._grad_src = self.grad.ptr()
 
     def tree(self, kind: str):
+        if self.zero and kind in ("p32", "m", "v"):
+            raise ValueError(f"tree({kind!r}): under ZeRO-1 this rank holds only its shard of the f32 state; "
+                             "use gather(kind) (a collective) for the full tree, or shard_chunks(kind)")
         arena = {"p32": self.p32, "half": self.p_half, "grad": self.grad, "m": self.m, "v": self.v}[kind]
-        it = iter(arena.views)
+        return self._tree_of(arena.views)
+
+    def _tree_of(self, views):
+        it = iter(views)
         return tree_map(lambda x: next(it) if isinstance(x, torch.Tensor) and x.is_floating_point() else x,
                         self.structure)
+
+    def shard_chunks(self, kind: str):
+        """ZeRO-1: [(full-arena offset, chunk view)] of this rank's p32 / m / v."""
+        if not self.zero:
+            raise ValueError("shard_chunks: not a ZeRO-1 step")
+        return {"p32": self.p32, "m": self.m, "v": self.v}[kind].chunks()
+
+    def gather(self, kind: str):
+        """The full p32 / m / v tree on every rank (ZeRO-1: all-gather of every
+        bucket's chunks over the process group — call it on all ranks)."""
+        if not self.zero or kind not in ("p32", "m", "v"):
+            return self.tree(kind)
+        if self.group is None:
+            raise ValueError("gather: ZeRO-1 without a process group (hand-driven shards) cannot gather")
+        from .dp import zero_bucket_views
+        full = torch.zeros(self.numel, dtype=torch.float32, device=self.device)
+        for (whole, mine), (_, chunk) in zip(zero_bucket_views(full, self.ranges, self.zero_world, self.zero_rank),
+                                             self.shard_chunks(kind)):
+            torch.distributed.all_gather_into_tensor(whole, chunk.contiguous(), group=self.group)
+        return self._tree_of([full[o:o + v.numel()].view(v.shape) for o, v in zip(self.offsets, self.grad.views)])
 
     @property
     def step_count(self) -> int:

@@ -119,6 +119,9 @@ class ViTEngine:
         self.ws_floats = max(8 * 1024 * 1024, 2 * (D * 3 * D), 3 * c.mlp * D, VK.colsum_ws_numel(self.M, c.mlp))
         self.ws = f(self.ws_floats)
         self.lib = _nat.load()
+        # forwards run so far: the activations in the buffers belong to the
+        # latest one (an autograd graph checks it still owns them)
+        self.generation = 0
 
     # ------------------------------------------------------------------
     def activation_bytes(self) -> int:
@@ -231,6 +234,7 @@ class ViTEngine:
                                            c.classes, self.nll.data_ptr(), self.loss.data_ptr(), st), "ce_fwd")
         self._labels = labels
         self._images = images
+        self.generation += 1
         return self.loss
 
     # ------------------------------------------------------------------
@@ -375,12 +379,19 @@ class _ViTLoss(torch.autograd.Function):
     def forward(ctx, engine, paths, images, labels, *leaves):
         p = dict(zip(paths, leaves))
         loss = engine.forward(p, images, labels).clone()
-        ctx.engine, ctx.paths = engine, paths
+        ctx.engine, ctx.paths, ctx.generation = engine, paths, engine.generation
         ctx.save_for_backward(*leaves)
         return loss
 
     @staticmethod
     def backward(ctx, dloss):
+        if ctx.engine.generation != ctx.generation:
+            # the engine keeps ONE set of activation buffers per (config, batch,
+            # dtype): a later forward has overwritten this graph's activations
+            raise RuntimeError(
+                "vit_loss: another forward of the same ViT engine ran between this loss's forward and its "
+                "backward (its activations were overwritten); call backward before the next forward, or "
+                "accumulate gradients over separate transform calls")
         leaves = ctx.saved_tensors
         p = dict(zip(ctx.paths, leaves))
         g = {k: torch.empty_like(v) for k, v in p.items()}

@@ -115,3 +115,22 @@ def test_vit_loss_through_filter_value_and_grad(cuda):
         assert bool(res.grads_finite)
         assert res.grads["blocks.0.qkv.w"].dtype == torch.float32
     assert losses[-1] < losses[0], losses
+
+
+def test_second_forward_before_backward_raises(cuda):
+    """The engine keeps one set of activation buffers: a second forward of the
+    same engine before the first loss's backward must refuse (not silently
+    produce gradients of the wrong activations)."""
+    cfg = ViTConfig(img=32, patch=4, dim=128, depth=1, heads=2, mlp=256, classes=16, pool="cls")
+    f = vit_loss(cfg)
+    p = {k: v.half().requires_grad_() for k, v in init_params(cfg, cuda, seed=0).items()}
+    g = torch.Generator(device=cuda).manual_seed(0)
+    xa, xb = (torch.randn(4, 32, 32, 3, device=cuda, generator=g).half() for _ in range(2))
+    y = torch.randint(0, 16, (4,), device=cuda, generator=g).to(torch.int32)
+    la = f(p, {"x": xa, "y": y})
+    lb = f(p, {"x": xb, "y": y})
+    with pytest.raises(RuntimeError, match="another forward"):
+        (la + lb).backward()
+    lc = f(p, {"x": xa, "y": y})  # forward -> backward in order is fine
+    lc.backward()
+    assert all(v.grad is not None for v in p.values())

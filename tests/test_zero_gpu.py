@@ -18,10 +18,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _leafwise(step, kind):
-    out = {}
-    for path, v in zip(step.paths, {"p32": step.p32, "m": step.m, "v": step.v, "half": step.p_half}[kind].views):
-        out[path] = v
-    return out
+    return dict(zip(step.paths, {"p32": step.p32, "half": step.p_half}[kind].views))
 
 
 def test_zero_shards_equal_replicated(cuda):
@@ -66,17 +63,24 @@ def test_zero_shards_equal_replicated(cuda):
                 hv[1 - r][b][0][o:o + src.numel()].copy_(src)
         torch.cuda.synchronize()
         assert bool(full.grads_finite) == bool(shards[0].grads_finite) == (it != 3)
-    for kind in ("p32", "m", "v"):  # each element from the shard that owns it
-        want = _leafwise(full, kind)
-        got = [_leafwise(s, kind) for s in shards]
+    for kind in ("p32", "m", "v"):  # each rank holds exactly its chunks, equal to the replicated state
+        want = {"p32": full.p32, "m": full.m, "v": full.v}[kind].buf
+        covered = [torch.zeros(v.numel(), dtype=torch.bool, device=cuda) for v in full.grad.views]
         for r, s in enumerate(shards):
-            mask = torch.zeros(s.numel, dtype=torch.bool, device=cuda)
-            for o, n in s.ranges:
-                mask[o:o + n] = True
-            arena = {"p32": s.p32, "m": s.m, "v": s.v}[kind]
-            for p, off, w in zip(s.paths, arena.offsets, want.values()):
-                sel = mask[off:off + w.numel()].view(w.shape)
-                assert torch.equal(got[r][p][sel], w[sel]), (kind, p, r)
+            chunks = s.shard_chunks(kind)
+            assert 2 * sum(c.numel() for _, c in chunks) == s.numel  # 1/W of the f32 state per rank
+            canvas = torch.full((s.numel,), float("nan"), device=cuda)
+            for off, c in chunks:
+                canvas[off:off + c.numel()] = c
+            for i, v in enumerate(full.grad.views):
+                got = canvas[s.offsets[i]:s.offsets[i] + v.numel()]
+                ref = want[full.offsets[i]:full.offsets[i] + v.numel()]
+                mine = ~torch.isnan(got)
+                assert torch.equal(got[mine], ref[mine]), (kind, r, s.paths[i])
+                covered[i] |= mine
+        assert all(bool(c.all()) for c in covered)  # the two shards cover every element
+        with pytest.raises(ValueError):
+            shards[0].tree(kind)
     for s in shards:  # the gathered half copy is whole on both ranks
         for p, h in _leafwise(s, "half").items():
             assert torch.equal(h, _leafwise(full, "half")[p]), p
