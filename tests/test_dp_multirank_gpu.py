@@ -161,6 +161,14 @@ def test_two_ranks_on_one_gpu_match_single_process(cuda):
         n = v.numel()
         d_ref = single["p32"][off:off + n] - p_init[off:off + n]
         d_dp = s0["p32"][off:off + n] - p_init[off:off + n]
+        if path.endswith("qkv.b"):
+            # the key-bias gradient is identically zero in exact arithmetic
+            # (q.(k + b) shifts every score of a query row by the same q.b,
+            # and softmax is shift-invariant): both runs see pure rounding
+            # noise there, which Adam normalises to lr-sized steps of random
+            # sign, so that third of the leaf carries no trajectory to compare
+            d = CFG["dim"]
+            d_ref, d_dp = np.delete(d_ref, np.s_[d:2 * d]), np.delete(d_dp, np.s_[d:2 * d])
         if np.abs(d_ref).max() <= 1e-4:
             continue
         assert np.linalg.norm(d_dp - d_ref) <= 0.25 * np.linalg.norm(d_ref), path
