@@ -43,6 +43,7 @@ enum {
 enum {
   MPX_EINVAL = 10001,     /* bad argument (dtype, size, null pointer) */
   MPX_ETOOMANY = 10002,   /* internal: leaf table overflow */
+  MPX_ENCCL = 10003,      /* NCCL missing or an NCCL call failed */
 };
 
 /* Device-resident dynamic loss-scaling state.  Field-for-field the
@@ -263,6 +264,26 @@ int mpx_rows_add(int dtype, const void* a, const void* b, void* dst, int64_t sb,
 /* dst[b][r][c] = alpha * src[b][c] (mean-pool backward) */
 int mpx_bcast_rows(int dtype, const void* src, int64_t ld_src, void* dst, int64_t ld_dst, int64_t sb_dst, int rows,
                    int B, int D, float alpha, void* stream);
+
+/* ---- data-parallel exchange over NCCL (NVLink / NVSwitch) --------------
+ * For hosts that drive this ABI without torch.distributed (the reference has
+ * no FFI; these replace the replicated-state agreement of PAPER.md:120-121 in
+ * the batch-split DP setup of PAPER.md:282).  libnccl.so.2
+ * is dlopen'ed on first use.  A comm is an ncclComm_t: one made here, or the
+ * host's own. */
+#define MPX_COMM_ID_BYTES 128
+int mpx_comm_unique_id(uint8_t* h_id /* [MPX_COMM_ID_BYTES], rank 0 makes it, all ranks share it */);
+int mpx_comm_init(void** h_comm, int nranks, const uint8_t* h_id, int rank, int device);
+int mpx_comm_destroy(void* comm);
+int mpx_comm_size(void* comm, int* h_nranks);
+/* *d_flag = MIN over ranks of the u32 finite flag K2 wrote: the AND of every
+ * rank's all_finite (tree.py:125-131), so K3 (precision.py:156-173) and the
+ * gated K4 (optim.py:100-113) take one skip / back-off decision everywhere.
+ * In place, stream-ordered, after K2 and before K3/K4. */
+int mpx_allreduce_flag(void* comm, uint32_t* d_flag, void* stream);
+/* in-place SUM of a gradient arena (f32 / f16 / bf16) across ranks: the
+ * scaled half grads, with 1/W folded into the loss cotangent upstream */
+int mpx_allreduce_grads(void* comm, void* d_grads, int64_t numel, int dtype, void* stream);
 
 #ifdef __cplusplus
 }

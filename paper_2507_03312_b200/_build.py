@@ -81,7 +81,7 @@ def build(verbose: bool = False, force: bool = False, defines: tuple = (), out: 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         list(ex.map(run, jobs))
     if force or jobs or _stale(lib, objs):
-        run([cc, *ARCH, "-shared", "-o", str(lib), *map(str, objs)])
+        run([cc, *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-ldl"])
     return lib
 
 

@@ -110,7 +110,15 @@ SIGNATURES = {
     "mpx_rows_add": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P]),
     "mpx_bcast_rows": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.c_int64,
                                       ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_float, _P]),
+    "mpx_comm_unique_id": (ctypes.c_int, [_P]),
+    "mpx_comm_init": (ctypes.c_int, [_PP, ctypes.c_int, _P, ctypes.c_int, ctypes.c_int]),
+    "mpx_comm_destroy": (ctypes.c_int, [_P]),
+    "mpx_comm_size": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int)]),
+    "mpx_allreduce_flag": (ctypes.c_int, [_P, _P, _P]),
+    "mpx_allreduce_grads": (ctypes.c_int, [_P, _P, ctypes.c_int64, ctypes.c_int, _P]),
 }
+
+MPX_COMM_ID_BYTES = 128
 
 _lib = None
 _lock = threading.Lock()

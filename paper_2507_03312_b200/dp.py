@@ -132,3 +132,77 @@ def allreduce_flag_min(flag: torch.Tensor, group=None):
 def env_world():
     return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(
         os.environ.get("LOCAL_RANK", "0"))
+
+
+class NativeComm:
+    """An NCCL communicator owned by libmpx_b200.so (mpx_comm_* in
+    include/mpx_b200.h) — the exchange a host without torch.distributed
+    drives: `allreduce_flag` (MIN = AND of the finite flags) and
+    `allreduce_grads` (SUM of the scaled half gradients).  Rank 0 makes the
+    id with `unique_id()` and ships the 128 bytes to every rank out of band."""
+
+    def __init__(self, nranks: int, uid: bytes, rank: int, device: int):
+        import ctypes
+
+        from . import _native as N
+
+        if len(uid) != N.MPX_COMM_ID_BYTES:
+            raise ValueError(f"NCCL unique id must be {N.MPX_COMM_ID_BYTES} bytes")
+        self._lib = N.load()
+        buf = ctypes.create_string_buffer(bytes(uid), N.MPX_COMM_ID_BYTES)
+        h = ctypes.c_void_p()
+        N.check(self._lib.mpx_comm_init(ctypes.byref(h), nranks, buf, rank, device), "mpx_comm_init")
+        self.handle, self.rank, self.device = h.value, rank, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+
+        from . import _native as N
+
+        buf = ctypes.create_string_buffer(N.MPX_COMM_ID_BYTES)
+        N.check(N.load().mpx_comm_unique_id(buf), "mpx_comm_unique_id")
+        return buf.raw
+
+    @property
+    def size(self) -> int:
+        import ctypes
+
+        from . import _native as N
+
+        n = ctypes.c_int()
+        N.check(self._lib.mpx_comm_size(self.handle, ctypes.byref(n)), "mpx_comm_size")
+        return n.value
+
+    def allreduce_flag(self, flag: torch.Tensor, stream=None):
+        from . import _native as N
+        from .kernels import stream_handle
+
+        if flag.dtype not in (torch.int32, torch.uint32) or flag.numel() != 1 or not flag.is_cuda:
+            raise TypeError("allreduce_flag: a 1-element 32-bit CUDA flag")
+        st = stream if stream is not None else stream_handle(flag.device)
+        N.check(self._lib.mpx_allreduce_flag(self.handle, flag.data_ptr(), st), "mpx_allreduce_flag")
+
+    def allreduce_grads(self, grads: torch.Tensor, stream=None):
+        from . import _native as N
+        from .kernels import stream_handle
+
+        code = {torch.float32: N.MPX_F32, torch.float16: N.MPX_F16, torch.bfloat16: N.MPX_BF16}.get(grads.dtype)
+        if code is None or not grads.is_cuda or not grads.is_contiguous():
+            raise TypeError("allreduce_grads: a contiguous f32/f16/bf16 CUDA arena")
+        st = stream if stream is not None else stream_handle(grads.device)
+        N.check(self._lib.mpx_allreduce_grads(self.handle, grads.data_ptr(), grads.numel(), code, st),
+                "mpx_allreduce_grads")
+
+    def close(self):
+        if self.handle:
+            from . import _native as N
+
+            N.check(self._lib.mpx_comm_destroy(self.handle), "mpx_comm_destroy")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass

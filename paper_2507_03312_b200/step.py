@@ -93,7 +93,14 @@ class FusedMPStep:
     def __init__(self, params, lr: float, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
                  weight_decay: float = 0.0, half_dtype=F16, scaling: DynamicLossScaling | None = None,
                  process_group=None, zero: bool = False, zero_world: int | None = None,
-                 zero_rank: int | None = None):
+                 zero_rank: int | None = None, comm=None):
+        """`comm` (a dp.NativeComm): the exchange through the library's own
+        NCCL entry points instead of torch.distributed — step() sums the half
+        grad arena over the ranks (mpx_allreduce_grads) before K2 and ANDs the
+        finite flag (mpx_allreduce_flag) after it."""
+        if comm is not None and (process_group is not None or zero):
+            raise ValueError("comm= is the torch-free replicated exchange: not with process_group / zero")
+        self.comm = comm
         self.structure = params
         fl = float_leaves(params)
         if not fl:
@@ -231,8 +238,14 @@ class FusedMPStep:
         d_scale = self.scaling.state.data_ptr()
         code = self.half.code
         L = self._L
+        if self.comm is not None:  # SUM of the scaled half grads over the ranks (1/W is in the loss cotangent)
+            base = grad_ptr if grad_ptr is not None else self.grad.ptr()
+            N.check(lib.mpx_allreduce_grads(self.comm.handle, base, self.grad.buf.numel(), code, st),
+                    "mpx_allreduce_grads")
         N.check(lib.mpx_unscale_finite(N.as_pp(g), None, self._n, L, code, 1.0, d_scale, self.flag.data_ptr(), 1,
                                        st), "mpx_unscale_finite")
+        if self.comm is not None:
+            N.check(lib.mpx_allreduce_flag(self.comm.handle, self.flag.data_ptr(), st), "mpx_allreduce_flag")
         if self.group is not None:  # AND over ranks (mandatory under ZeRO-1: shards see different grads)
             torch.distributed.all_reduce(self.flag, op=torch.distributed.ReduceOp.MIN, group=self.group)
         N.check(lib.mpx_optimizer_step(N.as_pp(self._p_tab), self._pd_tab, N.as_pp(self._m_tab),
