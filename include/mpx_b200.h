@@ -265,6 +265,64 @@ int mpx_rows_add(int dtype, const void* a, const void* b, void* dst, int64_t sb,
 int mpx_bcast_rows(int dtype, const void* src, int64_t ld_src, void* dst, int64_t ld_dst, int64_t sb_dst, int rows,
                    int B, int D, float alpha, void* stream);
 
+/* ---- the reference's generic tensor operators (mpsim.tensors, the `T`
+ * namespace of its models: tensors.py:220-555) -------------------------------
+ * Each evaluates in f32 and rounds its result once onto the output grid
+ * (quantize_array, dtypes.py:100-123); accumulations are the reference's
+ * stepwise ones (_stepwise_sum, tensors.py:327-338: re-rounded to the op dtype
+ * after every addition, in index order).  Not used by the ViT engine, whose
+ * hot ops are the fused kernels above. */
+enum {
+  MPX_EW_COPY = 0, /* cast / strided copy (T.cast, transpose / reshape materialisation) */
+  MPX_EW_ADD = 1, MPX_EW_SUB = 2, MPX_EW_MUL = 3, MPX_EW_DIV = 4, /* tensors.py:255-268 */
+  MPX_EW_NEG = 5, MPX_EW_EXP = 6, MPX_EW_LOG = 7, MPX_EW_SQRT = 8, MPX_EW_RELU = 9,
+  MPX_EW_GELU = 10,     /* tensors.py:271-292, _gelu_kernel :196-200 */
+  MPX_EW_GELU_BWD = 11, /* a = cotangent, b = input: a * quantize(gelu'(b), grad_dtype), autodiff.py:173-185 */
+  MPX_EW_RELU_BWD = 12, /* a * (b > 0), autodiff.py:167-170 */
+};
+enum { MPX_RED_SUM = 0, MPX_RED_MEAN = 1, MPX_RED_MAX = 2 };
+/* out (contiguous, `shape`) = op(a, b) with per-operand element strides
+ * (0 = broadcast, tensors.py:220-241 numpy broadcasting).  b == NULL for a
+ * binary op uses the weak scalar f32(scalar) (tensors.py:235-236), on the
+ * left when scalar_side != 0 (rsub / rtruediv). ndim <= 8. */
+int mpx_ew(int op, int ndim, const int64_t* h_shape, void* out, int out_dtype, const void* a, int a_dtype,
+           const int64_t* h_a_strides, const void* b, int b_dtype, const int64_t* h_b_strides, double scalar,
+           int scalar_side, int grad_dtype, void* stream);
+/* T.reduce (tensors.py:353-384) over the middle axis of a contiguous
+ * (outer, n, inner) view, one sequential stepwise accumulation per output */
+int mpx_reduce(int op, const void* a, int dtype, int64_t outer, int64_t n, int64_t inner, void* out, int out_dtype,
+               void* stream);
+/* _bw_max (autodiff.py:223-230): the cotangent c split equally among ties of
+ * the max m; out has a's (outer, n, inner) shape and c's dtype */
+int mpx_reduce_max_bwd(const void* a, int dtype, const void* m, const void* c, int c_dtype, int64_t outer, int64_t n,
+                       int64_t inner, void* out, void* stream);
+/* T.softmax along the middle axis (tensors.py:431-446) and _bw_softmax
+ * (autodiff.py:233-240) */
+int mpx_softmax_axis(const void* a, int dtype, int64_t outer, int64_t n, int64_t inner, void* out, void* stream);
+int mpx_softmax_axis_bwd(const void* y, const void* c, int dtype, int64_t outer, int64_t n, int64_t inner, void* out,
+                         void* stream);
+/* T.layernorm over the last axis in the promoted dtype (tensors.py:459-491);
+ * backward (autodiff.py:243-262): dx, and dgx = c * xhat per element (the
+ * caller sums it over the leading axes for dgain, as the reference does) */
+int mpx_layernorm_ref(const void* x, int x_dtype, const void* gain, int g_dtype, const void* bias, int b_dtype,
+                      int64_t rows, int64_t n, int dtype, void* out, void* stream);
+int mpx_layernorm_ref_bwd(const void* x, int x_dtype, const void* gain, int g_dtype, const void* c, int64_t rows,
+                          int64_t n, int dtype, void* dx, void* dgx, void* stream);
+/* T.cross_entropy (tensors.py:494-522): per-row nll in the logits' dtype
+ * (the mean is mpx_reduce MEAN), and _bw_cross_entropy (autodiff.py:265-276)
+ * with the 0-d cotangent cot */
+int mpx_xent_rows(const void* logits, int dtype, const int32_t* labels, int64_t B, int64_t C, void* nll,
+                  void* stream);
+int mpx_xent_bwd(const void* logits, int dtype, const int32_t* labels, int64_t B, int64_t C, const void* cot,
+                 int cot_dtype, void* out, void* stream);
+/* T.matmul (tensors.py:387-422) on CUDA cores for operands the tcgen05 GEMM
+ * cannot address (f32, mixed formats, unaligned strides): arbitrary element
+ * strides {sam, sak, sbk, sbn, scm, scn}, <= 4 broadcast batch dims; products
+ * and partial sums in f32, in k order (bit-exact to the reference for f32) */
+int mpx_matmul_simt(const void* a, int a_dtype, const void* b, int b_dtype, void* c, int c_dtype, int64_t M,
+                    int64_t N, int64_t K, const int64_t* h_strides, int nbatch_dims, const int64_t* h_bshape,
+                    const int64_t* h_sa_b, const int64_t* h_sb_b, const int64_t* h_sc_b, void* stream);
+
 /* ---- data-parallel exchange over NCCL (NVLink / NVSwitch) --------------
  * For hosts that drive this ABI without torch.distributed (the reference has
  * no FFI; these replace the replicated-state agreement of PAPER.md:120-121 in

@@ -110,6 +110,24 @@ SIGNATURES = {
     "mpx_rows_add": (ctypes.c_int, [ctypes.c_int, _P, _P, _P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P]),
     "mpx_bcast_rows": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int64, _P, ctypes.c_int64, ctypes.c_int64,
                                       ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_float, _P]),
+    "mpx_ew": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64P, _P, ctypes.c_int, _P, ctypes.c_int, _I64P, _P,
+                              ctypes.c_int, _I64P, ctypes.c_double, ctypes.c_int, ctypes.c_int, _P]),
+    "mpx_reduce": (ctypes.c_int, [ctypes.c_int, _P, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P,
+                                  ctypes.c_int, _P]),
+    "mpx_reduce_max_bwd": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                          ctypes.c_int64, _P, _P]),
+    "mpx_softmax_axis": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P, _P]),
+    "mpx_softmax_axis_bwd": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _P,
+                                            _P]),
+    "mpx_layernorm_ref": (ctypes.c_int, [_P, ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int, ctypes.c_int64,
+                                         ctypes.c_int64, ctypes.c_int, _P, _P]),
+    "mpx_layernorm_ref_bwd": (ctypes.c_int, [_P, ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int64, ctypes.c_int64,
+                                             ctypes.c_int, _P, _P, _P]),
+    "mpx_xent_rows": (ctypes.c_int, [_P, ctypes.c_int, _P, ctypes.c_int64, ctypes.c_int64, _P, _P]),
+    "mpx_xent_bwd": (ctypes.c_int, [_P, ctypes.c_int, _P, ctypes.c_int64, ctypes.c_int64, _P, ctypes.c_int, _P, _P]),
+    "mpx_matmul_simt": (ctypes.c_int, [_P, ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int, ctypes.c_int64,
+                                       ctypes.c_int64, ctypes.c_int64, _I64P, ctypes.c_int, _I64P, _I64P, _I64P, _I64P,
+                                       _P]),
     "mpx_comm_unique_id": (ctypes.c_int, [_P]),
     "mpx_comm_init": (ctypes.c_int, [_PP, ctypes.c_int, _P, ctypes.c_int, ctypes.c_int]),
     "mpx_comm_destroy": (ctypes.c_int, [_P]),
@@ -119,6 +137,9 @@ SIGNATURES = {
 }
 
 MPX_COMM_ID_BYTES = 128
+(MPX_EW_COPY, MPX_EW_ADD, MPX_EW_SUB, MPX_EW_MUL, MPX_EW_DIV, MPX_EW_NEG, MPX_EW_EXP, MPX_EW_LOG, MPX_EW_SQRT,
+ MPX_EW_RELU, MPX_EW_GELU, MPX_EW_GELU_BWD, MPX_EW_RELU_BWD) = range(13)
+MPX_RED_SUM, MPX_RED_MEAN, MPX_RED_MAX = 0, 1, 2
 
 _lib = None
 _lock = threading.Lock()

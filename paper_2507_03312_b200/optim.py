@@ -22,7 +22,7 @@ import torch
 
 from . import kernels as K
 from .dtypes import is_float_leaf
-from .precision import DeviceBool, ScaledGrads
+from .precision import DeviceBool, ScaledGrads, _keep_type
 from .tree import TreeError, float_leaves, tree_leaves, tree_map, tree_zip_map
 
 
@@ -159,7 +159,7 @@ def compute_updates(state: OptimizerState, grads):
         m2 = v2 = None
     K.optimizer_step(gs, gs, m2, v2, mode=mode, hp=_hp(state), counter=counter, bc_table=_bc(state, dev),
                      scale=scale, d_scale=d_scale, upd_out=upd)
-    umap = {id(g): u for g, u in zip(gs, upd)}
+    umap = {id(g): _keep_type(u, g) for g, u in zip(gs, upd)}
     updates = tree_map(lambda g: umap.get(id(g)) if is_float_leaf(g) else None, tree)
     if mode == 0:
         mmap = {id(r[2]): x for r, x in zip(rows, m2)}
@@ -214,7 +214,7 @@ def optimizer_update(model, state: OptimizerState, grads, grads_finite, *, donat
                      scale=scale, d_scale=d_scale, flag=flag, half_out=halves)
     if donate:
         return model, state
-    pmap = {id(p): q for p, q in zip(params, new_p)}
+    pmap = {id(p): _keep_type(q, p) for p, q in zip(params, new_p)}
     new_model = tree_map(lambda x: pmap.get(id(x), x), model)
     new_mu = new_nu = None
     if mode == 0:

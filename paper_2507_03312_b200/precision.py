@@ -67,7 +67,7 @@ class _CastLeaves(torch.autograd.Function):
         dst = {0: torch.float32, 1: torch.float16, 2: torch.bfloat16}[dst_code]
         outs = [torch.empty(t.shape, dtype=dst, device=t.device) for t in leaves]
         K.cast_into(leaves, outs)
-        return tuple(outs)
+        return tuple(_keep_type(o, t) for o, t in zip(outs, leaves))
 
     @staticmethod
     def backward(ctx, *grads):
@@ -90,7 +90,14 @@ def _cast_tensor_leaves(leaves: list[torch.Tensor], d: DType) -> list[torch.Tens
         return []
     if torch.is_grad_enabled() and any(t.requires_grad for t in leaves):
         return list(_CastLeaves.apply(d.code, *leaves))
-    return K.cast_leaves(leaves, d)
+    return [_keep_type(o, t) for o, t in zip(K.cast_leaves(leaves, d), leaves)]
+
+
+def _keep_type(out: torch.Tensor, src: torch.Tensor) -> torch.Tensor:
+    """A result stays a tensors.Tensor (the reference's operator sugar) when its source was one."""
+    from .tensors import Tensor
+
+    return out.as_subclass(Tensor) if isinstance(src, Tensor) and not isinstance(out, Tensor) else out
 
 
 def cast_tree(t, dtype):
@@ -180,13 +187,13 @@ def _scale_tree(t, scale: float = 1.0, d_scale: torch.Tensor | None = None):
     leaves = list({id(x): x for x in _float_leaf_positions(t)}.values())
     outs = [torch.empty_like(x, memory_format=torch.contiguous_format) for x in leaves]
     K.cast_into(leaves, outs, scale, d_scale)
-    return _substitute(t, dict(zip(map(id, leaves), outs)))
+    return _substitute(t, {id(x): _keep_type(o, x) for x, o in zip(leaves, outs)})
 
 
 def _unscale_tree(t, scale: float = 1.0, d_scale: torch.Tensor | None = None):
     leaves = list({id(x): x for x in _float_leaf_positions(t)}.values())
     outs, flag = K.unscale_finite(leaves, scale, d_scale, write_f32=True)
-    return _substitute(t, dict(zip(map(id, leaves), outs))), flag
+    return _substitute(t, {id(x): _keep_type(o, x) for x, o in zip(leaves, outs)}), flag
 
 
 class LossScaling(NamedTuple):

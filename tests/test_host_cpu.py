@@ -169,3 +169,45 @@ def test_package_has_no_oracle_imports():
     pkg = ROOT / "paper_2507_03312_b200"
     for f in pkg.rglob("*.py"):
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\S+)", f.read_text(), flags=re.M), f
+
+
+# the reference's public surface, pkg/src/mpsim/__init__.py:10-30 (Tape /
+# TapeEntry are the reference's own autodiff engine: torch.autograd replaces
+# it)
+REFERENCE_NAMES = [
+    "grad", "value_and_grad", "BF16", "DType", "F16", "F32", "I32", "Scalar", "promote", "promote_with_scalar",
+    "quantize", "quantize_array", "OptimizerState", "adam_init", "compute_updates", "optimizer_update", "sgd_init",
+    "GradResult", "LossScaling", "cast_function", "cast_to_bfloat16", "cast_to_float16", "cast_to_float32",
+    "cast_to_half_precision", "cast_tree", "filter_grad", "filter_value_and_grad", "force_full_precision",
+    "get_half_precision", "half_precision", "set_half_precision", "Tensor", "bytes_of", "cross_entropy",
+    "elementwise", "layernorm", "matmul", "reduce", "softmax", "tensor", "TreeError", "all_finite", "float_leaves",
+    "format_tree", "tree_leaves", "tree_map", "tree_structure", "tree_zip_map",
+]
+# mpsim.tensors (the `T` namespace the reference's models use, tensors.py:104-555)
+REFERENCE_T_NAMES = ["Tensor", "tensor", "zeros", "zeros_like", "ones", "bytes_of", "add", "sub", "mul", "div", "neg",
+                     "exp", "log", "sqrt", "relu", "gelu", "elementwise", "reduce", "matmul", "softmax", "layernorm",
+                     "cross_entropy", "cast", "reshape", "transpose"]
+
+
+def test_drop_in_names_exported():
+    import paper_2507_03312_b200 as mpx
+    from paper_2507_03312_b200 import tensors as T
+
+    missing = [n for n in REFERENCE_NAMES if not hasattr(mpx, n)]
+    assert not missing, missing
+    missing = [n for n in REFERENCE_T_NAMES if not hasattr(T, n)]
+    assert not missing, missing
+    assert issubclass(mpx.Tensor, __import__("torch").Tensor)
+    assert mpx.DynamicLossScaling is not None  # the paper's name for LossScaling
+
+
+def test_drop_in_ops_refuse_cpu_tensors():
+    import torch
+
+    from paper_2507_03312_b200 import tensors as T
+
+    x = torch.ones(2, 2).as_subclass(T.Tensor)
+    with pytest.raises(Exception):
+        T.add(x, x)
+    with pytest.raises(Exception):
+        x @ x
