@@ -86,7 +86,7 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.proc = None
         self.gpu = gpu_index
-        self.path = ROOT / "gpurun_out" / f".clocks_{os.getpid()}.csv"
+        self.path = ROOT / "gpurun_out" / f".clocks_{os.getpid()}_{id(self)}.csv"  # nested samplers
 
     def __enter__(self):
         try:
@@ -491,13 +491,15 @@ def vit_section(args, cfg, B, half_name, dev, ws, rank, group, barrier, max_over
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        loss = step()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    with ClockSampler(dev.index or 0) as clocks:  # this section's own clocks (power cap under GEMM load)
+        e0.record(stream)
+        for _ in range(steps):
+            loss = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
+    clk = clocks.summary()
     final_loss = float(loss.item())
     finite = bool(tr.grads_finite)
     # end to end: f32 images + labels from pinned host memory every step
@@ -544,7 +546,7 @@ def vit_section(args, cfg, B, half_name, dev, ws, rank, group, barrier, max_over
     out = {
         "metric": f"{name} mixed-precision train images/sec", "value": round(ws * B * steps / (ms * 1e-3), 1),
         "unit": "img/s", "ms_per_step": round(ms / steps, 3), "steps": steps, "warmup": warmup,
-        "gpu_launches": int(per_step * steps), "kernels_per_step": int(per_step),
+        "gpu_launches": int(per_step * steps), "kernels_per_step": int(per_step), "clocks": clk,
         "config": {"model": f"{name} 224x224 ({cfg.n_params() / 1e6:.1f}M params, cls token, 1000 classes)",
                    "per_gpu_batch": B, "global_batch": B * ws, "half": half_name,
                    "loss_scaling": f"dynamic, init 2^{int(round(__import__('math').log2(init_scale)))}",

@@ -168,7 +168,9 @@ typedef struct mpx_gemm_desc {
   int act;     /* 0 none, 1 GELU, 2 GELU backward, 3 row softmax of round_half(alpha*acc)
                   (whole rows: N <= 256 in one tile), 4 softmax backward: C = P*(alpha*acc -
                   rowsum(P*alpha*acc)) with aux = P (ld_aux >= round_up(N, 16)); aux is
-                  addressed with C's batch strides */
+                  addressed with C's batch strides; 5 GELU whose aux receives
+                  round_half(gelu'(pre)) (what _bw_gelu multiplies by, autodiff.py:173-185);
+                  6 C = acc * aux (the backward of 5: the saved derivative) */
   int block_n; /* 0 = auto (<= 256); 384 = the wide weight-gradient tile: CTA pair, 256 x 384,
                   one accumulator, MN-major B, no act / residual / aux, TMA-store epilogue
                   (aligned C or workspace) */

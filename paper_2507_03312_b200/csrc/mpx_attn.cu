@@ -576,11 +576,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* sV = sK + kAttnKV;
   uint8_t* sP = sV + kAttnKV;
   uint8_t* sdS = sP + kAttnP;
-  // 0 kv, 1 q/dO, 2 S, 3 P, 4 dP, 5 dS, 6 dQ(+dV,dK), 7 dQ read, 8 Q free (dK), 9 dO free (dV),
-  // 10 dV/dK read out (the next item may overwrite TMEM cols 256-511)
+  // 0 V landed, 1 dO_t (+ saved P_t) landed, 2 S, 3 P, 4 dP, 5 dS, 6 dQ done (K free), 7 dQ read,
+  // 8 dK done (Q free), 9 dV done (dO / P free), 10 dV/dK read out (the next item may overwrite
+  // TMEM cols 256-511), 11 Q_t landed, 12 K landed
   float* red = reinterpret_cast<float*>(sdS + kAttnP);
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + kSplit * 128);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int T = P.m_tiles;
@@ -591,7 +592,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     tma_prefetch(&tmdO);
-    for (int i = 0; i < 11; ++i) mbar_init(&bar[i], (i == 3 || i == 5 || i == 7 || i == 10) ? 128 * kSplit : 1);
+    for (int i = 0; i < 13; ++i) mbar_init(&bar[i], (i == 3 || i == 5 || i == 7 || i == 10) ? 128 * kSplit : 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -603,25 +604,35 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // persistent: items blockIdx.x, + gridDim.x, ...; the next item's K/V/Q/dO
-      // are loaded as soon as this item's last MMAs have read the tiles, so
-      // they land during the dQ / dV / dK readouts
+      // persistent: items blockIdx.x, + gridDim.x, ...  Every operand tile is
+      // reloaded the moment its last reader has finished, on its own barrier,
+      // so loads stream while the MMAs and the softmax warps work:
+      //   V      after the item's last dP (waited through dS ready)   -> next item's V
+      //   dO, P  after dV_t (and the dS pass, which read P_t)          -> tile t+1 / next item's tile 0
+      //   K      after the item's last dQ                             -> next item's K
+      //   Q      after dK_t                                           -> tile t+1 / next item's tile 0
+      // dP needs only dO and V, so the next item's first dP no longer waits for its K and Q.
       const bool saved = P.psaved != nullptr;
       const int n_pblk = ((P.N + 15) / 16 + 3) / 4;  // 64-key blocks of the saved P
-      const uint32_t qtx = 2 * kAttnQ + (saved ? n_pblk * 16384 : 0);  // Q, dO (+ the saved P) per tile
-      auto load_p = [&](int item, int t) {
-        for (int blk = 0; blk < n_pblk; ++blk)
-          tma_load_4d(sP + blk * 16384, &tmP, &bar[1], blk * 64, t * 128, item, 0);
+      const uint32_t dop_tx = kAttnQ + (saved ? n_pblk * 16384 : 0);  // dO (+ the saved P) per tile
+      auto load_dop = [&](int item, int t) {
+        mbar_arrive_expect_tx(&bar[1], dop_tx);
+        tma_load_4d(sdO, &tmdO, &bar[1], 0, t * 128, item % P.H, item / P.H);
+        if (saved)
+          for (int blk = 0; blk < n_pblk; ++blk)
+            tma_load_4d(sP + blk * 16384, &tmP, &bar[1], blk * 64, t * 128, item, 0);
       };
-      auto load_item = [&](int item) {
-        const int hh = item % P.H, bb = item / P.H;
-        mbar_arrive_expect_tx(&bar[0], 2 * kAttnKV);
-        tma_load_4d(sK, &tmK, &bar[0], 0, 0, hh, bb);
-        tma_load_4d(sV, &tmV, &bar[0], 0, 0, hh, bb);
-        mbar_arrive_expect_tx(&bar[1], qtx);
-        tma_load_4d(sQ, &tmQ, &bar[1], 0, 0, hh, bb);
-        tma_load_4d(sdO, &tmdO, &bar[1], 0, 0, hh, bb);
-        if (saved) load_p(item, 0);
+      auto load_q = [&](int item, int t) {
+        mbar_arrive_expect_tx(&bar[11], kAttnQ);
+        tma_load_4d(sQ, &tmQ, &bar[11], 0, t * 128, item % P.H, item / P.H);
+      };
+      auto load_v = [&](int item) {
+        mbar_arrive_expect_tx(&bar[0], kAttnKV);
+        tma_load_4d(sV, &tmV, &bar[0], 0, 0, item % P.H, item / P.H);
+      };
+      auto load_k = [&](int item) {
+        mbar_arrive_expect_tx(&bar[12], kAttnKV);
+        tma_load_4d(sK, &tmK, &bar[12], 0, 0, item % P.H, item / P.H);
       };
       const uint32_t q = smem_u32(sQ), dO = smem_u32(sdO), k = smem_u32(sK), v = smem_u32(sV);
       const uint32_t pp = smem_u32(sP), ds = smem_u32(sdS);
@@ -633,20 +644,27 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t id_q = idesc_f16(FMT, 128, 64, 0, 1);    // dQ: A K-major, B MN-major
       uint32_t gt = 0;  // tiles so far (barrier phases)
       int it = 0;       // items so far
-      if (blockIdx.x < P.items) load_item(blockIdx.x);
+      if (blockIdx.x < P.items) {
+        load_v(blockIdx.x);
+        load_dop(blockIdx.x, 0);
+        load_k(blockIdx.x);
+        load_q(blockIdx.x, 0);
+      }
       for (int item = blockIdx.x; item < P.items; item += gridDim.x, ++it) {
-        const int h = item % P.H, b = item / P.H;
+        const int next = item + (int)gridDim.x;
         if (it == kTraceIt) ATRACE(0);
         if (it == kTraceIt + 1) ATRACE(21);
-        mbar_wait(&bar[0], it & 1);
-        if (it == kTraceIt) ATRACE(1);
         for (int t = 0; t < T; ++t, ++gt) {
           const uint32_t ph = gt & 1;
-          mbar_wait(&bar[1], ph);
+          mbar_wait(&bar[1], ph);  // dO_t (+ P_t)
+          if (t == 0) mbar_wait(&bar[0], it & 1);  // V
           if (it == kTraceIt) ATRACE(2 + 8 * t);
           if (gt > 0) mbar_wait(&bar[7], ph ^ 1);  // previous dQ drained from TMEM cols 0-63
           tc_fence_after();
           if (!saved) {  // recompute P: S = Q K^T, softmax by the softmax warps
+            if (t == 0) mbar_wait(&bar[12], it & 1);
+            mbar_wait(&bar[11], ph);
+            tc_fence_after();
 #pragma unroll
             for (int s = 0; s < 4; ++s)  // S = Q K^T
               umma_f16(tmem, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), id_nk, s > 0);
@@ -674,13 +692,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           umma_commit(&bar[9]);
           mbar_wait(&bar[5], ph);  // dS_t written (dP consumed, P_t no longer read by the softmax warps)
           if (it == kTraceIt) ATRACE(4 + 8 * t);
+          if (t == T - 1 && next < P.items) load_v(next);  // the item's dP MMAs are done with V
+          if (t == 0) mbar_wait(&bar[12], it & 1);  // K
           tc_fence_after();
-          // dQ first, so the softmax warps read it out while dK runs; dK's
-          // completion (bar 8: every MMA of the tile) frees Q_t, dS_t and K
+          // dQ first, so the softmax warps read it out while dK runs
           for (int s = 0; s < n_chunks; ++s)  // dQ = dS K
             umma_f16(tmem, sw128_desc(ds + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
                      sw128_desc(k + s * 2048, 8192, 1024), id_q, s > 0);
           umma_commit(&bar[6]);
+          mbar_wait(&bar[11], ph);  // Q_t
+          tc_fence_after();
           for (int half = 0; half < halves; ++half) {
 #pragma unroll
             for (int s = 0; s < 8; ++s)  // over the 128 queries of the tile: dK += dS^T Q
@@ -688,16 +709,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                        sw128_desc(q + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
           }
           umma_commit(&bar[8]);
-          if (t + 1 < T) {  // next tile's Q / dO (/ P) as soon as this tile's MMAs have read them
-            mbar_arrive_expect_tx(&bar[1], qtx);
-            mbar_wait(&bar[8], ph);
-            tma_load_4d(sQ, &tmQ, &bar[1], 0, (t + 1) * 128, h, b);
-            mbar_wait(&bar[9], ph);  // dV done: dO and P free
-            tma_load_4d(sdO, &tmdO, &bar[1], 0, (t + 1) * 128, h, b);
-            if (saved) load_p(item, t + 1);
-          } else if (item + (int)gridDim.x < P.items) {  // next item, once every MMA has read its tiles
-            mbar_wait(&bar[8], ph);
-            load_item(item + gridDim.x);
+          const bool more = t + 1 < T;
+          if (more || next < P.items) {
+            const int li = more ? item : next, lt = more ? t + 1 : 0;
+            mbar_wait(&bar[9], ph);  // dV_t done: dO and P free (the dS pass finished with P_t)
+            load_dop(li, lt);
+            if (!more) {
+              mbar_wait(&bar[6], ph);  // the item's last dQ is done with K
+              load_k(next);
+            }
+            mbar_wait(&bar[8], ph);  // dK_t done: Q free
+            load_q(li, lt);
           }
         }
       }

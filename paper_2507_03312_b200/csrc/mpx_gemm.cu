@@ -62,7 +62,12 @@ static_assert(4 * (kATileBytes + kBTileBytes) <= 6 * (kATileBytes + kBTileBytes 
 //   over the row of round_half(alpha * acc) (f32 island, tensors.py:431-446)
 // ACT_SOFTMAX_BWD: aux = P (same layout as C); C = P * (acc - sum_row(P * acc))
 //   with acc = dP (autodiff.py:233-240)
-enum { ACT_NONE = 0, ACT_GELU = 1, ACT_GELU_BWD = 2, ACT_SOFTMAX = 3, ACT_SOFTMAX_BWD = 4 };
+// ACT_GELU_D: GELU forward whose aux receives round_half(gelu'(pre)) — the
+//   derivative _bw_gelu rounds onto the cotangent's grid (autodiff.py:173-185)
+//   — instead of the pre-activation; ACT_MUL_AUX: C = acc * aux (its backward:
+//   the saved derivative, so the dgrad epilogue needs no tanh)
+enum { ACT_NONE = 0, ACT_GELU = 1, ACT_GELU_BWD = 2, ACT_SOFTMAX = 3, ACT_SOFTMAX_BWD = 4, ACT_GELU_D = 5,
+       ACT_MUL_AUX = 6 };
 
 struct GemmParams {
   int M, N, K, BN;
@@ -129,6 +134,19 @@ __device__ __forceinline__ float2 gelu2(float2 x) {
   const float2 th = make_float2(tanh_fast(u.x), tanh_fast(u.y));
   const float2 hx = __fmul2_rn(x, f2(0.5f));
   return __ffma2_rn(hx, th, hx);
+}
+// GELU and its derivative from one tanh (ACT_GELU_D)
+__device__ __forceinline__ void gelu_and_grad2(float2 x, float2& y, float2& d) {
+  const float c0 = 0.7978845608028654f, c1 = 0.044715f;
+  const float2 x2 = __fmul2_rn(x, x);
+  const float2 u = __fmul2_rn(__fmul2_rn(x, __ffma2_rn(x2, f2(c1), f2(1.f))), f2(c0));
+  const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+  const float2 hx = __fmul2_rn(x, f2(0.5f));
+  y = __ffma2_rn(hx, t, hx);
+  const float2 a = __ffma2_rn(t, f2(0.5f), f2(0.5f));                      // 0.5 (1 + t)
+  const float2 sech2 = __ffma2_rn(make_float2(-t.x, -t.y), t, f2(1.f));    // 1 - t^2
+  const float2 k = __ffma2_rn(x2, f2(3.f * c0 * c1), f2(c0));              // c0 (1 + 3 c1 x^2)
+  d = __ffma2_rn(__fmul2_rn(hx, sech2), k, a);
 }
 __device__ __forceinline__ float2 gelu_grad2(float2 x) {
   const float c0 = 0.7978845608028654f, c1 = 0.044715f;
@@ -476,12 +494,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               v[2 * i + 1] = r2.y;
             }
           } else if (XO == XOP_AUX_IN) {
+            if (P.act == ACT_MUL_AUX) {  // the saved GELU derivative
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float2 r2 = __fmul2_rn(make_float2(v[2 * i], v[2 * i + 1]),
-                                           gelu_grad2(make_float2(xin[2 * i], xin[2 * i + 1])));
-              v[2 * i] = r2.x;
-              v[2 * i + 1] = r2.y;
+              for (int i = 0; i < 8; ++i) {
+                const float2 r2 = __fmul2_rn(make_float2(v[2 * i], v[2 * i + 1]), make_float2(xin[2 * i], xin[2 * i + 1]));
+                v[2 * i] = r2.x;
+                v[2 * i + 1] = r2.y;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float2 r2 = __fmul2_rn(make_float2(v[2 * i], v[2 * i + 1]),
+                                             gelu_grad2(make_float2(xin[2 * i], xin[2 * i + 1])));
+                v[2 * i] = r2.x;
+                v[2 * i + 1] = r2.y;
+              }
             }
           }
           return;  // XOP_AUX_OUT: the caller rounds (aux) and applies the GELU
@@ -513,24 +540,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += bb[i];
         }
-        if (P.act == ACT_GELU && XO == XOP_AUX_OUT) {
+        if ((P.act == ACT_GELU || P.act == ACT_GELU_D) && XO == XOP_AUX_OUT) {
           // bias only here; the staged aux store and the GELU happen in the caller
-        } else if (P.act == ACT_GELU) {
+        } else if (P.act == ACT_GELU || P.act == ACT_GELU_D) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = half_to_f32(f32_to_half(v[i], FMT), FMT);  // the rounded pre-activation
           if (P.aux) {
             uint16_t* ax = static_cast<uint16_t*>(P.aux) + b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ld_aux + col;
             uint32_t pk[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], FMT);
-              const uint16_t lo = (uint16_t)(pk[i] & 0xFFFFu), hi = (uint16_t)(pk[i] >> 16);
-              v[2 * i] = half_to_f32(lo, FMT);  // GELU of the rounded pre-activation
-              v[2 * i + 1] = half_to_f32(hi, FMT);
-            }
+            for (int i = 0; i < 8; ++i)
+              pk[i] = P.act == ACT_GELU_D ? pack2_fmt(gelu_grad_f(v[2 * i]), gelu_grad_f(v[2 * i + 1]), FMT)
+                                          : pack2_fmt(v[2 * i], v[2 * i + 1], FMT);
             *reinterpret_cast<uint4*>(ax) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             if (ncols == 16) *reinterpret_cast<uint4*>(ax + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
           }
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = gelu_f(v[i]);
+        } else if (P.act == ACT_MUL_AUX) {
+          float z[16];
+          if (XO == XOP_AUX_IN) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) z[i] = xin[i];
+          } else {
+            const long long ai = b1 * P.c_sb1 + b2 * P.c_sb2 + (long long)row * P.ld_aux + col;
+            load8(P.aux, ai, z);
+            if (ncols == 16) load8(P.aux, ai + 8, z + 8);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] *= z[i];
         } else if (P.act == ACT_GELU_BWD) {
           float z[16];
           if (XO == XOP_AUX_IN) {
@@ -623,13 +661,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               if (kAuxOut) {  // aux (rounded pre-activation) in the warp's buffer 0, C = GELU(aux) in buffer 1; SW128
                 if (row_ok && col < P.N_store) epi(v, col, min(16, P.N_store - col), v);
                 uint32_t pa[8], pc[8];
+                const bool dout = P.act == ACT_GELU_D;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                   pa[i] = pack2_fmt(v[2 * i], v[2 * i + 1], FMT);
                   const float a = half_to_f32((uint16_t)(pa[i] & 0xFFFFu), FMT);
                   const float b = half_to_f32((uint16_t)(pa[i] >> 16), FMT);
-                  const float2 y = gelu2(make_float2(a, b));  // GELU of the rounded pre-activation
-                  pc[i] = pack2_fmt(y.x, y.y, cf);
+                  if (dout) {  // aux = the rounded derivative, from the same tanh as the GELU
+                    float2 y, d;
+                    gelu_and_grad2(make_float2(a, b), y, d);
+                    pc[i] = pack2_fmt(y.x, y.y, cf);
+                    pa[i] = pack2_fmt(d.x, d.y, FMT);
+                  } else {
+                    const float2 y = gelu2(make_float2(a, b));  // GELU of the rounded pre-activation
+                    pc[i] = pack2_fmt(y.x, y.y, cf);
+                  }
                 }
                 const int s128 = lane & 7;
                 uint8_t* ra = obuf + lane * 128;
@@ -1110,10 +1156,12 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   if (P.tma_store && split == 1 && g->c_dtype != MPX_F32 && g->tma_store >= 0 && !no_xop) {
     const uint64_t es2 = 2;
     auto al16 = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
-    if ((g->act == ACT_GELU || g->act == ACT_GELU_BWD) && !g->residual && g->aux && al16(g->aux) && g->ld_aux % 8 == 0 &&
-        (nb1 == 1 || (g->c_sb1 > 0 && g->c_sb1 % 8 == 0)) && (nb2 == 1 || (g->c_sb2 > 0 && g->c_sb2 % 8 == 0))) {
+    const bool gelu_out = g->act == ACT_GELU || g->act == ACT_GELU_D;
+    if ((gelu_out || g->act == ACT_GELU_BWD || g->act == ACT_MUL_AUX) && !g->residual && g->aux && al16(g->aux) &&
+        g->ld_aux % 8 == 0 && (nb1 == 1 || (g->c_sb1 > 0 && g->c_sb1 % 8 == 0)) &&
+        (nb2 == 1 || (g->c_sb2 > 0 && g->c_sb2 % 8 == 0))) {
       const uint64_t s_m = (uint64_t)g->ld_aux * es2;
-      P.xop = g->act == ACT_GELU ? XOP_AUX_OUT : XOP_AUX_IN;
+      P.xop = gelu_out ? XOP_AUX_OUT : XOP_AUX_IN;
       // GELU out: aux and C leave as 64-column SW128 tiles, one 4 KB staging buffer each
       const bool out2 = P.xop == XOP_AUX_OUT;
       const CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B;

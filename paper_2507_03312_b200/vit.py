@@ -71,17 +71,29 @@ class ViTEngine:
         if not self.fused_attn:
             self.Sm = [e(B * H * S, self.ldS) for _ in range(c.depth)]  # scaled scores
             self.P = [e(B * H * S, self.ldS) for _ in range(c.depth)]
-        else:  # the forward's probabilities, saved for the backward (as the reference's autodiff saves
+        elif os.environ.get("MPX_ATTN_PSAVE", "1") == "1":
+            # the forward's probabilities, saved for the backward (as the reference's autodiff saves
             # the softmax output): the backward reloads P instead of recomputing scores and softmax
             self.attn_p = [torch.empty(VK.attention_psave_bytes(B, S, H), dtype=torch.uint8, device=self.dev)
                            for _ in range(c.depth)]
+            self.attn_stats = None
+        else:  # MPX_ATTN_PSAVE=0: only the row statistics; the backward recomputes P on chip
+            self.attn_p = [None] * c.depth
+            self.attn_stats = [torch.empty(VK.attention_stats_numel(B, S, H), dtype=torch.float32, device=self.dev)
+                               for _ in range(c.depth)]
         self.O = [e(M, D) for _ in range(c.depth)]
         # the blocks' weights transposed (K-major GEMM operands), refreshed every forward
         self._wt = [{"qkv": e(3 * D, D), "proj": e(D, D), "fc1": e(c.mlp, D), "fc2": e(D, c.mlp)}
                     for _ in range(c.depth)]
         self.xm = [e(M, D) for _ in range(c.depth)]  # after attention residual
         self.bn = [e(M, D) for _ in range(c.depth)]  # LN2 out
-        self.pre = [e(M, c.mlp) for _ in range(c.depth)]  # fc1 pre-activation
+        # gelu'(fc1 pre-activation) rounded to the half format — what _bw_gelu
+        # multiplies the cotangent by (autodiff.py:173-185) — saved by the fc1
+        # epilogue from the tanh its GELU evaluates, so the fc2 dgrad epilogue
+        # is a plain product (no second tanh pass over M x mlp elements)
+        self.pre = [e(M, c.mlp) for _ in range(c.depth)]
+        # MPX_GELU_SAVE_D=0: save the pre-activation instead and evaluate gelu' in the dgrad epilogue
+        self.gelu_d = os.environ.get("MPX_GELU_SAVE_D", "1") == "1"
         self.h = [e(M, c.mlp) for _ in range(c.depth)]  # GELU out
         f = lambda n: torch.empty(n, dtype=torch.float32, device=self.dev)  # noqa: E731
         self.mu1 = [f(M) for _ in range(c.depth)]
@@ -199,7 +211,8 @@ class ViTEngine:
             VK.linear_fwd_t(a, wt["qkv"], bias=p[q + "qkv.b"], out=qkv)
             O = self.O[i]
             if self.fused_attn:
-                VK.attention_fwd(qkv, B, S, H, hd, scale, out=O, p_save=self.attn_p[i])
+                VK.attention_fwd(qkv, B, S, H, hd, scale, out=O, p_save=self.attn_p[i],
+                                 stats=self.attn_stats[i] if self.attn_stats else None)
             else:
                 Sm, P_ = self.Sm[i], self.P[i]
                 VK.gemm(qkv, qkv[:, D:], M=S, N=S, K=hd, lda=3 * D, ldb=3 * D, nb=(H, B), a_sb=(hd, S * 3 * D),
@@ -213,7 +226,8 @@ class ViTEngine:
             VK.linear_fwd_t(O, wt["proj"], bias=p[q + "proj.b"], residual=x, out=xm)
             bn = self.bn[i]
             self._ln_fwd(xm, D, p[q + "ln2.g"], p[q + "ln2.b"], bn, D, self.mu2[i], self.rs2[i], M)
-            VK.linear_fwd_t(bn, wt["fc1"], bias=p[q + "fc1.b"], act=VK.ACT_GELU, aux=self.pre[i], out=self.h[i])
+            VK.linear_fwd_t(bn, wt["fc1"], bias=p[q + "fc1.b"], act=VK.ACT_GELU_D if self.gelu_d else VK.ACT_GELU,
+                            aux=self.pre[i], out=self.h[i])
             VK.linear_fwd_t(self.h[i], wt["fc2"], bias=p[q + "fc2.b"], residual=xm, out=self.x[i + 1])
         xl = self.x[c.depth]
         if cls:
@@ -294,7 +308,7 @@ class ViTEngine:
             VK.linear_wgrad(self.h[i], dX, out=g[q + "fc2.w"])  # fc2.b came with the LN backward above
             # dpre = (dX W2^T) * gelu'(pre); its column sum (the fc1.b grad) fused into the epilogue
             VK.linear_dgrad(dX, p[q + "fc2.w"], aux=self.pre[i], out=self.dpre, colsum_out=g[q + "fc1.b"],
-                            colsum_ws=self.ws)
+                            colsum_ws=self.ws, aux_act=VK.ACT_MUL_AUX if self.gelu_d else VK.ACT_GELU_BWD)
             # fc1: pre = bn @ W1 + b1
             VK.linear_wgrad(self.bn[i], self.dpre, out=g[q + "fc1.w"])
             VK.linear_dgrad(self.dpre, p[q + "fc1.w"], out=self.dA)
@@ -309,6 +323,7 @@ class ViTEngine:
             qkv, dqkv = self.qkv[i], self.dqkv
             if self.fused_attn:  # (the qkv.b gradient, colsum(dqkv), comes out of the kernel)
                 VK.attention_bwd(qkv, self.dO, B, S, H, hd, scale, dqkv=dqkv, p_saved=self.attn_p[i],
+                                 stats=self.attn_stats[i] if self.attn_stats else None,
                                  colsum_out=g[q + "qkv.b"], colsum_ws=self.ws)
             else:
                 self._attention_bwd_unfused(i, qkv, dqkv, scale)

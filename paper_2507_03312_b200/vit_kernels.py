@@ -12,7 +12,7 @@ from . import _native as _nat
 from .kernels import require_cuda, stream_handle
 
 _CODE = {torch.float32: _nat.MPX_F32, torch.float16: _nat.MPX_F16, torch.bfloat16: _nat.MPX_BF16}
-ACT_NONE, ACT_GELU, ACT_GELU_BWD, ACT_SOFTMAX, ACT_SOFTMAX_BWD = 0, 1, 2, 3, 4
+ACT_NONE, ACT_GELU, ACT_GELU_BWD, ACT_SOFTMAX, ACT_SOFTMAX_BWD, ACT_GELU_D, ACT_MUL_AUX = 0, 1, 2, 3, 4, 5, 6
 
 
 def _ptr(t):
@@ -111,14 +111,16 @@ def linear_fwd_t(x, wt, bias=None, act=ACT_NONE, aux=None, residual=None, out=No
                 out=out, ldc=N_ if out is not None else None, cta_group=cta_group)
 
 
-def linear_dgrad(dy, w, aux=None, out=None, cta_group=0, colsum_out=None, colsum_ws=None):
-    """dx[M,K] = dy[M,N] @ w[K,N]^T; with aux (the GELU pre-activation of
-    this layer's input) the GELU derivative is applied in the epilogue;
-    colsum_out receives sum_m dx[m,:] (the producing layer's bias gradient)."""
+def linear_dgrad(dy, w, aux=None, out=None, cta_group=0, colsum_out=None, colsum_ws=None, aux_act=ACT_GELU_BWD):
+    """dx[M,K] = dy[M,N] @ w[K,N]^T; with aux the GELU backward is applied in
+    the epilogue: aux_act ACT_GELU_BWD — aux is the pre-activation, gelu'
+    evaluated here; ACT_MUL_AUX — aux is the derivative the forward saved
+    (ACT_GELU_D), a plain product.  colsum_out receives sum_m dx[m,:] (the
+    producing layer's bias gradient)."""
     M, N_ = dy.shape
     K = w.shape[0]
     return gemm(dy, w, M=M, N=K, K=N_, lda=N_, ldb=N_, aux=aux, ld_aux=K,
-                act=ACT_GELU_BWD if aux is not None else ACT_NONE, out=out, ldc=K if out is not None else None,
+                act=aux_act if aux is not None else ACT_NONE, out=out, ldc=K if out is not None else None,
                 cta_group=cta_group, colsum_out=colsum_out, colsum_ws=colsum_ws)
 
 

@@ -4,7 +4,7 @@ on synthetic 32x32x3 batches of 64, f16 + LossScaling + Adam(lr 1e-3), built
 only from mpsim primitives and trained with
 mpsim.filter_value_and_grad / optimizer_update.
 
-    python tests/golden/gen_tiny_vit.py <init_scale_log2> <steps> [--hd64]
+    python tests/golden/gen_tiny_vit.py <init_scale_log2> <steps> [--hd64] [--gi=N] [--margins]
 
 writes tests/golden/tiny_vit_s<log2>.npz (--hd64: dim 128 / 2 heads, head
 dim 64 — the shape the GPU's fused attention kernels take — written to
@@ -122,30 +122,54 @@ def checksum(model):
     return h
 
 
+def _opt(name, default):
+    for a in sys.argv[1:]:
+        if a.startswith(f"--{name}="):
+            return int(a.split("=", 1)[1])
+    return default
+
+
 def main():
+    """--gi=N: growth interval N (default the reference's 2000): a small one
+    makes the scale grow back into the overflow boundary again and again.
+    --margins: at every step also evaluate the SAME model/batch at scale/2
+    and scale*2 (not applied); a step is marginal when those two flags
+    differ, i.e. the overflow boundary lies within a factor 2 of the scale
+    used, where f32 vs stepwise-f16 accumulation may legitimately flip it."""
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     log2 = int(args[0]) if len(args) > 0 else 15
     steps = int(args[1]) if len(args) > 1 else 20
+    gi = _opt("gi", 2000)
+    margins = "--margins" in sys.argv
     p0 = init_params()
     model = {k: tensor(v, F32) for k, v in p0.items()}
     opt = adam_init(model, 1e-3)
-    scaling = LossScaling(2.0 ** log2)
-    losses, scales, flags, sums = [], [], [], []
+    scaling = LossScaling(2.0 ** log2, growth_interval=gi)
+    losses, scales, flags, sums, lo_flags, hi_flags = [], [], [], [], [], []
     for step in range(steps):
         t0 = time.time()
         x, y = batch(step)
-        res = filter_value_and_grad(loss_fn, scaling)(model, {"x": tensor(x, F32), "y": tensor(y, I32)})
+        args_ = {"x": tensor(x, F32), "y": tensor(y, I32)}
+        res = filter_value_and_grad(loss_fn, scaling)(model, args_)
+        if margins:
+            for mult, col in ((0.5, lo_flags), (2.0, hi_flags)):
+                probe = scaling._replace(loss_scale=scaling.loss_scale * mult)
+                col.append(bool(filter_value_and_grad(loss_fn, probe)(model, args_).grads_finite))
         model, opt = mpsim.optimizer_update(model, opt, res.grads, res.grads_finite)
         losses.append(float(res.value.item()))
         scales.append(scaling.loss_scale)
         flags.append(bool(res.grads_finite))
         sums.append(checksum(model))
         scaling = res.scaling
-        print(f"step {step} loss {losses[-1]:.6f} scale {scales[-1]} finite {flags[-1]} ({time.time() - t0:.1f}s)",
+        print(f"step {step} loss {losses[-1]:.6f} scale {scales[-1]} finite {flags[-1]}"
+              + (f" (s/2 {lo_flags[-1]}, 2s {hi_flags[-1]})" if margins else "") + f" ({time.time() - t0:.1f}s)",
               flush=True)
-    out = Path(__file__).resolve().parent / (f"tiny_vit_hd64_s{log2}.npz" if HD64 else f"tiny_vit_s{log2}.npz")
+    tag = f"s{log2}" + (f"_gi{gi}" if gi != 2000 else "")
+    out = Path(__file__).resolve().parent / (f"tiny_vit_hd64_{tag}.npz" if HD64 else f"tiny_vit_{tag}.npz")
+    extra = {"flags_half_scale": np.asarray(lo_flags), "flags_double_scale": np.asarray(hi_flags)} if margins else {}
     np.savez_compressed(out, losses=np.asarray(losses), scales=np.asarray(scales), flags=np.asarray(flags),
-                        checksums=np.asarray(sums, dtype=np.uint64), **{"init." + k: v for k, v in p0.items()})
+                        checksums=np.asarray(sums, dtype=np.uint64), growth_interval=np.asarray(gi),
+                        **extra, **{"init." + k: v for k, v in p0.items()})
     print("wrote", out)
 
 

@@ -66,6 +66,17 @@ def test_epilogue_bias_gelu_residual_alpha(cuda, cg):
     zz = zin.float().requires_grad_(True)
     torch.nn.functional.gelu(zz, approximate="tanh").backward(dh.float() @ w2.float().t())
     close(dzg, zz.grad, rel=2e-2)
+    # GELU forward saving round_half(gelu'(pre)) (ACT_GELU_D), and its backward as a
+    # plain product (ACT_MUL_AUX): _bw_gelu rounds the derivative onto the
+    # cotangent's grid before multiplying (autodiff.py:173-185)
+    gd = torch.empty(M, N, device=cuda, dtype=dt)
+    y3 = VK.linear_fwd(x, w, bias=b, act=VK.ACT_GELU_D, aux=gd, cta_group=cg)
+    assert torch.equal(y3, y)  # the same GELU output as ACT_GELU
+    zz = pre.float().requires_grad_(True)
+    torch.nn.functional.gelu(zz, approximate="tanh").backward(torch.ones_like(zz))
+    close(gd, zz.grad, rel=1e-2)
+    dzm = VK.linear_dgrad(dh, w2, aux=zin, aux_act=VK.ACT_MUL_AUX, cta_group=cg)
+    close(dzm, (dh.float() @ w2.float().t()) * zin.float())
     # alpha + f32 output
     o = VK.gemm(x, w, M=M, N=N, K=K, lda=K, ldb=N, b_mn=True, alpha=0.125, out_dtype=torch.float32, cta_group=cg)
     close(o, 0.125 * (x.float() @ w.float()), rel=1e-3)
