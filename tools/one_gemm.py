@@ -1,7 +1,8 @@
 """One ViT-B fc1-shaped GEMM (M=50432, K=768, N=3072, bf16) for ncu.
 argv[1]: "bare" (default), "gelu" (bias + GELU, pre-activation saved to aux:
 the fc1 forward), "gelu_bwd" (fc2 dgrad with the GELU derivative from aux),
-"res" (fc2 forward: bias + residual)."""
+"res" (fc2 forward: bias + residual), "gelu_d" / "mul_aux" (the round-2 fc1
+forward saving gelu' and the fc2 dgrad multiplying by it)."""
 import sys
 from pathlib import Path
 
@@ -28,6 +29,10 @@ for _ in range(4):
         VK.linear_fwd(x, w, bias=b, act=VK.ACT_GELU, aux=aux, out=y)
     elif mode == "gelu_bwd":
         VK.linear_dgrad(aux, w, aux=y, out=x)
+    elif mode == "gelu_d":  # the round-2 fc1 forward: GELU + its rounded derivative saved to aux
+        VK.linear_fwd(x, w, bias=b, act=VK.ACT_GELU_D, aux=aux, out=y)
+    elif mode == "mul_aux":  # the round-2 fc2 dgrad: the saved derivative as a plain product
+        VK.linear_dgrad(aux, w, aux=y, out=x, aux_act=VK.ACT_MUL_AUX)
     elif mode == "res":
         VK.linear_fwd(aux, w2, bias=b[:K], residual=res, out=dx)
 torch.cuda.synchronize()
