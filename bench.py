@@ -476,13 +476,33 @@ def vit_section(args, cfg, B, half_name, dev, ws, rank, group, barrier, max_over
         traj = {"init_scale": init_scale, "flags": flags, "scales": scales, "replays_on_adjust": bool(replays),
                 "note": "used scale and finite flag of each step read from the device; replayed on "
                         "LossScaling.adjust (the reference's state machine, precision.py:156-173)"}
-    use_graph = (group is None or args.dp_graph) and not args.no_graph
+    # one CUDA graph per step, at N > 1 too (the NCCL bucket all-reduces, flag MIN and ZeRO
+    # collectives are captured with the kernels; every rank captures the same sequence).
+    # --dp-eager (or --no-graph) launches eagerly; a capture that fails on ANY rank makes
+    # every rank fall back to eager launches (agreed through a MIN all-reduce), so the
+    # ranks' collective sequences stay matched
+    use_graph = not args.no_graph and not (group is not None and args.dp_eager)
+    exec_note = None
     lib = _native.load()
     n0 = lib.mpx_launch_count()
     tr.step(images, labels)  # one eager step: the library kernels a step launches (a graph replays them)
     per_step = lib.mpx_launch_count() - n0
     if use_graph:  # the whole step as one CUDA graph (warm-up steps run inside capture())
-        tr.capture(images, labels, warmup=warmup)
+        ok = 1
+        try:
+            tr.capture(images, labels, warmup=warmup)
+        except Exception as e:  # noqa: BLE001 - agreed fallback below
+            if group is None:
+                raise
+            ok, exec_note = 0, f"eager (graph capture failed: {type(e).__name__})"
+            print(f"bench.py: rank {rank}: data-parallel graph capture failed: {e!r}", file=sys.stderr, flush=True)
+        if group is not None:
+            import torch.distributed as dist
+            t = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            if int(t.item()) == 0:
+                use_graph, exec_note = False, exec_note or "eager (graph capture failed on another rank)"
+    if use_graph:
         step = tr.replay
     else:
         for _ in range(warmup):
@@ -555,7 +575,7 @@ def vit_section(args, cfg, B, half_name, dev, ws, rank, group, barrier, max_over
                                                 "sharded K2/K4, half all-gather)" if args.zero else
                                                 " (per-block NCCL grad all-reduce overlapped with backward)")
                                                if group is not None else ""),
-                   "execution": "one CUDA graph per step" if use_graph else "eager stream-ordered launches",
+                   "execution": "one CUDA graph per step" if use_graph else (exec_note or "eager stream-ordered launches"),
                    "l2": "activations >> 126 MB L2: no flush needed"},
         "roofline": {"bound": "tensor", "achieved": round(tflops, 1), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(tflops / peak, 4), "flops_per_image": cfg.flops_per_image(),
@@ -742,8 +762,10 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="ViT sections: eager launches instead of a CUDA graph")
     ap.add_argument("--zero", action="store_true", help="ViT sections at N > 1: ZeRO-1 sharded optimizer step")
     ap.add_argument("--dp-graph", action="store_true",
-                    help="ViT sections at N > 1: capture the data-parallel step (NCCL collectives included) as a "
-                         "CUDA graph")
+                    help="(default now) ViT sections at N > 1: the data-parallel step (NCCL collectives included) "
+                         "captured as one CUDA graph")
+    ap.add_argument("--dp-eager", action="store_true",
+                    help="ViT sections at N > 1: eager stream-ordered launches instead of the captured graph")
     ap.add_argument("--dp-path", action="store_true",
                     help="validation: run the N > 1 code path (NCCL group, eager ViT steps, f16) at world size 1")
     ap.add_argument("--ref-sample-params", type=int, default=0,

@@ -70,15 +70,20 @@ def _opt(name, default):
 def main():
     """--gi=N: growth interval N (default the reference's 2000): a small one
     makes the scale grow back into the overflow boundary again and again.
-    --margins: at every step also evaluate the SAME model/batch at scale/2
-    and scale*2 (not applied); a step is marginal when those two flags
-    differ, i.e. the overflow boundary lies within a factor 2 of the scale
-    used, where f32 vs stepwise-f16 accumulation may legitimately flip it."""
+    --margins [--probe=F]: at every step also evaluate the SAME model/batch at
+    scale/F and scale*F (F = 1.25 by default; not applied); a step is marginal
+    when those two flags differ, i.e. the overflow boundary lies within a
+    factor F of the scale used, where f32 vs stepwise-f16 accumulation may
+    legitimately flip it."""
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     log2 = int(args[0]) if len(args) > 0 else 15
     steps = int(args[1]) if len(args) > 1 else 20
     gi = _opt("gi", 2000)
     margins = "--margins" in sys.argv
+    probe = 1.25
+    for a in sys.argv[1:]:
+        if a.startswith("--probe="):
+            probe = float(a.split("=", 1)[1])
     p0 = init_params()
     model = {k: tensor(v, F32) for k, v in p0.items()}
     opt = adam_init(model, 1e-3)
@@ -90,7 +95,7 @@ def main():
         args_ = {"x": tensor(x, F32), "y": tensor(y, I32)}
         res = filter_value_and_grad(loss_fn, scaling)(model, args_)
         if margins:
-            for mult, col in ((0.5, lo_flags), (2.0, hi_flags)):
+            for mult, col in ((1.0 / probe, lo_flags), (probe, hi_flags)):
                 probe = scaling._replace(loss_scale=scaling.loss_scale * mult)
                 col.append(bool(filter_value_and_grad(loss_fn, probe)(model, args_).grads_finite))
         model, opt = mpsim.optimizer_update(model, opt, res.grads, res.grads_finite)
@@ -100,11 +105,12 @@ def main():
         sums.append(checksum(model))
         scaling = res.scaling
         print(f"step {step} loss {losses[-1]:.6f} scale {scales[-1]} finite {flags[-1]}"
-              + (f" (s/2 {lo_flags[-1]}, 2s {hi_flags[-1]})" if margins else "") + f" ({time.time() - t0:.1f}s)",
+              + (f" (s/{probe} {lo_flags[-1]}, {probe}s {hi_flags[-1]})" if margins else "") + f" ({time.time() - t0:.1f}s)",
               flush=True)
     tag = f"s{log2}" + (f"_gi{gi}" if gi != 2000 else "")
     out = Path(__file__).resolve().parent / (f"tiny_vit_hd64_{tag}.npz" if HD64 else f"tiny_vit_{tag}.npz")
-    extra = {"flags_half_scale": np.asarray(lo_flags), "flags_double_scale": np.asarray(hi_flags)} if margins else {}
+    extra = {"flags_scale_down": np.asarray(lo_flags), "flags_scale_up": np.asarray(hi_flags),
+             "probe_factor": np.asarray(probe)} if margins else {}
     np.savez_compressed(out, losses=np.asarray(losses), scales=np.asarray(scales), flags=np.asarray(flags),
                         checksums=np.asarray(sums, dtype=np.uint64), growth_interval=np.asarray(gi),
                         **extra, **{"init." + k: v for k, v in p0.items()})
