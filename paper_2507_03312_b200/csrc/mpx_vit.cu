@@ -344,6 +344,133 @@ __global__ void __launch_bounds__(128, 4) ln_bwd_fused_kernel(const void* __rest
   }
 }
 
+// One-pass LayerNorm backward with the column partials in REGISTERS: a warp
+// per row, each lane owns 8 V fixed columns for every row it visits, so the
+// dgain / dbias (/ colsum dx) partials accumulate in 8 V x NSUM registers
+// instead of read-modify-write shared-memory slabs (the slab version spends
+// ~2 x NSUM shared-memory ops per element pair; this one none until the
+// block's final fixed-order combine).  The gain stays packed in registers;
+// x and dy are re-unpacked for the second pass (after the row reductions)
+// rather than kept as f32.  Same math and partial layout as
+// ln_bwd_fused_kernel ([NSUM][gridDim.x][D] for partials_reduce3_kernel).
+template <int V, int FMT, int NSUM>
+__global__ void __launch_bounds__(128, 2) ln_bwd_reg_kernel(const void* __restrict__ x, long long ldx,
+                                                           const void* __restrict__ g, const float* __restrict__ mean,
+                                                           const float* __restrict__ rstd, const void* __restrict__ dy,
+                                                           long long lddy, const void* __restrict__ dres,
+                                                           long long ldres, void* __restrict__ dx, long long lddx,
+                                                           float* __restrict__ ws, int rows, int D) {
+  constexpr int fmt = FMT;
+  ::mpx::pdl_grid_sync();
+  __shared__ float comb[4][NSUM][V * 256];  // per-warp column partials for the block's fixed-order combine
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float ag[V][8], ab[V][8], ax[V][8];
+#pragma unroll
+  for (int j = 0; j < V; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ag[j][e] = ab[j][e] = ax[j][e] = 0.f;
+  uint4 gw[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) gw[j] = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(g) + (j * 32 + lane) * 8));
+  auto f2v = [](float a) { return make_float2(a, a); };
+  const long long stride = (long long)gridDim.x * 4;
+  uint4 nx[V], nd[V];  // the next row's x / dy words, in flight during this row's work
+  auto load = [&](long long rr) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int c0 = (j * 32 + lane) * 8;
+      nx[j] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + rr * ldx + c0));
+      nd[j] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dy) + rr * lddy + c0));
+    }
+  };
+  long long row = (long long)blockIdx.x * 4 + warp;
+  if (row < rows) load(row);
+  for (; row < rows; row += stride) {
+    uint4 wx[V], wd[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      wx[j] = nx[j];
+      wd[j] = nd[j];
+    }
+    if (row + stride < rows) load(row + stride);
+    const float mu = mean[row], rs = rstd[row];
+    float2 s1 = f2v(0.f), s2 = f2v(0.f);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      float xv[8], dv[8], gg[8];
+      unpack8(wx[j], xv, fmt);
+      unpack8(wd[j], dv, fmt);
+      unpack8(gw[j], gg, fmt);
+#pragma unroll
+      for (int e2 = 0; e2 < 4; ++e2) {
+        const float2 d2 = make_float2(dv[2 * e2], dv[2 * e2 + 1]);
+        const float2 xh = __fmul2_rn(__fadd2_rn(make_float2(xv[2 * e2], xv[2 * e2 + 1]), f2v(-mu)), f2v(rs));
+        const float2 dg = __fmul2_rn(d2, make_float2(gg[2 * e2], gg[2 * e2 + 1]));
+        s1 = __fadd2_rn(s1, dg);
+        s2 = __ffma2_rn(dg, xh, s2);
+        const float2 pg = __ffma2_rn(d2, xh, make_float2(ag[j][2 * e2], ag[j][2 * e2 + 1]));
+        const float2 pb = __fadd2_rn(make_float2(ab[j][2 * e2], ab[j][2 * e2 + 1]), d2);
+        ag[j][2 * e2] = pg.x;
+        ag[j][2 * e2 + 1] = pg.y;
+        ab[j][2 * e2] = pb.x;
+        ab[j][2 * e2 + 1] = pb.y;
+      }
+    }
+    uint4 wr[V];
+    if (dres) {
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+        wr[j] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(dres) + row * ldres + (j * 32 + lane) * 8));
+    }
+    const float m1 = warp_sum(s1.x + s1.y) / (float)D;
+    const float m2 = warp_sum(s2.x + s2.y) / (float)D;
+    // o = rs (dy g - m1 - xhat m2) + dres = a (dy g) + (c x + b) + dres
+    const float a = rs, c = -rs * rs * m2, bb = -rs * m1 + rs * rs * m2 * mu;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int c0 = (j * 32 + lane) * 8;
+      float xv[8], dv[8], gg[8], rv[8], o[8];
+      unpack8(wx[j], xv, fmt);
+      unpack8(wd[j], dv, fmt);
+      unpack8(gw[j], gg, fmt);
+      if (dres) unpack8(wr[j], rv, fmt);
+#pragma unroll
+      for (int e2 = 0; e2 < 4; ++e2) {
+        const float2 t1 = __fmul2_rn(make_float2(dv[2 * e2], dv[2 * e2 + 1]), make_float2(gg[2 * e2], gg[2 * e2 + 1]));
+        const float2 t2 = __ffma2_rn(f2v(c), make_float2(xv[2 * e2], xv[2 * e2 + 1]), f2v(bb));
+        float2 r2 = __ffma2_rn(f2v(a), t1, t2);
+        if (dres) r2 = __fadd2_rn(r2, make_float2(rv[2 * e2], rv[2 * e2 + 1]));
+        o[2 * e2] = r2.x;
+        o[2 * e2 + 1] = r2.y;
+      }
+      const uint4 w = pack8(o, fmt);
+      *reinterpret_cast<uint4*>(static_cast<uint16_t*>(dx) + row * lddx + c0) = w;
+      if (NSUM == 3) {
+        float ov[8];
+        unpack8(w, ov, fmt);  // the column sum of the stored dx
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ax[j][e] += ov[e];
+      }
+    }
+  }
+  // fixed-order combine of the 4 warps' partials: one partial row per block
+#pragma unroll
+  for (int j = 0; j < V; ++j)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int col = (j * 32 + lane) * 8 + e;
+      comb[warp][0][col] = ag[j][e];
+      comb[warp][1][col] = ab[j][e];
+      if (NSUM == 3) comb[warp][NSUM - 1][col] = ax[j][e];
+    }
+  __syncthreads();
+  for (int col = threadIdx.x; col < D; col += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < NSUM; ++k)
+      ws[((long long)k * gridDim.x + blockIdx.x) * D + col] =
+          ((comb[0][k][col] + comb[1][k][col]) + comb[2][k][col]) + comb[3][k][col];
+}
+
 // block = 32 column vectors of 8 (256 columns) x 8 row lanes; ws layout
 // [nsum][split][D] with nsum = 2 (dgain, dbias) or 3 (+ colsum(dx))
 __global__ void __launch_bounds__(256) ln_colsum_kernel(const void* __restrict__ x, long long ldx,
@@ -1240,7 +1367,33 @@ int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int f = fmt_of(dtype);
   static const bool fused_off = getenv("MPX_LN_FUSED") && getenv("MPX_LN_FUSED")[0] == '0';
-  if (D <= 768 && !fused_off) {  // one pass: dx + all column partials
+  static const bool reg_off = getenv("MPX_LN_BWD_REG") && getenv("MPX_LN_BWD_REG")[0] == '0';
+  if (D <= 768 && !fused_off && !reg_off) {  // one pass, column partials in registers
+    const int nsum = dxsum ? 3 : 2;
+    int blocks = current_num_sms() * 2;
+    while ((long long)nsum * blocks * D > workspace_floats && blocks > 1) blocks /= 2;
+    auto launch = [&](auto k) {
+      return ::mpx::launch_k(k, blocks, 128, 0, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx,
+                             workspace, rows, D);
+    };
+    const int v = D / 256;
+    cudaError_t e;
+    if (nsum == 3) {
+      e = v == 1 ? (f ? launch(ln_bwd_reg_kernel<1, 1, 3>) : launch(ln_bwd_reg_kernel<1, 0, 3>))
+        : v == 2 ? (f ? launch(ln_bwd_reg_kernel<2, 1, 3>) : launch(ln_bwd_reg_kernel<2, 0, 3>))
+                 : (f ? launch(ln_bwd_reg_kernel<3, 1, 3>) : launch(ln_bwd_reg_kernel<3, 0, 3>));
+    } else {
+      e = v == 1 ? (f ? launch(ln_bwd_reg_kernel<1, 1, 2>) : launch(ln_bwd_reg_kernel<1, 0, 2>))
+        : v == 2 ? (f ? launch(ln_bwd_reg_kernel<2, 1, 2>) : launch(ln_bwd_reg_kernel<2, 0, 2>))
+                 : (f ? launch(ln_bwd_reg_kernel<3, 1, 2>) : launch(ln_bwd_reg_kernel<3, 0, 2>));
+    }
+    MPX_CUDA_CHECK(e);
+    MPX_LAUNCH_CHECK("ln_bwd_reg_kernel");
+    MPX_CUDA_CHECK(::mpx::launch_k(partials_reduce3_kernel, dim3((D + 31) / 32, nsum), 1024, 0, st, workspace, blocks, D, dgain, dbias, dxsum, f));
+    MPX_LAUNCH_CHECK("partials_reduce3_kernel");
+    return 0;
+  }
+  if (D <= 768 && !fused_off) {  // one pass: dx + all column partials (shared-memory slabs)
     const int nsum = dxsum ? 3 : 2;
     int blocks = current_num_sms() * 4;
     while ((long long)nsum * blocks * D > workspace_floats && blocks > 1) blocks /= 2;

@@ -96,8 +96,8 @@ def main():
         res = filter_value_and_grad(loss_fn, scaling)(model, args_)
         if margins:
             for mult, col in ((1.0 / probe, lo_flags), (probe, hi_flags)):
-                probe = scaling._replace(loss_scale=scaling.loss_scale * mult)
-                col.append(bool(filter_value_and_grad(loss_fn, probe)(model, args_).grads_finite))
+                probed = scaling._replace(loss_scale=scaling.loss_scale * mult)
+                col.append(bool(filter_value_and_grad(loss_fn, probed)(model, args_).grads_finite))
         model, opt = mpsim.optimizer_update(model, opt, res.grads, res.grads_finite)
         losses.append(float(res.value.item()))
         scales.append(scaling.loss_scale)
@@ -107,7 +107,7 @@ def main():
         print(f"step {step} loss {losses[-1]:.6f} scale {scales[-1]} finite {flags[-1]}"
               + (f" (s/{probe} {lo_flags[-1]}, {probe}s {hi_flags[-1]})" if margins else "") + f" ({time.time() - t0:.1f}s)",
               flush=True)
-    tag = f"s{log2}" + (f"_gi{gi}" if gi != 2000 else "")
+    tag = f"s{log2}" + (f"_gi{gi}" if gi != 2000 else "") + (f"_m{probe:g}" if margins else "")
     out = Path(__file__).resolve().parent / (f"tiny_vit_hd64_{tag}.npz" if HD64 else f"tiny_vit_{tag}.npz")
     extra = {"flags_scale_down": np.asarray(lo_flags), "flags_scale_up": np.asarray(hi_flags),
              "probe_factor": np.asarray(probe)} if margins else {}

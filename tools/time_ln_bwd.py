@@ -37,8 +37,9 @@ for _ in range(3):
     run()
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ITERS = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 e0.record()
-for _ in range(20):
+for _ in range(ITERS):
     run()
 e1.record()
 torch.cuda.synchronize()
@@ -48,5 +49,5 @@ ref = rs[:, None] * (d - d.mean(1, keepdim=True) - xh * (d * xh).mean(1, keepdim
 err = ((dx.float() - ref).abs().max() / ref.abs().max()).item()
 e_dg = ((dg.float() - (dy.float() * xh).sum(0)).abs().max() / (dy.float() * xh).sum(0).abs().max()).item()
 e_xs = ((dxs.float() - dx.float().sum(0)).abs().max() / dx.float().sum(0).abs().max()).item()
-print(json.dumps({"ln_bwd2_us": round(e0.elapsed_time(e1) / 20 * 1000, 1), "dx_rel": err, "dgain_rel": e_dg,
+print(json.dumps({"ln_bwd2_us": round(e0.elapsed_time(e1) / ITERS * 1000, 1), "dx_rel": err, "dgain_rel": e_dg,
                   "dxsum_rel": e_xs}))
