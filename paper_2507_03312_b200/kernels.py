@@ -216,9 +216,20 @@ def optimizer_step(params: Sequence[torch.Tensor], grads: Sequence[torch.Tensor]
     dev = params[0].device
     gdt = {dtype_of(g) for g in grads}
     if len(gdt) != 1:
-        # mixed gradient dtypes: one call per dtype group, only the last one
-        # advances the step counter -> do it with an explicit split
-        raise ValueError("optimizer_update: all gradient leaves must share one dtype")
+        # mixed gradient formats (the reference accepts any float leaves,
+        # optim.py:58-97): one K4 call per format group.  Every group must see
+        # the same step t = step_count + 1, so all but the last group count on
+        # private copies of the counter taken before any group runs; the last
+        # group advances the real one (once, when the step is applied).
+        order = sorted(gdt, key=lambda d: d.value)
+        groups = [[i for i, g in enumerate(grads) if dtype_of(g) is d] for d in order]
+        privs = [counter.clone() for _ in groups[:-1]]
+        for k, idx in enumerate(groups):
+            sel = lambda seq: [seq[i] for i in idx] if seq is not None else None  # noqa: E731
+            optimizer_step(sel(params), sel(grads), sel(m), sel(v), mode=mode, hp=hp,
+                           counter=privs[k] if k < len(privs) else counter, bc_table=bc_table, scale=scale,
+                           d_scale=d_scale, flag=flag, half_out=sel(half_out), upd_out=sel(upd_out))
+        return
     gdt = gdt.pop()
     hdt = -1
     if half_out is not None:

@@ -391,3 +391,33 @@ def test_mixed_vs_full_gradient_agreement(cuda):
 def test_non_cuda_tensors_raise(cuda):
     with pytest.raises(Exception):
         mpx.cast_tree({"w": torch.ones(3)}, mpx.F16)
+
+
+@pytest.mark.parametrize("gate", ["host", "device"])
+def test_optimizer_accepts_mixed_gradient_formats(cuda, gate):
+    """The reference's optimizer takes any float gradient leaves (optim.py:58-97):
+    f32, f16 and bf16 gradients in one tree step with one t, and the step
+    counter advances once per applied step (optim.py:77)."""
+    rng = np.random.default_rng(9)
+    fmts = {"a": "f16", "b": "bf16", "c": "f32", "d": "f16"}
+    shapes = {"a": (33, 17), "b": (1000,), "c": (7, 3), "d": (64,)}
+    p0 = {k: (rng.standard_normal(s) * 0.1).astype(np.float32) for k, s in shapes.items()}
+    model = {k: dev(v, "f32", cuda) for k, v in p0.items()}
+    state = mpx.adam_init(model, 1e-3)
+    ref_p = dict(p0)
+    ref_m = {k: np.zeros_like(v) for k, v in p0.items()}
+    ref_v = {k: np.zeros_like(v) for k, v in p0.items()}
+    t = 0
+    for step, finite in enumerate([True, True, False, True]):
+        g = {k: O.quantize((rng.standard_normal(s) * 0.01).astype(np.float32), fmts[k]) for k, s in shapes.items()}
+        grads = {k: dev(g[k], fmts[k], cuda) for k in shapes}
+        fl = finite if gate == "host" else mpx.DeviceBool(torch.tensor(int(finite), dtype=torch.int32, device=cuda))
+        model, state = mpx.optimizer_update(model, state, grads, fl)
+        if finite:
+            t += 1
+            for k in shapes:
+                ref_p[k], ref_m[k], ref_v[k], _ = O.adam_leaf(ref_p[k], "f32", ref_m[k], ref_v[k], g[k], t, 1e-3)
+        for k in shapes:
+            assert same_bits(host(model[k]), ref_p[k]), (step, k)
+            assert same_bits(host(state.mu[k]), ref_m[k]), (step, k)
+        assert state.step_count == t
