@@ -1,0 +1,31 @@
+"""Steady-state time and NVML energy of one ViT-B GEMM shape launched back to
+back (power-capped regime): python tools/time_gemm_loop.py <one_gemm mode> [seconds]."""
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parent))
+from energy import Meter  # noqa: E402
+from paper_2507_03312_b200 import vit_kernels as VK  # noqa: E402
+
+mode = sys.argv[1] if len(sys.argv) > 1 else "gelu_d"
+secs = float(sys.argv[2]) if len(sys.argv) > 2 else 4.0
+M, K, N = 256 * 197, 768, 3072
+bf = torch.bfloat16
+x = torch.randn(M, K, device="cuda").to(bf)
+w = (torch.randn(K, N, device="cuda") * 0.03).to(bf)
+wt = w.t().contiguous()
+b = (torch.randn(N, device="cuda") * 0.1).to(bf)
+y = torch.empty(M, N, device="cuda", dtype=bf)
+aux = torch.randn(M, N, device="cuda").to(bf)
+fns = {
+    "gelu_d": lambda: VK.linear_fwd_t(x, wt, bias=b, act=VK.ACT_GELU_D, aux=aux, out=y),
+    "gelu": lambda: VK.linear_fwd_t(x, wt, bias=b, act=VK.ACT_GELU, aux=aux, out=y),
+    "bare": lambda: VK.linear_fwd_t(x, wt, out=y),
+    "mul_aux": lambda: VK.linear_dgrad(aux, w, aux=y, out=x, aux_act=VK.ACT_MUL_AUX),
+}
+n, ms, j, wts, mhz = Meter(0).run(fns[mode], secs)
+print(json.dumps({"mode": mode, "us": round(ms * 1e3, 2), "mJ": round(j * 1e3, 2), "W": round(wts, 1), "sm_mhz": mhz}))
