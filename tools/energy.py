@@ -4,7 +4,7 @@ clock ~1.55-1.7 GHz of 1.965 under GEMM load): there, step time ~ energy /
 power cap, so a change that only hides latency (same work, same joules)
 does not speed the step up — a change that removes work or bytes does.
 
-    python tools/energy.py [step|kernels|all|cublas] [bf16|f16] [seconds_per_item]
+    python tools/energy.py [step|kernels|all|cublas|attn] [bf16|f16] [seconds_per_item]
 
 `step`: replays the captured step graph for ~N s; prints ms/step, J/step,
 mean W, median SM MHz.  `kernels`: each kernel class of the step at the
@@ -110,6 +110,33 @@ def main():
                                   "mJ": round(j * 1e3, 3), "W": round(w, 1), "sm_mhz": mhz,
                                   "GFLOP_per_J": round(fl / 1e9 / j, 1), "TFLOPs": round(fl / ms / 1e9, 1)}),
                       flush=True)
+        return
+    if mode == "attn":  # fused attention fwd+bwd vs cuDNN SDPA fwd+bwd, same shape, steady state
+        import torch.nn.functional as F
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        S_, H_, hd_ = 197, 12, 64
+        D_ = H_ * hd_
+        qkv = torch.randn(B * S_, 3 * D_, device=dev).to(half.torch)
+        dO = torch.randn(B * S_, D_, device=dev).to(half.torch)
+        O_ = torch.empty(B * S_, D_, device=dev, dtype=half.torch)
+        dqkv = torch.empty_like(qkv)
+        ps = torch.empty(VK.attention_psave_bytes(B, S_, H_), dtype=torch.uint8, device=dev)
+        sc = hd_ ** -0.5
+
+        def ours():
+            VK.attention_fwd(qkv, B, S_, H_, hd_, sc, out=O_, p_save=ps)
+            VK.attention_bwd(qkv, dO, B, S_, H_, hd_, sc, dqkv=dqkv, p_saved=ps)
+        q, k, v = (t.detach().requires_grad_() for t in qkv.view(B, S_, 3, H_, hd_).permute(2, 0, 3, 1, 4).unbind(0))
+        dOv = dO.view(B, S_, H_, hd_).transpose(1, 2)
+
+        def cudnn():
+            with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+                out = F.scaled_dot_product_attention(q, k, v, scale=sc)
+                torch.autograd.grad(out, (q, k, v), dOv)
+        for name, fn in (("mpx fused attention fwd+bwd", ours), ("cuDNN SDPA fwd+bwd", cudnn)):
+            n, ms, j, w, mhz = m.run(fn, secs)
+            print(json.dumps({"item": name, "us": round(ms * 1e3, 2), "mJ": round(j * 1e3, 3), "W": round(w, 1),
+                              "sm_mhz": mhz}), flush=True)
         return
     if mode in ("step", "all"):
         emit("step (CUDA graph replay)", 1, m.run(tr.replay, secs * 2))
