@@ -38,20 +38,32 @@ constexpr int kBK = 64;
 constexpr int kBNMax = 256;
 constexpr int kATileBytes = kBM * kBK * 2;       // 16 KB
 constexpr int kBTileBytes = kBNMax * kBK * 2;    // 32 KB
-constexpr int kEpiWarps = 8;                  // epilogue warps: kEpiWarps / 4 per TMEM lane quarter (16: no gain)
+// epilogue warps: kEpiWarps / 4 per TMEM lane quarter (16: no gain for the plain /
+// operand-in epilogues).  -DMPX_GELU_EPI_WARPS=16 gives the GELU-aux-out variant 16
+// epilogue warps (one 64-column group per warp per tile, its two 4 KB buffers free
+// a whole tile ahead) with a 3-deep ring in the same 230 KB of smem: measured
+// slower (331 vs 300 us steady state at the fc1 shape), so 8 is the default
+#ifndef MPX_GELU_EPI_WARPS
+#define MPX_GELU_EPI_WARPS 8
+#endif
+template <int XO> struct EpiCfg {
+  static constexpr int kWarps = XO == 3 ? MPX_GELU_EPI_WARPS : 8;  // XOP_AUX_OUT
+  static constexpr int kPerQ = kWarps / 4;
+  static constexpr int kThreads = 64 + 32 * kWarps;  // TMA warp, MMA warp, epilogue warps
+};
+constexpr int kEpiWarps = 8;  // the default variants (host-side BN checks)
 constexpr int kEpiPerQ = kEpiWarps / 4;
-constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // TMA warp, MMA warp, epilogue warps
 // Shared memory = A/B ring + epilogue staging, 230 KB either way.  Variants
 // that stage an operand (residual / GELU aux in) keep two 4 KB buffers per
 // epilogue warp (64 KB: operand prefetch + in-place output) and a 5-deep ring;
 // the others one buffer per warp (32 KB) and a 6-deep ring (measured: plain
 // epilogue 209 -> 205 us, operand-in variants 250 -> 262 us with one buffer).
 template <int XO> struct GemmSmem {
-  static constexpr int kStageKB = (XO == 1 || XO == 2 || XO == 3) ? 64 : 32;  // RES_IN, AUX_IN, AUX_OUT
+  static constexpr int kStageKB = (XO == 1 || XO == 2) ? 64 : XO == 3 ? 8 * EpiCfg<XO>::kWarps : 32;
   static constexpr int kEpiStage = kStageKB * 1024;
   static constexpr int kStages2 = (192 - kStageKB) / 32 + 1;  // CTA-pair ring depth (32 KB stages)
-  static constexpr int kStages1 = (kStages2 * 2) / 3;          // single-CTA ring depth (48 KB stages)
-  static constexpr int kBufPerWarp = kEpiStage / kEpiWarps / 4096;
+  static constexpr int kStages1 = (kStages2 * 2) / 3 > 1 ? (kStages2 * 2) / 3 : 2;  // single-CTA (48 KB stages)
+  static constexpr int kBufPerWarp = kEpiStage / EpiCfg<XO>::kWarps / 4096;
 };
 constexpr int kGroupM = 16;  // tile raster: groups of kGroupM m-blocks, m fastest
 constexpr size_t kGemmSmem = 1024 + 5 * (kATileBytes + kBTileBytes / 2) + 65536 + 384;
@@ -192,12 +204,14 @@ __device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, long long t
 // per-CTA halves land in column order.  Bytes per MAC from L2 are 5/6 / 3/4 of
 // the 256 x 256 tile's, the feed the long wgrad mainloops are bound by.
 template <int CG, int XO, int FMT, int WN = 0>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
                 const __grid_constant__ GemmParams P) {
   static_assert(!WN || (CG == 2 && XO == XOP_PLAIN), "the wide tile is a CTA-pair plain-epilogue variant");
   using SM = GemmSmem<XO>;
+  constexpr int kEpiWarps = EpiCfg<XO>::kWarps;  // (shadows the file-scope default)
+  constexpr int kEpiPerQ = EpiCfg<XO>::kPerQ;
   constexpr int kBNw = WN == 2 ? 512 : WN == 1 ? 384 : kBNMax;  // tile width
   constexpr int BT = kBNw * kBK * 2 / CG;  // B bytes per stage per CTA
   // smem ring depth: 48 / 32 KB stages; wide: 40 KB stages in the same 224 KB budget
@@ -1213,17 +1227,18 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   if (wide && P.xop != XOP_PLAIN)
     return fail(MPX_EINVAL, "mpx_gemm: block_n 384 / 512 needs the TMA-store plain epilogue (aligned C / workspace)");
   const KernelFn kern = wide ? wide_kernels[wn - 1][fmt] : kernels[fmt][CG - 1][P.xop];
+  const unsigned threads = P.xop == XOP_AUX_OUT ? EpiCfg<XOP_AUX_OUT>::kThreads : EpiCfg<XOP_PLAIN>::kThreads;
   const cudaError_t attr_err = ensure_smem_attr((const void*)kern, (int)kGemmSmem);
   if (attr_err != cudaSuccess) return fail((int)attr_err, "cudaFuncSetAttribute(gemm_kernel)");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (CG == 1) {
     const long long grid = std::min<long long>(P.total_tiles, current_num_sms());
-    MPX_CUDA_CHECK(::mpx::launch_k(kern, (unsigned)grid, kGemmThreads, kGemmSmem, st, ta, tb, tc, tx, P));
+    MPX_CUDA_CHECK(::mpx::launch_k(kern, (unsigned)grid, threads, kGemmSmem, st, ta, tb, tc, tx, P));
   } else {
     const long long pairs = std::min<long long>(P.total_tiles, current_num_sms() / 2);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(2 * pairs));
-    cfg.blockDim = dim3(kGemmThreads);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = kGemmSmem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
