@@ -172,3 +172,88 @@ def test_two_ranks_on_one_gpu_match_single_process(cuda):
         if np.abs(d_ref).max() <= 1e-4:
             continue
         assert np.linalg.norm(d_dp - d_ref) <= 0.25 * np.linalg.norm(d_ref), path
+
+
+def _zero_worker(rank, world, port, q):
+    """ZeRO-1 with two real ranks on one GPU: per-bucket
+    reduce-scatter during the backward, K2/K4 on this rank's chunk, the half
+    working copy all-gathered; the +inf is planted in rank 1's own chunk."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        from paper_2507_03312_b200.trainer import ViTTrainer
+        from paper_2507_03312_b200.tree import float_leaves
+        from paper_2507_03312_b200.vit_config import ViTConfig
+
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        tr = ViTTrainer(ViTConfig(**CFG), B // world, half="f16", device=dev, seed=0, loss_scale=INIT,
+                        group=dist.group.WORLD, world_size=world, zero=True)
+        own = tr.mp.ranges[0][0]  # first element of this rank's first chunk
+        flags, scales, losses = [], [], []
+        lo = rank * (B // world)
+        for i in range(STEPS):
+            x, y = _data(i)
+            tr.forward_backward(x[lo:lo + B // world].to(dev), y[lo:lo + B // world].to(dev))
+            tr.exchange.wait()
+            if i == BAD and rank == 1:
+                tr.mp.grad.buf[own] = float("inf")
+            tr.mp.step()
+            torch.cuda.synchronize()
+            flags.append(int(tr.mp.flag.item()))
+            scales.append(float(tr.mp.used_scale.item()))
+            losses.append(float(tr.engine.loss.item()))
+        full = {k: {path: v.float().cpu().numpy().reshape(-1) for path, v in float_leaves(tr.mp.gather(k))}
+                for k in ("p32", "m", "v", "half")}
+        q.put((rank, full, flags, scales, losses, tr.mp.step_count))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # noqa: BLE001 - surface the failure in the parent
+        import traceback
+        q.put((rank, "error", traceback.format_exc() + repr(e), None, None, None))
+
+
+def test_zero1_two_ranks_on_one_gpu(cuda):
+    """ZeRO-1 at world size 2 (not just the world-size-1 NCCL identity): both
+    ranks end with bit-identical gathered master weights / moments and half
+    copies, the same flags and scales as the single process (the planted +inf
+    lives only in rank 1's shard: the flag MIN makes rank 0 skip too), and
+    Adam trajectories within the same bar as the replicated data-parallel run."""
+    from paper_2507_03312_b200.trainer import ViTTrainer
+    from paper_2507_03312_b200.vit_config import ViTConfig
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_zero_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in procs], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=120)
+    for r in res:
+        assert r[1] != "error", r[2]
+    (_, f0, fl0, sc0, _, c0), (_, f1, fl1, sc1, _, c1) = res
+    for k in f0:
+        for path in f0[k]:
+            assert np.array_equal(f0[k][path].view(np.uint32), f1[k][path].view(np.uint32)), (k, path)
+    ref = ViTTrainer(ViTConfig(**CFG), B, half="f16", device=cuda, seed=0, loss_scale=INIT)
+    flags, scales = [], []
+    for i in range(STEPS):
+        x, y = _data(i)
+        _, f, s, _ = _run(ref, x.to(cuda), y.to(cuda), i, poison=(i == BAD))
+        flags.append(f)
+        scales.append(s)
+    assert fl0 == fl1 == flags and sc0 == sc1 == scales and c0 == c1 == ref.mp.step_count == STEPS - 1
+    p_init = ViTTrainer(ViTConfig(**CFG), B, half="f16", device=cuda, seed=0).mp.p32.buf.cpu().numpy()
+    single = ref.mp.p32.buf.cpu().numpy()
+    for path, off, v in zip(ref.mp.paths, ref.mp.offsets, ref.mp.grad.views):
+        n = v.numel()
+        d_ref = single[off:off + n] - p_init[off:off + n]
+        d_z = f0["p32"][path] - p_init[off:off + n]
+        if path.endswith("qkv.b"):  # the key-bias third carries no trajectory (see above)
+            d = CFG["dim"]
+            d_ref, d_z = np.delete(d_ref, np.s_[d:2 * d]), np.delete(d_z, np.s_[d:2 * d])
+        if np.abs(d_ref).max() <= 1e-4:
+            continue
+        assert np.linalg.norm(d_z - d_ref) <= 0.25 * np.linalg.norm(d_ref), path
