@@ -43,6 +43,9 @@ constexpr int kBTileBytes = kBNMax * kBK * 2;    // 32 KB
 // epilogue warps (one 64-column group per warp per tile, its two 4 KB buffers free
 // a whole tile ahead) with a 3-deep ring in the same 230 KB of smem: measured
 // slower (331 vs 300 us steady state at the fc1 shape), so 8 is the default
+#ifndef MPX_AUXOUT_GW
+#define MPX_AUXOUT_GW 32
+#endif
 #ifndef MPX_GELU_EPI_WARPS
 #define MPX_GELU_EPI_WARPS 8
 #endif
@@ -619,8 +622,13 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
         // one group ahead and the output overwrites it in place, row by row.
         constexpr bool kXin = XO == XOP_RES_IN || XO == XOP_AUX_IN;
         constexpr bool kAuxOut = XO == XOP_AUX_OUT;
+        constexpr int kAuxGW = MPX_AUXOUT_GW;
         const bool f32out = P.split > 1 || P.c_dtype == MPX_F32;
-        const int GW = f32out ? 32 : 64;
+        // GELU-aux-out with kAuxGW == 32: 32-column groups whose aux + C tiles (2 KB
+        // each, SW64) fill ONE 4 KB buffer, so the warp's two buffers ping-pong and a
+        // group waits only for the stores of the group before last (64: one 64-column
+        // group fills both buffers and waits for all earlier stores)
+        const int GW = (f32out || (kAuxOut && kAuxGW == 32)) ? 32 : 64;
         constexpr int cf = FMT;  // 16-bit C has the A/B format (checked on the host)
         const int n_groups = (P.BN + GW - 1) / GW;
         const int my_groups = n_groups > h ? (n_groups - h + kEpiPerQ - 1) / kEpiPerQ : 0;
@@ -691,6 +699,16 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
                     pc[i] = pack2_fmt(y.x, y.y, cf);
                   }
                 }
+                if (kAuxGW == 32) {  // 64 B rows, SW64: 16-byte unit u of row r at u ^ ((r >> 1) & 3)
+                  const int s64 = (lane >> 1) & 3;
+                  uint8_t* ra = bb + lane * 64;
+                  uint8_t* rc = ra + 2048;
+                  *reinterpret_cast<uint4*>(ra + (((2 * k) ^ s64) << 4)) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+                  *reinterpret_cast<uint4*>(ra + (((2 * k + 1) ^ s64) << 4)) = make_uint4(pa[4], pa[5], pa[6], pa[7]);
+                  *reinterpret_cast<uint4*>(rc + (((2 * k) ^ s64) << 4)) = make_uint4(pc[0], pc[1], pc[2], pc[3]);
+                  *reinterpret_cast<uint4*>(rc + (((2 * k + 1) ^ s64) << 4)) = make_uint4(pc[4], pc[5], pc[6], pc[7]);
+                  continue;
+                }
                 const int s128 = lane & 7;
                 uint8_t* ra = obuf + lane * 128;
                 uint8_t* rc = ra + 4096;
@@ -725,6 +743,9 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
         auto store_group = [&](int g, uint8_t* bb) {  // lane 0
           if (P.split > 1) {
             tma_store_4d(&tmC, bb, n0 + g * GW, row0, tc.s, 0);
+          } else if (kAuxOut && kAuxGW == 32) {
+            tma_store_4d(&tmX, bb, n0 + g * GW, row0, b1, b2);
+            tma_store_4d(&tmC, bb + 2048, n0 + g * GW, row0, b1, b2);
           } else if (kAuxOut) {
             tma_store_4d(&tmX, obuf, n0 + g * GW, row0, b1, b2);
             tma_store_4d(&tmC, obuf + 4096, n0 + g * GW, row0, b1, b2);
@@ -763,8 +784,8 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
               eph ^= 1u;
             }
           } else if (!batched) {
-            if (lane == 0) {  // the store that last used this buffer (both, for GELU-aux-out) has read it
-              if (kAuxOut)
+            if (lane == 0) {  // the store that last used this buffer (both, for 64-column GELU-aux-out) has read it
+              if (kAuxOut && kAuxGW != 32)
                 bulk_wait_read0();
               else
                 bulk_wait_read<kBufPerWarp - 1>();
@@ -1178,15 +1199,18 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
       P.xop = gelu_out ? XOP_AUX_OUT : XOP_AUX_IN;
       // GELU out: aux and C leave as 64-column SW128 tiles, one 4 KB staging buffer each
       const bool out2 = P.xop == XOP_AUX_OUT;
-      const CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B;
+      // (GELU-aux-out with 32-column groups: 32-column SW64 boxes)
+      const bool gw32 = out2 && MPX_AUXOUT_GW == 32;
+      const CUtensorMapSwizzle swz = gw32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+      const uint32_t box_c = gw32 ? 32 : 64;
       rc = make_map(&tx, g->aux, fmt, g->N, g->M, nb1, nb2, s_m, nb1 > 1 ? (uint64_t)g->c_sb1 * es2 : s_m * g->M,
-                    nb2 > 1 ? (uint64_t)g->c_sb2 * es2 : s_m * g->M, 64, 32, swz);
+                    nb2 > 1 ? (uint64_t)g->c_sb2 * es2 : s_m * g->M, box_c, 32, swz);
       if (rc) return rc;
       if (out2) {
         const uint64_t s_c = (uint64_t)g->ldc * es2;
         rc = make_map(&tc, g->C, g->c_dtype == MPX_BF16 ? 1 : 0, g->N, g->M, nb1, nb2, s_c,
                       nb1 > 1 ? (uint64_t)g->c_sb1 * es2 : s_c * g->M, nb2 > 1 ? (uint64_t)g->c_sb2 * es2 : s_c * g->M,
-                      64, 32, swz);
+                      box_c, 32, swz);
         if (rc) return rc;
       }
     } else if (g->act == ACT_NONE && g->residual && al16(g->residual) && g->ldr % 8 == 0 &&
