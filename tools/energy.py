@@ -133,7 +133,15 @@ def main():
             with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
                 out = F.scaled_dot_product_attention(q, k, v, scale=sc)
                 torch.autograd.grad(out, (q, k, v), dOv)
-        for name, fn in (("mpx fused attention fwd+bwd", ours), ("cuDNN SDPA fwd+bwd", cudnn)):
+        def ours_f():
+            VK.attention_fwd(qkv, B, S_, H_, hd_, sc, out=O_, p_save=ps)
+
+        def ours_b():
+            VK.attention_bwd(qkv, dO, B, S_, H_, hd_, sc, dqkv=dqkv, p_saved=ps)
+        items = (("mpx fused attention fwd+bwd", ours), ("cuDNN SDPA fwd+bwd", cudnn))
+        if len(sys.argv) > 4 and sys.argv[4] == "split":
+            items = (("mpx fused attention fwd", ours_f), ("mpx fused attention bwd", ours_b))
+        for name, fn in items:
             n, ms, j, w, mhz = m.run(fn, secs)
             print(json.dumps({"item": name, "us": round(ms * 1e3, 2), "mJ": round(j * 1e3, 3), "W": round(w, 1),
                               "sm_mhz": mhz}), flush=True)
