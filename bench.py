@@ -522,17 +522,23 @@ def vit_section(args, cfg, B, half_name, dev, ws, rank, group, barrier, max_over
     clk = clocks.summary()
     final_loss = float(loss.item())
     finite = bool(tr.grads_finite)
-    # end to end: f32 images + labels from pinned host memory every step
-    # (copy stream, double-buffered), loss read back every step
-    h_img = torch.empty(images.shape, dtype=torch.float32, pin_memory=True)
-    h_img.copy_(images)
+    # end to end: images + labels from pinned host memory every step (copy
+    # stream, double-buffered), loss read back every step.  The images travel
+    # in the half format the step computes in: the model's first op rounds
+    # them to it anyway (cast_tree(args, half), precision.py:209-210), so half
+    # host data is the same input bit for bit, at half the PCIe bytes
+    from paper_2507_03312_b200 import kernels as K
+    img_half = torch.empty(images.shape, dtype=half.torch, device=dev)
+    K.cast_into([images], [img_half])  # K1, RNE: the rounding the trainer's own cast applies
+    h_img = torch.empty(images.shape, dtype=half.torch, pin_memory=True)
+    h_img.copy_(img_half)
     h_lab = torch.empty(labels.shape, dtype=torch.int32, pin_memory=True)
     h_lab.copy_(labels)
-    d_img = [torch.empty_like(images), torch.empty_like(images)]
+    d_img = [torch.empty_like(img_half), torch.empty_like(img_half)]
     d_lab = [torch.empty_like(labels), torch.empty_like(labels)]
     if use_graph:  # one captured step per input buffer (they share every state buffer)
         for b in range(2):
-            d_img[b].copy_(images)
+            d_img[b].copy_(img_half)
             d_lab[b].copy_(labels)
         gidx = [tr.capture(d_img[b], d_lab[b], warmup=1) for b in range(2)]
     out_loss = torch.empty(steps, dtype=torch.float32, pin_memory=True)
@@ -582,12 +588,14 @@ def vit_section(args, cfg, B, half_name, dev, ws, rank, group, barrier, max_over
                      "note": "whole-step training FLOPs (3x forward GEMM+attention) / step time vs measured "
                              "sustained cuBLAS bf16"},
         "e2e": {"value": round(ws * B * steps / (e2e_ms * 1e-3), 1), "unit": "img/s",
-                "h2d_bytes_per_step": h_img.numel() * 4 + h_lab.numel() * 4, "d2h_bytes_per_step": 4},
+                "h2d_bytes_per_step": h_img.numel() * h_img.element_size() + h_lab.numel() * 4,
+                "d2h_bytes_per_step": 4, "inputs": f"{half_name} images (the step's first op rounds f32 to it) "
+                                                  "+ i32 labels, pinned host memory"},
         "final_loss": round(final_loss, 5), "last_step_finite": finite, "loss_scale": tr.scaling.loss_scale,
     }
     if traj is not None:
         out["scale_trajectory"] = traj
-    del tr, images, labels, d_img, d_lab
+    del tr, images, labels, d_img, d_lab, img_half
     torch.cuda.empty_cache()
     return out
 
