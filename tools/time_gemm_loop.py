@@ -1,5 +1,5 @@
 """Steady-state time and NVML energy of one ViT-B GEMM shape launched back to
-back (power-capped regime): python tools/time_gemm_loop.py <one_gemm mode> [seconds]."""
+back (power-capped regime): python tools/time_gemm_loop.py <mode> [seconds] [cta_group]."""
 import json
 import sys
 from pathlib import Path
@@ -21,7 +21,17 @@ wt = w.t().contiguous()
 b = (torch.randn(N, device="cuda") * 0.1).to(bf)
 y = torch.empty(M, N, device="cuda", dtype=bf)
 aux = torch.randn(M, N, device="cuda").to(bf)
+cg = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+x2 = torch.randn(M, N, device="cuda").to(bf)  # fc2 forward: [M, 3072] @ [3072, 768] + b + residual
+w2t = (torch.randn(K, N, device="cuda") * 0.02).to(bf)
+res = torch.randn(M, K, device="cuda").to(bf)
+b2 = (torch.randn(K, device="cuda") * 0.1).to(bf)
+o2 = torch.empty(M, K, device="cuda", dtype=bf)
+xp = torch.randn(M, K, device="cuda").to(bf)  # proj forward: [M, 768] @ [768, 768] + b + residual
+wpt = (torch.randn(K, K, device="cuda") * 0.03).to(bf)
 fns = {
+    "fc2_res": lambda: VK.linear_fwd_t(x2, w2t, bias=b2, residual=res, out=o2, cta_group=cg),
+    "proj_res": lambda: VK.linear_fwd_t(xp, wpt, bias=b2, residual=res, out=o2, cta_group=cg),
     "gelu_d": lambda: VK.linear_fwd_t(x, wt, bias=b, act=VK.ACT_GELU_D, aux=aux, out=y),
     "gelu": lambda: VK.linear_fwd_t(x, wt, bias=b, act=VK.ACT_GELU, aux=aux, out=y),
     "bare": lambda: VK.linear_fwd_t(x, wt, out=y),
