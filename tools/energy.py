@@ -24,6 +24,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2507_03312_b200 import as_dtype  # noqa: E402
+from paper_2507_03312_b200 import kernels as K_  # noqa: E402
 from paper_2507_03312_b200 import vit_kernels as VK  # noqa: E402
 from paper_2507_03312_b200.trainer import ViTTrainer  # noqa: E402
 from paper_2507_03312_b200.vit_config import VIT_B16  # noqa: E402
@@ -138,9 +139,25 @@ def main():
 
         def ours_b():
             VK.attention_bwd(qkv, dO, B, S_, H_, hd_, sc, dqkv=dqkv, p_saved=ps)
+        cs_out = torch.empty(3 * D_, dtype=half.torch, device=dev)
+        cs_ws = torch.empty(B * 3 * D_, dtype=torch.float32, device=dev)
+        cs_ws2 = torch.empty(1 << 22, dtype=torch.float32, device=dev)
+
+        def ours_b_cs():  # with the in-kernel qkv-bias gradient (column sums of dqkv), as the engine runs it
+            VK.attention_bwd(qkv, dO, B, S_, H_, hd_, sc, dqkv=dqkv, p_saved=ps, colsum_out=cs_out, colsum_ws=cs_ws)
+
+        def ours_b_sep():  # the same bias gradient by a separate column-sum pass over dqkv
+            from paper_2507_03312_b200 import _native as NN
+            VK.attention_bwd(qkv, dO, B, S_, H_, hd_, sc, dqkv=dqkv, p_saved=ps)
+            NN.check(NN.load().mpx_colsum(VK._CODE[half.torch], dqkv.data_ptr(), 3 * D_, 0, B * S_, 3 * D_, 1,
+                                          cs_ws2.data_ptr(), cs_ws2.numel(), cs_out.data_ptr(), 3 * D_,
+                                          VK._CODE[half.torch], 1.0, K_.stream_handle(dev)), "colsum")
         items = (("mpx fused attention fwd+bwd", ours), ("cuDNN SDPA fwd+bwd", cudnn))
         if len(sys.argv) > 4 and sys.argv[4] == "split":
             items = (("mpx fused attention fwd", ours_f), ("mpx fused attention bwd", ours_b))
+        if len(sys.argv) > 4 and sys.argv[4] == "colsum":
+            items = (("bwd, no bias grad", ours_b), ("bwd + in-kernel bias grad", ours_b_cs),
+                     ("bwd + separate colsum pass", ours_b_sep))
         for name, fn in items:
             n, ms, j, w, mhz = m.run(fn, secs)
             print(json.dumps({"item": name, "us": round(ms * 1e3, 2), "mJ": round(j * 1e3, 3), "W": round(w, 1),
