@@ -26,6 +26,7 @@ import torch
 
 from . import kernels as K
 from .dtypes import BF16, F16, F32, DType, Scalar, as_dtype, dtype_of, is_float_leaf, quantize_host_scalar
+from .tensors import _note
 from .tree import tree_leaves, tree_map
 
 _HALF: DType = F16
@@ -117,9 +118,11 @@ def cast_tree(t, dtype):
             todo.append(x)
     outs = dict(zip(map(id, todo), _cast_tensor_leaves(todo, d)))
 
+    from .tensors import _note  # a tape entry per float leaf (T.cast records even same-format casts)
+
     def leaf(x):
         if is_float_leaf(x):
-            return outs.get(id(x), x)
+            return _note(outs.get(id(x), x))
         if isinstance(x, Scalar) and not x.weak and x.dtype.is_float:
             return Scalar(quantize_host_scalar(x.value, d), weak=False, dtype=d)
         return x
@@ -383,6 +386,15 @@ class ActivationTape:
 
     def __init__(self):
         self._seen: dict[tuple, int] = {}
+        self._outputs = 0  # bytes of the drop-in tensor ops' outputs (the reference's tape entries)
+        self._n_outputs = 0
+
+    def note_output(self, t):
+        """A drop-in tensor op produced `t` (tensors._note): the reference's
+        tape entry (tensors.py:173-180), counted at its nominal width."""
+        if isinstance(t, torch.Tensor):
+            self._outputs += t.numel() * t.element_size()
+            self._n_outputs += 1
 
     def pack(self, t: torch.Tensor):
         if isinstance(t, torch.Tensor) and t.device.type != "meta":
@@ -395,6 +407,11 @@ class ActivationTape:
         return t
 
     def activation_bytes(self) -> int:
+        """The reference's definition (autodiff.py:43-45: every forward
+        intermediate on the tape) when the forward ran on the drop-in tensor
+        ops; otherwise (the fused ViT engine) the tensors autograd saved."""
+        if self._n_outputs:
+            return int(self._outputs)
         return int(sum(self._seen.values()))
 
 
@@ -407,7 +424,9 @@ def value_and_grad(f, params, args, has_aux: bool = False, *, tape_hook=None):
     live = {id(x): x.detach().requires_grad_(True) for x in uniq}
     p = tree_map(lambda x: live.get(id(x), x) if is_float_leaf(x) else x, params)
     tape = ActivationTape()
-    with torch.enable_grad(), torch.autograd.graph.saved_tensors_hooks(tape.pack, tape.unpack):
+    from .tensors import recording
+
+    with torch.enable_grad(), torch.autograd.graph.saved_tensors_hooks(tape.pack, tape.unpack), recording(tape):
         out = f(p, args)
     if has_aux:
         try:
@@ -473,10 +492,10 @@ def filter_value_and_grad(f, scaling, has_aux: bool = False, use_mixed_precision
         if has_aux:
             def scaled_f(p, a):
                 loss, aux = f(p, a)
-                return _ScaleLoss.apply(loss, s, d_s), aux
+                return _note(_ScaleLoss.apply(loss, s, d_s)), aux
         else:
             def scaled_f(p, a):
-                return _ScaleLoss.apply(f(p, a), s, d_s)
+                return _note(_ScaleLoss.apply(f(p, a), s, d_s))
 
         res = value_and_grad(scaled_f, params_h, args_h, has_aux=has_aux, tape_hook=tape_hook)
         scaled_value, grads_h = res[0], res[1]

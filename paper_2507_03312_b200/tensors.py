@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 
 import numpy as np
 import torch
@@ -96,6 +97,35 @@ class Tensor(torch.Tensor):
 
 def _wrap(t: torch.Tensor) -> Tensor:
     return t if isinstance(t, Tensor) else t.as_subclass(Tensor)
+
+
+# the reference's tape records every primitive's output (tensors.py:173-180,
+# _record); Tape.activation_bytes sums bytes_of over them (autodiff.py:43-45).
+# precision.value_and_grad installs an ActivationTape here while the forward
+# runs, and every public op below reports its output to it.
+_REC = threading.local()
+
+
+def _note(out):
+    rec = getattr(_REC, "tape", None)
+    if rec is not None:
+        rec.note_output(out)
+    return out
+
+
+class recording:
+    """Context manager: route op outputs to `tape.note_output` (thread-local)."""
+
+    def __init__(self, tape):
+        self.tape = tape
+
+    def __enter__(self):
+        self.prev = getattr(_REC, "tape", None)
+        _REC.tape = self.tape
+        return self.tape
+
+    def __exit__(self, *exc):
+        _REC.tape = self.prev
 
 
 def _device(device):
@@ -382,13 +412,13 @@ def _binary(name: str, a, b) -> Tensor:
         _require_float(b, name)
     if ta and tb:
         out = promote(dtype_of(a), dtype_of(b))
-        return _Binary.apply(name, a, b, 0.0, 0, out.torch)
+        return _note(_Binary.apply(name, a, b, 0.0, 0, out.torch))
     if ta:
         out = promote_with_scalar(dtype_of(a), b)
-        return _Binary.apply(name, a, None, b.value, 0, out.torch)
+        return _note(_Binary.apply(name, a, None, b.value, 0, out.torch))
     if tb:
         out = promote_with_scalar(dtype_of(b), a)
-        return _Binary.apply(name, None, b, a.value, 1, out.torch)
+        return _note(_Binary.apply(name, None, b, a.value, 1, out.torch))
     raise TypeError(f"{name} needs at least one tensor operand")
 
 
@@ -444,7 +474,7 @@ def _unary(name: str, a) -> Tensor:
     if not isinstance(a, torch.Tensor):
         raise TypeError(f"{name} expects a tensor")
     _require_float(a, name)
-    return _Unary.apply(name, a)
+    return _note(_Unary.apply(name, a))
 
 
 def neg(a) -> Tensor:
@@ -545,7 +575,7 @@ def reduce(op_code: str, a, axis: int | None = None) -> Tensor:
         raise ValueError("mean over an empty axis")
     if n == 0 and op_code == "max":
         raise ValueError("max over an empty axis")
-    return _Reduce.apply(op_code, a, ax)
+    return _note(_Reduce.apply(op_code, a, ax))
 
 
 # ---------------------------------------------------------------- matmul
@@ -591,7 +621,7 @@ def matmul(a, b) -> Tensor:
     kb = b.shape[0] if b.ndim == 1 else b.shape[-2]
     if ka != kb:
         raise ValueError(f"matmul inner extents disagree: {tuple(a.shape)} @ {tuple(b.shape)}")
-    return _Matmul.apply(a, b, promote(dtype_of(a), dtype_of(b)).torch)
+    return _note(_Matmul.apply(a, b, promote(dtype_of(a), dtype_of(b)).torch))
 
 
 # ---------------------------------------------------------------- softmax / layernorm / cross-entropy
@@ -623,7 +653,7 @@ def softmax(a, axis: int) -> Tensor:
     if not isinstance(a, torch.Tensor):
         raise TypeError("softmax expects a tensor")
     _require_float(a, "softmax")
-    return _Softmax.apply(a, _normalize_axis(axis, a.ndim, "softmax"))
+    return _note(_Softmax.apply(a, _normalize_axis(axis, a.ndim, "softmax")))
 
 
 class _LayerNorm(torch.autograd.Function):
@@ -671,7 +701,7 @@ def layernorm(a, gain, bias) -> Tensor:
     if tuple(gain.shape) != (n,) or tuple(bias.shape) != (n,):
         raise ValueError(f"gain/bias must have shape ({n},)")
     d = promote(promote(dtype_of(a), dtype_of(gain)), dtype_of(bias))
-    return _LayerNorm.apply(a, _contig(gain), _contig(bias), d.torch)
+    return _note(_LayerNorm.apply(a, _contig(gain), _contig(bias), d.torch))
 
 
 class _CrossEntropy(torch.autograd.Function):
@@ -718,7 +748,7 @@ def cross_entropy(logits, labels) -> Tensor:
         lab = labels.cpu().numpy()  # the reference's range check (tensors.py:509-511) is a host decision
         if lab.min() < 0 or lab.max() >= classes:
             raise ValueError("label out of range")
-    return _CrossEntropy.apply(logits, _contig(labels))
+    return _note(_CrossEntropy.apply(logits, _contig(labels)))
 
 
 # ---------------------------------------------------------------- structural ops
@@ -749,7 +779,7 @@ class _Reshape(torch.autograd.Function):
 def reshape(a, shape) -> Tensor:
     if not isinstance(a, torch.Tensor):
         raise TypeError("reshape expects a tensor")
-    return _Reshape.apply(a, tuple(shape) if not isinstance(shape, int) else (shape,))
+    return _note(_Reshape.apply(a, tuple(shape) if not isinstance(shape, int) else (shape,)))
 
 
 class _Transpose(torch.autograd.Function):
@@ -769,7 +799,7 @@ def transpose(a, axes=None) -> Tensor:
     axes = tuple(range(a.ndim))[::-1] if axes is None else tuple(axes)
     if sorted(axes) != list(range(a.ndim)):
         raise ValueError(f"transpose: {axes} is not a permutation of {a.ndim} axes")
-    return _Transpose.apply(a, axes)
+    return _note(_Transpose.apply(a, axes))
 
 
 __all__ = ["Tensor", "tensor", "zeros", "zeros_like", "ones", "bytes_of", "quantize", "quantize_array", "add", "sub",

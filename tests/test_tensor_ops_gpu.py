@@ -258,3 +258,44 @@ def test_reference_attention_model_trains_through_drop_in_api(cuda, prec):
         ref = G[f"attn_{prec}__p_final__{name}"]
         rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         assert rel <= (1e-4 if prec == "f32" else 5e-2), (prec, name, rel)
+
+
+def test_activation_bytes_match_reference_tape(cuda):
+    """The reference's acceptance criterion 6 (pkg/tests/test_acceptance.py:257-270):
+    one step of its attention classifier (feature_dim 64, 4 heads, batch 32) records
+    the analytic activation footprint of every forward intermediate on the tape
+    (autodiff.py:43-45) — mixed / full must land in [0.45, 0.60].  Through the
+    drop-in layer the tape_hook sees the same definition (every op's output at its
+    nominal width).  The reference's own counts, from
+        python -c "from mpsim.bench import RunConfig, fit; ..."  (f16: 225540, f32: 401924, ratio 0.5612)
+    are the expected values."""
+    import paper_2507_03312_b200 as mpx
+    from paper_2507_03312_b200 import tensors as T
+
+    f_dim, n_cls, batch = 64, 2, 32
+    rng = np.random.default_rng(0)
+
+    def lin(i, o):
+        return {"w": T.tensor((rng.standard_normal((i, o)) / i ** 0.5).astype(np.float32)),
+                "b": T.tensor(np.zeros(o, np.float32))}
+
+    params = {"embed": lin(f_dim, f_dim),
+              "attn": {"ln_gain": T.tensor(np.ones(f_dim, np.float32)), "ln_bias": T.tensor(np.zeros(f_dim, np.float32)),
+                       "q": lin(f_dim, f_dim), "k": lin(f_dim, f_dim), "v": lin(f_dim, f_dim), "o": lin(f_dim, f_dim)},
+              "num_heads": 4, "ffn": {"lift": lin(f_dim, 4 * f_dim), "drop": lin(4 * f_dim, f_dim)},
+              "head": lin(f_dim, n_cls)}
+    batch_ = {"x": T.tensor(rng.standard_normal((batch, f_dim)).astype(np.float32)),
+              "y": T.tensor(rng.integers(0, n_cls, batch).astype(np.int32), "i32")}
+
+    def loss_fn(p, b):
+        return T.cross_entropy(_attention_forward(T, mpx, p, b["x"]), b["y"])
+
+    counts = {}
+    for prec in ("f16", "f32"):
+        box = []
+        mpx.filter_value_and_grad(loss_fn, mpx.LossScaling(2.0 ** 15), use_mixed_precision=prec != "f32",
+                                  tape_hook=lambda tape: box.append(tape.activation_bytes()))(params, batch_)
+        counts[prec] = box[0]
+    ratio = counts["f16"] / counts["f32"]
+    assert 0.45 <= ratio <= 0.60, (counts, ratio)
+    assert counts == {"f16": 225540, "f32": 401924}, counts
