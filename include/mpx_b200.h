@@ -185,6 +185,19 @@ typedef struct mpx_gemm_desc {
    * C, no GELU-aux-out); colsum_out has C's dtype. */
   float* colsum_ws;
   void* colsum_out;
+  /* optional fused LayerNorm of the stored C rows (tensors.py:459-491):
+   * ln_out[m, :] = (C[m, :] - mean) * rstd * ln_gain + ln_bias over each WHOLE row,
+   * mean / rstd (f32 per row) saved for the backward.  Needs N == 768 (a cluster of
+   * three CTA pairs owns a 256-row block and exchanges row sums over distributed
+   * shared memory), the residual epilogue (no act), batch 1, 16-bit C, split 1;
+   * ln_out has C's layout with leading dimension ld_ln.  NULL ln_out = off. */
+  const void* ln_gain;
+  const void* ln_bias;
+  void* ln_out;
+  int64_t ld_ln;
+  float* ln_mean;
+  float* ln_rstd;
+  float ln_eps;
 } mpx_gemm_desc;
 
 int mpx_gemm(const mpx_gemm_desc* desc, void* stream);

@@ -59,6 +59,9 @@ class GemmDescC(ctypes.Structure):
         ("alpha", ctypes.c_float), ("act", ctypes.c_int), ("block_n", ctypes.c_int), ("split_k", ctypes.c_int),
         ("workspace", ctypes.c_void_p), ("cta_group", ctypes.c_int), ("tma_store", ctypes.c_int),
         ("colsum_ws", ctypes.c_void_p), ("colsum_out", ctypes.c_void_p),
+        ("ln_gain", ctypes.c_void_p), ("ln_bias", ctypes.c_void_p), ("ln_out", ctypes.c_void_p),
+        ("ld_ln", ctypes.c_int64), ("ln_mean", ctypes.c_void_p), ("ln_rstd", ctypes.c_void_p),
+        ("ln_eps", ctypes.c_float),
     ]
 
 

@@ -62,9 +62,9 @@ constexpr int kEpiPerQ = kEpiWarps / 4;
 // the others one buffer per warp (32 KB) and a 6-deep ring (measured: plain
 // epilogue 209 -> 205 us, operand-in variants 250 -> 262 us with one buffer).
 template <int XO> struct GemmSmem {
-  static constexpr int kStageKB = (XO == 1 || XO == 2) ? 64 : XO == 3 ? 8 * EpiCfg<XO>::kWarps : 32;
+  static constexpr int kStageKB = (XO == 1 || XO == 2 || XO == 5) ? 64 : XO == 3 ? 8 * EpiCfg<XO>::kWarps : 32;
   static constexpr int kEpiStage = kStageKB * 1024;
-  static constexpr int kStages2 = (192 - kStageKB) / 32 + 1;  // CTA-pair ring depth (32 KB stages)
+  static constexpr int kStages2 = (192 - kStageKB) / 32 + 1 - (XO == 5 ? 1 : 0);  // CTA-pair ring depth (32 KB stages)
   static constexpr int kStages1 = (kStages2 * 2) / 3 > 1 ? (kStages2 * 2) / 3 : 2;  // single-CTA (48 KB stages)
   static constexpr int kBufPerWarp = kEpiStage / EpiCfg<XO>::kWarps / 4096;
 };
@@ -110,11 +110,25 @@ struct GemmParams {
   float* csum;  // fused column sum: per-32-row partials [ceil(M/32)][N] (f32), or null
   int tma_store;  // 16-bit C written through swizzled smem staging + TMA bulk stores
   int xop;        // epilogue operand through TMA (tmX): 0 none, 1 residual in, 2 aux in (GELU'), 3 aux out (GELU)
+  // XOP_RES_LN: LayerNorm of the stored rows (gain / bias in the A/B format, f32 row stats)
+  const void* ln_g;
+  const void* ln_b;
+  float* ln_mean;
+  float* ln_rstd;
+  float ln_eps;
 };
 // kernel variants by epilogue: XOP_NONE = generic (every act / operand at run
 // time, operands read from global); the others are lean staged-path variants
 // (bias optional): residual in, GELU' with aux in, GELU with aux out, plain
-enum { XOP_NONE = 0, XOP_RES_IN = 1, XOP_AUX_IN = 2, XOP_AUX_OUT = 3, XOP_PLAIN = 4 };
+enum { XOP_NONE = 0, XOP_RES_IN = 1, XOP_AUX_IN = 2, XOP_AUX_OUT = 3, XOP_PLAIN = 4, XOP_RES_LN = 5 };
+// XOP_RES_LN — bias + residual epilogue followed by the LayerNorm of every
+// stored row (LN folded into the GEMM that produces the residual
+// stream, tensors.py:459-491).  N = 768 = 3 x 256: a cluster of 3 CTA pairs
+// (6 CTAs) owns one 256-row block, pair p computes columns 256p..256p+255;
+// each CTA's per-row partial sums (of the ROUNDED stored values) are
+// exchanged over distributed shared memory, so every CTA normalises its own
+// columns from smem and TMA-stores LN(x) next to x: the LayerNorm never
+// re-reads x from HBM and needs no launch of its own.
 
 __device__ __forceinline__ float half_to_f32(uint16_t h, int fmt) {
   return fmt ? to_f32<MPX_BF16>(h) : to_f32<MPX_F16>(h);
@@ -210,8 +224,11 @@ template <int CG, int XO, int FMT, int WN = 0>
 __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
-                const __grid_constant__ GemmParams P) {
+                const __grid_constant__ CUtensorMap tmL, const __grid_constant__ GemmParams P) {
   static_assert(!WN || (CG == 2 && XO == XOP_PLAIN), "the wide tile is a CTA-pair plain-epilogue variant");
+  static_assert(XO != XOP_RES_LN || CG == 2, "the LayerNorm epilogue is a CTA-pair variant");
+  constexpr bool kLN = XO == XOP_RES_LN;
+  constexpr int kClusterCTAs = kLN ? 6 : CG;
   using SM = GemmSmem<XO>;
   constexpr int kEpiWarps = EpiCfg<XO>::kWarps;  // (shadows the file-scope default)
   constexpr int kEpiPerQ = EpiCfg<XO>::kPerQ;
@@ -237,9 +254,18 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0u;
+  const uint32_t rank = crank & 1u;     // rank within the CTA pair
+  const uint32_t pr = crank >> 1;       // pair within the cluster (LN variant: the 256-column block)
+  const uint16_t pair_mask = (uint16_t)(3u << (2 * pr));
+  const uint32_t leader_rank = crank & ~1u;
   const bool leader = rank == 0;
-  const long long t_first = blockIdx.x / CG, t_step = gridDim.x / CG;
+  const long long t_first = blockIdx.x / kClusterCTAs, t_step = gridDim.x / kClusterCTAs;
+  // the LayerNorm exchange scratch (RES_LN only; past the barriers, in the ring space the shorter ring frees):
+  // lnq [4 quarters][2 warps][32 rows] float2, lnx [2 tile parities][3 pairs][128 rows] float2, lnbar[2]
+  float2* lnq = reinterpret_cast<float2*>(stage_epi + kEpiStage + 512);
+  float2* lnx = lnq + 4 * 2 * 32;
+  uint64_t* lnbar = reinterpret_cast<uint64_t*>(lnx + 2 * 3 * 128);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -255,6 +281,8 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
       mbar_init(&tempty[i], 32 * kEpiWarps * CG);
     }
     for (int i = 0; i < kEpiWarps; ++i) mbar_init(&ebar[i], 1);
+    if (kLN)
+      for (int i = 0; i < 2; ++i) mbar_init(&lnbar[i], 3 * 128);  // 3 CTAs x 128 rows arrive per phase
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -282,7 +310,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (long long t = t_first; t < P.total_tiles; t += t_step) {
-        const TileCoord tc = tile_coord(P, t);
+        const TileCoord tc = kLN ? TileCoord{0, 0, (int)t, (int)pr} : tile_coord(P, t);
         const int b1 = tc.z % P.nb1, b2 = tc.z / P.nb1;
         const int m0 = tc.m_blk * (kBM * CG) + (int)rank * kBM;
         const int n0 = tc.n_blk * P.BN + (WN ? 0 : (int)rank * bn_cta);
@@ -335,7 +363,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (long long t = t_first; t < P.total_tiles; t += t_step) {
-        const TileCoord tc = tile_coord(P, t);
+        const TileCoord tc = kLN ? TileCoord{0, 0, (int)t, (int)pr} : tile_coord(P, t);
         const int kb0 = tc.s * P.kb_per_split;
         const int kb1 = min(P.k_blocks, kb0 + P.kb_per_split);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -362,7 +390,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
           }
           // smem slot free (in both CTAs) once these MMAs have read it
           if (CG == 2)
-            umma_commit_2sm_mc(&empty[stage], 3);
+            umma_commit_2sm_mc(&empty[stage], pair_mask);
           else
             umma_commit(&empty[stage]);
           if (++stage == S) {
@@ -371,7 +399,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
           }
         }
         if (CG == 2)
-          umma_commit_2sm_mc(&tfull[acc], 3);  // accumulator ready for both epilogues
+          umma_commit_2sm_mc(&tfull[acc], pair_mask);  // accumulator ready for both epilogues
         else
           umma_commit(&tfull[acc]);
         if (!WN) acc ^= 1;  // (wide: one accumulator, its phase flips every tile)
@@ -391,10 +419,11 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
     uint8_t* stg = obuf;
     uint32_t gcount = 0;  // staged column groups so far (selects the ping-pong buffer)
     uint32_t eph = 0;  // phase of this warp's operand barrier
+    uint32_t ln_tiles = 0;  // RES_LN: tiles exchanged so far (slot / phase of lnbar)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (long long t = t_first; t < P.total_tiles; t += t_step) {
-      const TileCoord tc = tile_coord(P, t);
+      const TileCoord tc = kLN ? TileCoord{0, 0, (int)t, (int)pr} : tile_coord(P, t);
       const int b1 = tc.z % P.nb1, b2 = tc.z / P.nb1;
       const int row0 = tc.m_blk * (kBM * CG) + (int)rank * kBM + q * 32;
       const int row = row0 + lane;
@@ -502,7 +531,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
               v[2 * i + 1] = r2.y;
             }
           }
-          if (XO == XOP_RES_IN) {
+          if (XO == XOP_RES_IN || XO == XOP_RES_LN) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const float2 r2 =
@@ -599,7 +628,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] *= gelu_grad_f(z[i]);
         }
-        if (P.res && XO == XOP_RES_IN) {
+        if (P.res && (XO == XOP_RES_IN || XO == XOP_RES_LN)) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += xin[i];
         } else if (P.res) {
@@ -620,7 +649,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
         // TMA store of group gc overlaps the TMEM loads and math of gc + 1; a
         // staged operand (residual / GELU aux in) lands in the group's buffer
         // one group ahead and the output overwrites it in place, row by row.
-        constexpr bool kXin = XO == XOP_RES_IN || XO == XOP_AUX_IN;
+        constexpr bool kXin = XO == XOP_RES_IN || XO == XOP_AUX_IN || XO == XOP_RES_LN;
         constexpr bool kAuxOut = XO == XOP_AUX_OUT;
         constexpr int kAuxGW = MPX_AUXOUT_GW;
         const bool f32out = P.split > 1 || P.c_dtype == MPX_F32;
@@ -630,12 +659,13 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
         // group fills both buffers and waits for all earlier stores)
         const int GW = (f32out || (kAuxOut && kAuxGW == 32)) ? 32 : 64;
         constexpr int cf = FMT;  // 16-bit C has the A/B format (checked on the host)
+        float ln_s1 = 0.f, ln_s2 = 0.f;  // RES_LN: this row's sum / sum of squares over this warp's columns
         const int n_groups = (P.BN + GW - 1) / GW;
         const int my_groups = n_groups > h ? (n_groups - h + kEpiPerQ - 1) / kEpiPerQ : 0;
         auto buf = [&](uint32_t c) { return obuf + (c % kBufPerWarp) * 4096; };
         auto x_load = [&](int g, uint32_t c) {  // operand tile of group g -> buffer of group count c
-          const int xb1 = XO == XOP_RES_IN && P.r_sb1 == 0 ? 0 : b1;
-          const int xb2 = XO == XOP_RES_IN && P.r_sb2 == 0 ? 0 : b2;
+          const int xb1 = (XO == XOP_RES_IN || XO == XOP_RES_LN) && P.r_sb1 == 0 ? 0 : b1;
+          const int xb2 = (XO == XOP_RES_IN || XO == XOP_RES_LN) && P.r_sb2 == 0 ? 0 : b2;
           bulk_wait_read<kBufPerWarp - 1>();  // the store that last used this buffer has read it
           mbar_arrive_expect_tx(&ebar[warp - 2], 4096);
           tma_load_4d(buf(c), &tmX, &ebar[warp - 2], n0 + g * GW, row0, xb1, xb2);
@@ -643,7 +673,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
         auto release_acc = [&]() {  // this warp is done with the accumulator: the MMA may reuse it
           tc_fence_before();
           if (CG == 2)
-            mbar_arrive_remote(&tempty[acc], 0);
+            mbar_arrive_remote(&tempty[acc], leader_rank);
           else
             mbar_arrive(&tempty[acc]);
         };
@@ -735,6 +765,15 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
               uint32_t pk[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) pk[i] = pack2_fmt(v[2 * i], v[2 * i + 1], cf);
+              if (kLN) {  // row statistics of the ROUNDED stored values (the LayerNorm's input)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const float a = half_to_f32((uint16_t)(pk[i] & 0xFFFFu), FMT);
+                  const float b = half_to_f32((uint16_t)(pk[i] >> 16), FMT);
+                  ln_s1 += a + b;
+                  ln_s2 = fmaf(a, a, fmaf(b, b, ln_s2));
+                }
+              }
               *reinterpret_cast<uint4*>(rowp + (((2 * k) ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
               *reinterpret_cast<uint4*>(rowp + (((2 * k + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
             }
@@ -762,8 +801,8 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
           if (lane == 0) {
             bulk_wait_read0();
             if (kXin && my_groups > 0) {
-              const int xb1 = XO == XOP_RES_IN && P.r_sb1 == 0 ? 0 : b1;
-              const int xb2 = XO == XOP_RES_IN && P.r_sb2 == 0 ? 0 : b2;
+              const int xb1 = (XO == XOP_RES_IN || XO == XOP_RES_LN) && P.r_sb1 == 0 ? 0 : b1;
+              const int xb2 = (XO == XOP_RES_IN || XO == XOP_RES_LN) && P.r_sb2 == 0 ? 0 : b2;
               mbar_arrive_expect_tx(&ebar[warp - 2], 4096u * my_groups);
               for (int j = 0; j < my_groups; ++j)
                 tma_load_4d(buf(j), &tmX, &ebar[warp - 2], n0 + (h + kEpiPerQ * j) * GW, row0, xb1, xb2);
@@ -805,6 +844,85 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
             bulk_commit();
             if (!batched && kXin && j + 1 < my_groups) x_load(g + kEpiPerQ, gcount + 1);  // next group's operand
           }
+        }
+        if (kLN) {
+          // ---- LayerNorm of the stored rows.  (1) combine this quarter's warps
+          lnq[(q * kEpiPerQ + h) * 32 + lane] = make_float2(ln_s1, ln_s2);
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * kEpiPerQ) : "memory");
+          float2 part = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int j = 0; j < kEpiPerQ; ++j) {
+            const float2 o = lnq[(q * kEpiPerQ + j) * 32 + lane];
+            part.x += o.x;
+            part.y += o.y;
+          }
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * kEpiPerQ) : "memory");
+          // (2) send the row's partial over this CTA's 256 columns to the 3 CTAs
+          // holding the same 128 rows (pair rank `rank` of each pair); slot by tile parity
+          const int slot = (int)(ln_tiles & 1u);
+          const int r = q * 32 + lane;
+          if (h == 0) {
+#pragma unroll
+            for (int dst = 0; dst < 3; ++dst) {
+              const uint32_t target = 2u * dst + rank;
+              st_cluster_f2(lnx + (slot * 3 + (int)pr) * 128 + r, target, part);
+              mbar_arrive_remote_cluster(&lnbar[slot], target);
+            }
+          }
+          // (3) the whole row's statistics
+          mbar_wait_cluster(&lnbar[slot], (ln_tiles >> 1) & 1u);
+          float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+          for (int src = 0; src < 3; ++src) {
+            const float2 o = lnx[(slot * 3 + src) * 128 + r];
+            s1 += o.x;
+            s2 += o.y;
+          }
+          const float inv_n = 1.f / (float)P.N;
+          const float mean = s1 * inv_n;
+          const float rstd = rsqrtf(fmaxf(s2 * inv_n - mean * mean, 0.f) + P.ln_eps);
+          if (pr == 0 && h == 0 && row_ok) {
+            P.ln_mean[row] = mean;
+            P.ln_rstd[row] = rstd;
+          }
+          // (4) once the x stores have read the staging buffers, y = LN(x) in place -> TMA store
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+          const int sw = lane & 7;
+          for (int j = 0; j < my_groups; ++j) {
+            uint8_t* rowp = buf(j) + lane * 128;
+            const int cbase = n0 + (h + kEpiPerQ * j) * GW;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              float xv[16], gg[16], bb[16];
+              const uint4 w0 = *reinterpret_cast<const uint4*>(rowp + (((2 * k) ^ sw) << 4));
+              const uint4 w1 = *reinterpret_cast<const uint4*>(rowp + (((2 * k + 1) ^ sw) << 4));
+              const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                xv[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), FMT);
+                xv[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), FMT);
+              }
+              load8(P.ln_g, cbase + k * 16, gg);
+              load8(P.ln_g, cbase + k * 16 + 8, gg + 8);
+              load8(P.ln_b, cbase + k * 16, bb);
+              load8(P.ln_b, cbase + k * 16 + 8, bb + 8);
+              uint32_t pk[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                pk[e] = pack2_fmt((xv[2 * e] - mean) * rstd * gg[2 * e] + bb[2 * e],
+                                  (xv[2 * e + 1] - mean) * rstd * gg[2 * e + 1] + bb[2 * e + 1], FMT);
+              *reinterpret_cast<uint4*>(rowp + (((2 * k) ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              *reinterpret_cast<uint4*>(rowp + (((2 * k + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            }
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            for (int j = 0; j < my_groups; ++j) tma_store_4d(&tmL, buf(j), n0 + (h + kEpiPerQ * j) * GW, row0, 0, 0);
+            bulk_commit();
+          }
+          ++ln_tiles;
         }
         if (XO != XOP_NONE && XO != XOP_AUX_OUT && P.csum != nullptr && batched && row0 < P.M) {
           // fused column sum of the staged (rounded) C: lane l sums columns 2l, 2l+1
@@ -870,7 +988,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
       if (!P.tma_store) {  // (the staged path released it after its last TMEM load)
         tc_fence_before();
         if (CG == 2)
-          mbar_arrive_remote(&tempty[acc], 0);  // the leader's MMA reuses this accumulator
+          mbar_arrive_remote(&tempty[acc], leader_rank);  // the leader's MMA reuses this accumulator
         else
           mbar_arrive(&tempty[acc]);
       }
@@ -1081,8 +1199,15 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
     if (g->act == ACT_SOFTMAX_BWD && (!g->aux || g->ld_aux < (g->N + 15) / 16 * 16 || g->ld_aux % 8))
       return fail(MPX_EINVAL, "mpx_gemm: softmax backward needs aux = P with ld_aux >= round_up(N, 16)");
   }
+  const bool ln = g->ln_out != nullptr;
+  if (ln && (g->N != 3 * kBNMax || BN != kBNMax || split > 1 || nb1 * nb2 != 1 || g->act != ACT_NONE ||
+             !g->residual || g->b_mn_major || (g->c_dtype != MPX_F16 && g->c_dtype != MPX_BF16) || !g->ln_gain ||
+             !g->ln_bias || !g->ln_mean || !g->ln_rstd || g->ld_ln % 8 || g->tma_store < 0 ||
+             (g->cta_group != 0 && g->cta_group != 2)))
+    return fail(MPX_EINVAL, "mpx_gemm: the fused LayerNorm needs N = 768, K-major B, a residual epilogue (no act), "
+                            "batch 1, 16-bit C, no split-K, gain / bias / out / mean / rstd, ld_ln % 8 == 0");
   // CTA pair (M = 256 tiles) for the large problems; single CTA otherwise
-  int CG = g->cta_group;
+  int CG = ln ? 2 : g->cta_group;
   const bool pair_ok = (BN == 256 || BN == 128 || wide) && (!g->b_mn_major || BN % 128 == 0);
   if (CG == 0) CG = (pair_ok && (g->M >= 512 || wide)) ? 2 : 1;
   if (wide && CG != 2) return fail(MPX_EINVAL, "mpx_gemm: block_n 384 / 512 needs the CTA pair");
@@ -1224,18 +1349,33 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
     }
   }
   if (P.tma_store && P.xop == XOP_NONE && g->act == ACT_NONE && !g->residual && !no_xop) P.xop = XOP_PLAIN;
+  CUtensorMap tl = tb;  // the LayerNorm output (RES_LN), laid out like C
+  if (ln) {
+    if (P.xop != XOP_RES_IN || !P.tma_store)
+      return fail(MPX_EINVAL, "mpx_gemm: the fused LayerNorm needs the staged residual epilogue (aligned C / residual)");
+    P.xop = XOP_RES_LN;
+    const uint64_t s_l = (uint64_t)g->ld_ln * 2;
+    rc = make_map(&tl, g->ln_out, fmt, g->N, g->M, 1, 1, s_l, s_l * g->M, s_l * g->M, 64, 32);
+    if (rc) return rc;
+    P.ln_g = g->ln_gain;
+    P.ln_b = g->ln_bias;
+    P.ln_mean = g->ln_mean;
+    P.ln_rstd = g->ln_rstd;
+    P.ln_eps = g->ln_eps;
+    P.total_tiles = P.m_blocks;  // the cluster's pairs share each 256-row block
+  }
 
   using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
-                           const GemmParams);
-  static const KernelFn kernels[2][2][5] = {
+                           const CUtensorMap, const GemmParams);
+  static const KernelFn kernels[2][2][6] = {
       {{gemm_kernel<1, XOP_NONE, 0>, gemm_kernel<1, XOP_RES_IN, 0>, gemm_kernel<1, XOP_AUX_IN, 0>,
-        gemm_kernel<1, XOP_AUX_OUT, 0>, gemm_kernel<1, XOP_PLAIN, 0>},
+        gemm_kernel<1, XOP_AUX_OUT, 0>, gemm_kernel<1, XOP_PLAIN, 0>, nullptr},
        {gemm_kernel<2, XOP_NONE, 0>, gemm_kernel<2, XOP_RES_IN, 0>, gemm_kernel<2, XOP_AUX_IN, 0>,
-        gemm_kernel<2, XOP_AUX_OUT, 0>, gemm_kernel<2, XOP_PLAIN, 0>}},
+        gemm_kernel<2, XOP_AUX_OUT, 0>, gemm_kernel<2, XOP_PLAIN, 0>, gemm_kernel<2, XOP_RES_LN, 0>}},
       {{gemm_kernel<1, XOP_NONE, 1>, gemm_kernel<1, XOP_RES_IN, 1>, gemm_kernel<1, XOP_AUX_IN, 1>,
-        gemm_kernel<1, XOP_AUX_OUT, 1>, gemm_kernel<1, XOP_PLAIN, 1>},
+        gemm_kernel<1, XOP_AUX_OUT, 1>, gemm_kernel<1, XOP_PLAIN, 1>, nullptr},
        {gemm_kernel<2, XOP_NONE, 1>, gemm_kernel<2, XOP_RES_IN, 1>, gemm_kernel<2, XOP_AUX_IN, 1>,
-        gemm_kernel<2, XOP_AUX_OUT, 1>, gemm_kernel<2, XOP_PLAIN, 1>}}};
+        gemm_kernel<2, XOP_AUX_OUT, 1>, gemm_kernel<2, XOP_PLAIN, 1>, gemm_kernel<2, XOP_RES_LN, 1>}}};
   static const KernelFn wide_kernels[2][2] = {{gemm_kernel<2, XOP_PLAIN, 0, 1>, gemm_kernel<2, XOP_PLAIN, 1, 1>},
                                               {gemm_kernel<2, XOP_PLAIN, 0, 2>, gemm_kernel<2, XOP_PLAIN, 1, 2>}};
   // fused column sum: in the staged lean epilogues (16-bit C, one batch), else a separate pass
@@ -1257,23 +1397,25 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (CG == 1) {
     const long long grid = std::min<long long>(P.total_tiles, current_num_sms());
-    MPX_CUDA_CHECK(::mpx::launch_k(kern, (unsigned)grid, threads, kGemmSmem, st, ta, tb, tc, tx, P));
+    MPX_CUDA_CHECK(::mpx::launch_k(kern, (unsigned)grid, threads, kGemmSmem, st, ta, tb, tc, tx, tl, P));
   } else {
-    const long long pairs = std::min<long long>(P.total_tiles, current_num_sms() / 2);
+    // the LayerNorm variant: clusters of 3 CTA pairs, one 256-row block each
+    const int per = P.xop == XOP_RES_LN ? 6 : 2;
+    const long long units = std::min<long long>(P.total_tiles, current_num_sms() / per);
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(2 * pairs));
+    cfg.gridDim = dim3((unsigned)(per * units));
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = kGemmSmem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = per;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;  // (no PDL for the ViT kernels, see launch_k)
     count_launch();
-    MPX_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, P));
+    MPX_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tx, tl, P));
   }
   MPX_LAUNCH_CHECK("gemm_kernel");
   if (split > 1) {

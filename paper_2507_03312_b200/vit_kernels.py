@@ -22,7 +22,7 @@ def _ptr(t):
 def gemm(A, B, *, M, N, K, lda, ldb, a_mn=False, b_mn=False, out=None, ldc=None, out_dtype=None, bias=None,
          residual=None, ldr=None, aux=None, ld_aux=None, act=ACT_NONE, alpha=1.0, nb=(1, 1), a_sb=(0, 0),
          b_sb=(0, 0), c_sb=(0, 0), r_sb=(0, 0), split_k=1, workspace=None, block_n=0, cta_group=0,
-         tma_store=0, colsum_out=None, colsum_ws=None):
+         tma_store=0, colsum_out=None, colsum_ws=None, ln=None):
     """C = epi(alpha * A @ B) on the tcgen05 GEMM (see mpx_gemm_desc)."""
     require_cuda([A, B], "gemm")
     if A.dtype != B.dtype or A.dtype not in (torch.float16, torch.bfloat16):
@@ -58,6 +58,11 @@ def gemm(A, B, *, M, N, K, lda, ldb, a_mn=False, b_mn=False, out=None, ldc=None,
             colsum_ws = torch.empty(colsum_ws_numel(M, N), dtype=torch.float32, device=A.device)
         assert colsum_ws.dtype == torch.float32 and colsum_ws.numel() >= colsum_ws_numel(M, N)
         d.colsum_ws, d.colsum_out = colsum_ws.data_ptr(), colsum_out.data_ptr()
+    if ln is not None:  # (gain, bias, out, mean, rstd, eps): LayerNorm of the stored rows, fused
+        g_, b_, o_, mu_, rs_, eps_ = ln
+        d.ln_gain, d.ln_bias, d.ln_out = g_.data_ptr(), b_.data_ptr(), o_.data_ptr()
+        d.ld_ln = o_.stride(0)
+        d.ln_mean, d.ln_rstd, d.ln_eps = mu_.data_ptr(), rs_.data_ptr(), eps_
     _nat.check(_nat.load().mpx_gemm(ctypes.byref(d), stream_handle(A.device)), "mpx_gemm")
     return out
 
@@ -102,13 +107,15 @@ def transpose_batch(srcs, outs):
     return outs
 
 
-def linear_fwd_t(x, wt, bias=None, act=ACT_NONE, aux=None, residual=None, out=None, cta_group=0):
+def linear_fwd_t(x, wt, bias=None, act=ACT_NONE, aux=None, residual=None, out=None, cta_group=0, ln=None):
     """y[M,N] = x[M,K] @ wt[N,K]^T — the weight held transposed (K-major B,
-    faster than linear_fwd's MN-major read of w[K,N])."""
+    faster than linear_fwd's MN-major read of w[K,N]).  ln = (gain, bias,
+    out, mean, rstd, eps): also LN(y) over each whole row (N == 768, with a
+    residual), in the same kernel."""
     M, K = x.shape
     N_ = wt.shape[0]
     return gemm(x, wt, M=M, N=N_, K=K, lda=K, ldb=K, bias=bias, act=act, aux=aux, residual=residual,
-                out=out, ldc=N_ if out is not None else None, cta_group=cta_group)
+                out=out, ldc=N_ if out is not None else None, cta_group=cta_group, ln=ln)
 
 
 def linear_dgrad(dy, w, aux=None, out=None, cta_group=0, colsum_out=None, colsum_ws=None, aux_act=ACT_GELU_BWD):

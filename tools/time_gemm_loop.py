@@ -29,7 +29,27 @@ b2 = (torch.randn(K, device="cuda") * 0.1).to(bf)
 o2 = torch.empty(M, K, device="cuda", dtype=bf)
 xp = torch.randn(M, K, device="cuda").to(bf)  # proj forward: [M, 768] @ [768, 768] + b + residual
 wpt = (torch.randn(K, K, device="cuda") * 0.03).to(bf)
+from paper_2507_03312_b200 import _native as NN  # noqa: E402
+from paper_2507_03312_b200.kernels import stream_handle  # noqa: E402
+
+lg = torch.ones(K, device="cuda", dtype=bf)
+lb = torch.zeros(K, device="cuda", dtype=bf)
+ln_o = torch.empty(M, K, device="cuda", dtype=bf)
+mu = torch.empty(M, device="cuda")
+rs = torch.empty(M, device="cuda")
+
+
+def sep(xa, wa):  # residual GEMM, then the standalone LayerNorm kernel
+    VK.linear_fwd_t(xa, wa, bias=b2, residual=res, out=o2)
+    NN.check(NN.load().mpx_layernorm_fwd(2, o2.data_ptr(), K, lg.data_ptr(), lb.data_ptr(), ln_o.data_ptr(), K,
+                                         mu.data_ptr(), rs.data_ptr(), M, K, 1e-5, stream_handle(o2.device)), "ln")
+
+
 fns = {
+    "fc2_ln": lambda: VK.linear_fwd_t(x2, w2t, bias=b2, residual=res, out=o2, ln=(lg, lb, ln_o, mu, rs, 1e-5)),
+    "fc2_res_sep": lambda: sep(x2, w2t),
+    "proj_ln": lambda: VK.linear_fwd_t(xp, wpt, bias=b2, residual=res, out=o2, ln=(lg, lb, ln_o, mu, rs, 1e-5)),
+    "proj_res_sep": lambda: sep(xp, wpt),
     "fc2_res": lambda: VK.linear_fwd_t(x2, w2t, bias=b2, residual=res, out=o2, cta_group=cg),
     "proj_res": lambda: VK.linear_fwd_t(xp, wpt, bias=b2, residual=res, out=o2, cta_group=cg),
     "gelu_d": lambda: VK.linear_fwd_t(x, wt, bias=b, act=VK.ACT_GELU_D, aux=aux, out=y),
