@@ -492,10 +492,11 @@ __global__ void __launch_bounds__(kAttnThreadsF, 1)
         quarter_wait<kSplitF>(&bar[9], (g - 1) & 1, split, q);  // ... and its TMA store has read it
       }
       if (tr) ATRACE(4 + 8 * t);
-      if (live) {
-        softmax_store_p<kSplitF, KC, FMT>(split, r, P.N, st.y, a, sP);
-        if (P.stats != nullptr && split == 0) P.stats[((long long)item * T + t) * 128 + r] = st;
-      }
+      if (live) softmax_store_p<kSplitF, KC, FMT>(split, r, P.N, st.y, a, sP);
+      // every row's statistics, padding quarters included: (0, 0) makes the backward's
+      // recomputed P of those rows exactly 0 (they multiply dO rows that are zero, and
+      // garbage statistics would turn 0 * P into NaN in dV)
+      if (P.stats != nullptr && split == 0) P.stats[((long long)item * T + t) * 128 + r] = live ? st : make_float2(0.f, 0.f);
       fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core / TMA
       tc_fence_before();
       mbar_arrive(&bar[4]);

@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
   float2* lnq = reinterpret_cast<float2*>(stage_epi + kEpiStage + 512);
   float2* lnx = lnq + 4 * 2 * 32;
   uint64_t* lnbar = reinterpret_cast<uint64_t*>(lnx + 2 * 3 * 128);
+  float2* lngb = reinterpret_cast<float2*>(lnbar + 2);  // [256 columns] (gain, bias) of this CTA's columns
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
     }
     for (int i = 0; i < kEpiWarps; ++i) mbar_init(&ebar[i], 1);
     if (kLN)
-      for (int i = 0; i < 2; ++i) mbar_init(&lnbar[i], 3 * 128);  // 3 CTAs x 128 rows arrive per phase
+      for (int i = 0; i < 2; ++i) mbar_init(&lnbar[i], 1);  // this CTA's expect_tx + 3 x 128 x 8 B of st.async
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -290,6 +291,15 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
       tmem_alloc_2sm<512>(tmem_slot);
     else
       tmem_alloc<512>(tmem_slot);
+  }
+  if (kLN) {  // this CTA's 256 columns of the LayerNorm gain / bias, as f32, once (global reads before the
+              // PDL wait are fine: the parameters are not produced by the predecessor in the step graph)
+    for (int c = threadIdx.x; c < kBNMax; c += blockDim.x) {
+      const int col = (int)(crank >> 1) * kBNMax + c;
+      lngb[c] = col < P.N ? make_float2(half_to_f32(static_cast<const uint16_t*>(P.ln_g)[col], FMT),
+                                        half_to_f32(static_cast<const uint16_t*>(P.ln_b)[col], FMT))
+                          : make_float2(0.f, 0.f);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -659,7 +669,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
         // group fills both buffers and waits for all earlier stores)
         const int GW = (f32out || (kAuxOut && kAuxGW == 32)) ? 32 : 64;
         constexpr int cf = FMT;  // 16-bit C has the A/B format (checked on the host)
-        float ln_s1 = 0.f, ln_s2 = 0.f;  // RES_LN: this row's sum / sum of squares over this warp's columns
+        float2 ln_s1 = make_float2(0.f, 0.f), ln_s2 = make_float2(0.f, 0.f);  // RES_LN: this row's sums (pairs)
         const int n_groups = (P.BN + GW - 1) / GW;
         const int my_groups = n_groups > h ? (n_groups - h + kEpiPerQ - 1) / kEpiPerQ : 0;
         auto buf = [&](uint32_t c) { return obuf + (c % kBufPerWarp) * 4096; };
@@ -768,10 +778,10 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
               if (kLN) {  // row statistics of the ROUNDED stored values (the LayerNorm's input)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                  const float a = half_to_f32((uint16_t)(pk[i] & 0xFFFFu), FMT);
-                  const float b = half_to_f32((uint16_t)(pk[i] >> 16), FMT);
-                  ln_s1 += a + b;
-                  ln_s2 = fmaf(a, a, fmaf(b, b, ln_s2));
+                  const float2 ab = make_float2(half_to_f32((uint16_t)(pk[i] & 0xFFFFu), FMT),
+                                                half_to_f32((uint16_t)(pk[i] >> 16), FMT));
+                  ln_s1 = __fadd2_rn(ln_s1, ab);
+                  ln_s2 = __ffma2_rn(ab, ab, ln_s2);
                 }
               }
               *reinterpret_cast<uint4*>(rowp + (((2 * k) ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -845,9 +855,9 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
             if (!batched && kXin && j + 1 < my_groups) x_load(g + kEpiPerQ, gcount + 1);  // next group's operand
           }
         }
-        if (kLN) {
+        if (kLN && P.ln_eps >= 0.f) {  // (experiment: ln_eps < 0 = the cluster schedule without the LN work)
           // ---- LayerNorm of the stored rows.  (1) combine this quarter's warps
-          lnq[(q * kEpiPerQ + h) * 32 + lane] = make_float2(ln_s1, ln_s2);
+          lnq[(q * kEpiPerQ + h) * 32 + lane] = make_float2(ln_s1.x + ln_s1.y, ln_s2.x + ln_s2.y);
           asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * kEpiPerQ) : "memory");
           float2 part = make_float2(0.f, 0.f);
 #pragma unroll
@@ -861,16 +871,16 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
           // holding the same 128 rows (pair rank `rank` of each pair); slot by tile parity
           const int slot = (int)(ln_tiles & 1u);
           const int r = q * 32 + lane;
+          // (the phase completes when this CTA has armed it and all 3 x 128 partials have landed:
+          // st.async signals the destination's barrier itself — no cluster-scope fences)
+          if (warp == 2 && lane == 0) mbar_arrive_expect_tx(&lnbar[slot], 3u * 128u * 8u);
           if (h == 0) {
 #pragma unroll
-            for (int dst = 0; dst < 3; ++dst) {
-              const uint32_t target = 2u * dst + rank;
-              st_cluster_f2(lnx + (slot * 3 + (int)pr) * 128 + r, target, part);
-              mbar_arrive_remote_cluster(&lnbar[slot], target);
-            }
+            for (int dst = 0; dst < 3; ++dst)
+              st_async_f2(lnx + (slot * 3 + (int)pr) * 128 + r, 2u * dst + rank, part, &lnbar[slot]);
           }
           // (3) the whole row's statistics
-          mbar_wait_cluster(&lnbar[slot], (ln_tiles >> 1) & 1u);
+          mbar_wait(&lnbar[slot], (ln_tiles >> 1) & 1u);
           float s1 = 0.f, s2 = 0.f;
 #pragma unroll
           for (int src = 0; src < 3; ++src) {
@@ -894,24 +904,20 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
             const int cbase = n0 + (h + kEpiPerQ * j) * GW;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              float xv[16], gg[16], bb[16];
               const uint4 w0 = *reinterpret_cast<const uint4*>(rowp + (((2 * k) ^ sw) << 4));
               const uint4 w1 = *reinterpret_cast<const uint4*>(rowp + (((2 * k + 1) ^ sw) << 4));
               const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                xv[2 * e] = half_to_f32((uint16_t)(u[e] & 0xFFFFu), FMT);
-                xv[2 * e + 1] = half_to_f32((uint16_t)(u[e] >> 16), FMT);
-              }
-              load8(P.ln_g, cbase + k * 16, gg);
-              load8(P.ln_g, cbase + k * 16 + 8, gg + 8);
-              load8(P.ln_b, cbase + k * 16, bb);
-              load8(P.ln_b, cbase + k * 16 + 8, bb + 8);
+              const float4* gb = reinterpret_cast<const float4*>(lngb + (cbase - (int)pr * kBNMax) + k * 16);
               uint32_t pk[8];
 #pragma unroll
-              for (int e = 0; e < 8; ++e)
-                pk[e] = pack2_fmt((xv[2 * e] - mean) * rstd * gg[2 * e] + bb[2 * e],
-                                  (xv[2 * e + 1] - mean) * rstd * gg[2 * e + 1] + bb[2 * e + 1], FMT);
+              for (int e = 0; e < 8; ++e) {  // y = ((x - mean) rstd) g + b = (x rstd - mean rstd) g + b
+                const float2 xx = make_float2(half_to_f32((uint16_t)(u[e] & 0xFFFFu), FMT),
+                                              half_to_f32((uint16_t)(u[e] >> 16), FMT));
+                const float4 q4 = gb[e];  // (g, b) of columns 2e, 2e + 1
+                const float2 t = __ffma2_rn(xx, make_float2(rstd, rstd), make_float2(-mean * rstd, -mean * rstd));
+                const float2 y = __ffma2_rn(t, make_float2(q4.x, q4.z), make_float2(q4.y, q4.w));
+                pk[e] = pack2_fmt(y.x, y.y, FMT);
+              }
               *reinterpret_cast<uint4*>(rowp + (((2 * k) ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
               *reinterpret_cast<uint4*>(rowp + (((2 * k + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
             }
@@ -1399,10 +1405,29 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
     const long long grid = std::min<long long>(P.total_tiles, current_num_sms());
     MPX_CUDA_CHECK(::mpx::launch_k(kern, (unsigned)grid, threads, kGemmSmem, st, ta, tb, tc, tx, tl, P));
   } else {
-    // the LayerNorm variant: clusters of 3 CTA pairs, one 256-row block each
+    // the LayerNorm variant: clusters of 3 CTA pairs, one 256-row block each.  A
+    // 6-CTA cluster must fit in one GPC, so fewer than SMs / 6 may be co-resident:
+    // the persistent grid is sized by the occupancy query (a second wave of
+    // clusters would double the tail)
     const int per = P.xop == XOP_RES_LN ? 6 : 2;
-    const long long units = std::min<long long>(P.total_tiles, current_num_sms() / per);
+    long long slots = current_num_sms() / per;
     cudaLaunchConfig_t cfg{};
+    if (per == 6) {
+      cudaLaunchConfig_t q{};
+      q.gridDim = dim3((unsigned)(6 * slots));
+      q.blockDim = dim3(threads);
+      q.dynamicSmemBytes = kGemmSmem;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = 6;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, (const void*)kern, &q) == cudaSuccess && n > 0) slots = n;
+    }
+    const long long units = std::min<long long>(P.total_tiles, slots);
     cfg.gridDim = dim3((unsigned)(per * units));
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = kGemmSmem;

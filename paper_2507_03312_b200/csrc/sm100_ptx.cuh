@@ -121,6 +121,16 @@ __device__ __forceinline__ void st_cluster_f2(void* local, uint32_t rank, float2
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
   asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(remote), "f"(v.x), "f"(v.y) : "memory");
 }
+// asynchronous remote store that completes `8 bytes` of the remote CTA's
+// mbarrier transaction count when the data has landed (no fences needed)
+__device__ __forceinline__ void st_async_f2(void* local, uint32_t rank, float2 v, uint64_t* local_bar) {
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(local_bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(ra),
+               "f"(v.x), "f"(v.y), "r"(rb)
+               : "memory");
+}
 // arrive (release at cluster scope: orders this thread's st.shared::cluster before it)
 __device__ __forceinline__ void mbar_arrive_remote_cluster(uint64_t* bar, uint32_t rank) {
   uint32_t remote;

@@ -94,6 +94,10 @@ class ViTEngine:
         self.pre = [e(M, c.mlp) for _ in range(c.depth)]
         # MPX_GELU_SAVE_D=0: save the pre-activation instead and evaluate gelu' in the dgrad epilogue
         self.gelu_d = os.environ.get("MPX_GELU_SAVE_D", "1") == "1"
+        # LayerNorm folded into the residual GEMMs' epilogue (mpx_gemm_desc.ln_*, N = 768 only: a
+        # cluster of 3 CTA pairs per row block): proj -> LN2, fc2 -> the next block's LN1.
+        # MPX_LN_FOLD=0 runs the standalone LayerNorm kernel after each residual GEMM instead.
+        self.ln_fold = D == 768 and os.environ.get("MPX_LN_FOLD", "1") == "1"
         self.h = [e(M, c.mlp) for _ in range(c.depth)]  # GELU out
         f = lambda n: torch.empty(n, dtype=torch.float32, device=self.dev)  # noqa: E731
         self.mu1 = [f(M) for _ in range(c.depth)]
@@ -206,7 +210,8 @@ class ViTEngine:
         for i in range(c.depth):
             q = f"blocks.{i}."
             x, a, qkv = self.x[i], self.a[i], self.qkv[i]
-            self._ln_fwd(x, D, p[q + "ln1.g"], p[q + "ln1.b"], a, D, self.mu1[i], self.rs1[i], M)
+            if i == 0 or not self.ln_fold:  # (folded: block i-1's fc2 epilogue produced LN1(x) already)
+                self._ln_fwd(x, D, p[q + "ln1.g"], p[q + "ln1.b"], a, D, self.mu1[i], self.rs1[i], M)
             wt = self._wt[i]
             VK.linear_fwd_t(a, wt["qkv"], bias=p[q + "qkv.b"], out=qkv)
             O = self.O[i]
@@ -223,12 +228,22 @@ class ViTEngine:
                 VK.gemm(P_, qkv[:, 2 * D:], M=S, N=hd, K=S, lda=self.ldS, ldb=3 * D, b_mn=True, nb=(H, B),
                         a_sb=(S * self.ldS, H * S * self.ldS), b_sb=(hd, S * 3 * D), out=O, ldc=D, c_sb=(hd, S * D))
             xm = self.xm[i]
-            VK.linear_fwd_t(O, wt["proj"], bias=p[q + "proj.b"], residual=x, out=xm)
             bn = self.bn[i]
-            self._ln_fwd(xm, D, p[q + "ln2.g"], p[q + "ln2.b"], bn, D, self.mu2[i], self.rs2[i], M)
+            if self.ln_fold:  # xm = O Wp + bp + x and bn = LN2(xm) in one kernel
+                VK.linear_fwd_t(O, wt["proj"], bias=p[q + "proj.b"], residual=x, out=xm,
+                                ln=(p[q + "ln2.g"], p[q + "ln2.b"], bn, self.mu2[i], self.rs2[i], LN_EPS))
+            else:
+                VK.linear_fwd_t(O, wt["proj"], bias=p[q + "proj.b"], residual=x, out=xm)
+                self._ln_fwd(xm, D, p[q + "ln2.g"], p[q + "ln2.b"], bn, D, self.mu2[i], self.rs2[i], M)
             VK.linear_fwd_t(bn, wt["fc1"], bias=p[q + "fc1.b"], act=VK.ACT_GELU_D if self.gelu_d else VK.ACT_GELU,
                             aux=self.pre[i], out=self.h[i])
-            VK.linear_fwd_t(self.h[i], wt["fc2"], bias=p[q + "fc2.b"], residual=xm, out=self.x[i + 1])
+            if self.ln_fold and i + 1 < c.depth:  # x_{i+1} and the next block's LN1 in one kernel
+                n = f"blocks.{i + 1}."
+                VK.linear_fwd_t(self.h[i], wt["fc2"], bias=p[q + "fc2.b"], residual=xm, out=self.x[i + 1],
+                                ln=(p[n + "ln1.g"], p[n + "ln1.b"], self.a[i + 1], self.mu1[i + 1], self.rs1[i + 1],
+                                    LN_EPS))
+            else:
+                VK.linear_fwd_t(self.h[i], wt["fc2"], bias=p[q + "fc2.b"], residual=xm, out=self.x[i + 1])
         xl = self.x[c.depth]
         if cls:
             self._ln_fwd(xl, S * D, p["ln_f.g"], p["ln_f.b"], self.fin, D, self.muf, self.rsf, B)

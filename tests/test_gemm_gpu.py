@@ -133,7 +133,8 @@ def test_fused_attention_backward(cuda, dt, Nt):
     dO = torch.randn(Bsz * Nt, D, device=cuda, generator=g).to(dt)
     dqkv = VK.attention_bwd(qkv, dO, Bsz, Nt, H, hd, 0.125)
     # with the forward's row statistics P is rebuilt bit-identically
-    stats = torch.empty(VK.attention_stats_numel(Bsz, Nt, H), device=cuda)
+    # NaN-filled: every entry the backward reads must have been written by the forward
+    stats = torch.full((VK.attention_stats_numel(Bsz, Nt, H),), float("nan"), device=cuda)
     VK.attention_fwd(qkv, Bsz, Nt, H, hd, 0.125, stats=stats)
     assert torch.equal(VK.attention_bwd(qkv, dO, Bsz, Nt, H, hd, 0.125, stats=stats), dqkv)
     # fused bias gradient: colsum over the stored dqkv rows

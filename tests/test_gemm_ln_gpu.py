@@ -19,7 +19,7 @@ CODE = {torch.float16: 1, torch.bfloat16: 2}
 
 
 @pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
-@pytest.mark.parametrize("M,K", [(50432, 768), (1536, 3072), (300, 768), (256, 768), (2000, 768)])
+@pytest.mark.parametrize("M,K", [(50432, 768), (1536, 3072), (300, 768), (256, 768), (2000, 768), (68, 768), (1, 768)])
 def test_fused_layernorm_matches_separate(cuda, dt, M, K):
     D = 768
     g = torch.Generator(device=cuda).manual_seed(M + K)

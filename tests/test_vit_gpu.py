@@ -53,6 +53,8 @@ CFGS = {
     "tiny-mean": VIT_TINY,
     "small-cls": ViTConfig(img=32, patch=4, dim=128, depth=2, heads=2, mlp=256, classes=16, pool="cls"),
     "vitb-shape": ViTConfig(img=64, patch=16, dim=768, depth=1, heads=12, mlp=3072, classes=1000, pool="cls"),
+    # depth 2 at width 768: both LayerNorm folds (proj -> LN2, fc2 -> the next block's LN1)
+    "vitb-shape-d2": ViTConfig(img=64, patch=16, dim=768, depth=2, heads=12, mlp=3072, classes=1000, pool="cls"),
 }
 
 

@@ -50,6 +50,9 @@ fns = {
     "fc2_res_sep": lambda: sep(x2, w2t),
     "proj_ln": lambda: VK.linear_fwd_t(xp, wpt, bias=b2, residual=res, out=o2, ln=(lg, lb, ln_o, mu, rs, 1e-5)),
     "proj_res_sep": lambda: sep(xp, wpt),
+    "fc2_ln_dry": lambda: VK.linear_fwd_t(x2, w2t, bias=b2, residual=res, out=o2, ln=(lg, lb, ln_o, mu, rs, -1.0)),
+    "proj_ln_dry": lambda: VK.linear_fwd_t(xp, wpt, bias=b2, residual=res, out=o2, ln=(lg, lb, ln_o, mu, rs, -1.0)),
+    "fc2_res": lambda: VK.linear_fwd_t(x2, w2t, bias=b2, residual=res, out=o2),
     "fc2_res": lambda: VK.linear_fwd_t(x2, w2t, bias=b2, residual=res, out=o2, cta_group=cg),
     "proj_res": lambda: VK.linear_fwd_t(xp, wpt, bias=b2, residual=res, out=o2, cta_group=cg),
     "gelu_d": lambda: VK.linear_fwd_t(x, wt, bias=b, act=VK.ACT_GELU_D, aux=aux, out=y),
