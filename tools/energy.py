@@ -174,16 +174,21 @@ def main():
     wt = e._wt[0]
     scale = hd ** -0.5
     items = [
-        ("ln_fwd", 25, lambda: e._ln_fwd(e.x[0], D, P[q + "ln1.g"], P[q + "ln1.b"], e.a[0], D, e.mu1[0], e.rs1[0], M)),
+        ("ln_fwd (standalone: block 0's LN1, ln_f)", 2 if e.ln_fold else 25,
+         lambda: e._ln_fwd(e.x[0], D, P[q + "ln1.g"], P[q + "ln1.b"], e.a[0], D, e.mu1[0], e.rs1[0], M)),
         ("qkv fwd GEMM (+bias)", 12, lambda: VK.linear_fwd_t(e.a[0], wt["qkv"], bias=P[q + "qkv.b"], out=e.qkv[0])),
         ("attention fwd (P saved)", 12, lambda: VK.attention_fwd(e.qkv[0], B, S, H, hd, scale, out=e.O[0],
                                                                   p_save=e.attn_p[0])),
-        ("proj fwd GEMM (+bias+res)", 12, lambda: VK.linear_fwd_t(e.O[0], wt["proj"], bias=P[q + "proj.b"],
-                                                                  residual=e.x[0], out=e.xm[0])),
+        ("proj fwd GEMM (+bias+res" + (", +LN2 fused)" if e.ln_fold else ")"), 12,
+         lambda: VK.linear_fwd_t(e.O[0], wt["proj"], bias=P[q + "proj.b"], residual=e.x[0], out=e.xm[0],
+                                 ln=(P[q + "ln2.g"], P[q + "ln2.b"], e.bn[0], e.mu2[0], e.rs2[0], 1e-5)
+                                 if e.ln_fold else None)),
         ("fc1 fwd GEMM (+bias, GELU, aux out)", 12,
          lambda: VK.linear_fwd_t(e.bn[0], wt["fc1"], bias=P[q + "fc1.b"], act=VK.ACT_GELU_D, aux=e.pre[0], out=e.h[0])),
-        ("fc2 fwd GEMM (+bias+res)", 12, lambda: VK.linear_fwd_t(e.h[0], wt["fc2"], bias=P[q + "fc2.b"],
-                                                                 residual=e.xm[0], out=e.x[1])),
+        ("fc2 fwd GEMM (+bias+res" + (", +next LN1 fused)" if e.ln_fold else ")"), 12,
+         lambda: VK.linear_fwd_t(e.h[0], wt["fc2"], bias=P[q + "fc2.b"], residual=e.xm[0], out=e.x[1],
+                                 ln=(P["blocks.1.ln1.g"], P["blocks.1.ln1.b"], e.a[1], e.mu1[1], e.rs1[1], 1e-5)
+                                 if e.ln_fold else None)),
         ("fc2 wgrad GEMM", 12, lambda: VK.linear_wgrad(e.h[0], e.dX, out=G[q + "fc2.w"])),
         ("fc2 dgrad GEMM (GELU' aux in, colsum)", 12,
          lambda: VK.linear_dgrad(e.dX, P[q + "fc2.w"], aux=e.pre[0], out=e.dpre, colsum_out=G[q + "fc1.b"],
