@@ -22,6 +22,9 @@ b = (torch.randn(N, device="cuda") * 0.1).to(bf)
 y = torch.empty(M, N, device="cuda", dtype=bf)
 aux = torch.randn(M, N, device="cuda").to(bf)
 cg = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+b_cs = torch.empty(N, device="cuda", dtype=bf)
+w2 = (torch.randn(N, K, device="cuda") * 0.02).to(bf)  # W2 [3072, 768]
+ws_cs = torch.empty(((M + 31) // 32) * N, device="cuda")
 x2 = torch.randn(M, N, device="cuda").to(bf)  # fc2 forward: [M, 3072] @ [3072, 768] + b + residual
 w2t = (torch.randn(K, N, device="cuda") * 0.02).to(bf)
 res = torch.randn(M, K, device="cuda").to(bf)
@@ -59,6 +62,9 @@ fns = {
     "gelu": lambda: VK.linear_fwd_t(x, wt, bias=b, act=VK.ACT_GELU, aux=aux, out=y),
     "bare": lambda: VK.linear_fwd_t(x, wt, out=y),
     "mul_aux": lambda: VK.linear_dgrad(aux, w, aux=y, out=x, aux_act=VK.ACT_MUL_AUX),
+    # the fc2 dgrad as the engine runs it: dpre[M, 3072] = dX[M, 768] @ W2^T, x the saved gelu', + colsum
+    "fc2_dgrad": lambda: VK.linear_dgrad(res, w2, aux=aux, out=y, aux_act=VK.ACT_MUL_AUX, colsum_out=b_cs,
+                                         colsum_ws=ws_cs),
 }
 n, ms, j, wts, mhz = Meter(0).run(fns[mode], secs)
 print(json.dumps({"mode": mode, "us": round(ms * 1e3, 2), "mJ": round(j * 1e3, 2), "W": round(wts, 1), "sm_mhz": mhz}))
