@@ -84,6 +84,14 @@ static_assert(4 * (kATileBytes + kBTileBytes) <= 6 * (kATileBytes + kBTileBytes 
 enum { ACT_NONE = 0, ACT_GELU = 1, ACT_GELU_BWD = 2, ACT_SOFTMAX = 3, ACT_SOFTMAX_BWD = 4, ACT_GELU_D = 5,
        ACT_MUL_AUX = 6 };
 
+// n / d for 0 <= n < 2^31 by a multiply-high, an add and a shift (d >= 1
+// fixed per launch, m and s from make_fastdiv on the host): the per-tile raster
+// arithmetic every warp repeats for every tile, without integer divisions
+struct FastDiv {
+  uint32_t d, m, s;
+};
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.m) + n) >> f.s; }
+
 struct GemmParams {
   int M, N, K, BN;
   int N_store;     // N rounded up to 8: stores cover whole 8-column groups
@@ -92,6 +100,7 @@ struct GemmParams {
   int a_bc1, a_bc2, b_bc1, b_bc2;  // operand shared across that batch dim (coordinate 0)
   int m_blocks, n_blocks, k_blocks, kb_per_split;
   long long total_tiles;
+  FastDiv fd_mn, fd_split, fd_grp, fd_gmt, fd_nb1;  // m_blocks*n_blocks, split, kGroupM*n_blocks, tail group, nb1
   uint32_t idesc;
   uint32_t idesc2;  // WN variants: the second MMA of each K step (N = 128 at 384 wide, 256 at 512)
   int ab_fmt;  // 0 = f16, 1 = bf16 (also the dtype of bias/residual/aux)
@@ -191,19 +200,29 @@ __device__ __forceinline__ float2 gelu_grad2(float2 x) {
 struct TileCoord {
   int z, s, m_blk, n_blk;
 };
-__device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, long long t) {
-  const long long per_mn = (long long)P.m_blocks * P.n_blocks;
-  const long long zs = t / per_mn;
-  const int r = (int)(t - zs * per_mn);
+// tile t -> (batch z, split s, m block, n block): groups of kGroupM m-blocks,
+// m fastest inside a group (t < 2^31, checked on the host)
+__device__ __forceinline__ TileCoord tile_coord(const GemmParams& P, long long t64) {
+  const uint32_t t = (uint32_t)t64;
+  const uint32_t zs = fdiv(t, P.fd_mn);
+  const uint32_t r = t - zs * P.fd_mn.d;
   TileCoord c;
-  c.z = (int)(zs / P.split);
-  c.s = (int)(zs - (long long)c.z * P.split);
-  const int group = r / (kGroupM * P.n_blocks);
-  const int first_m = group * kGroupM;
-  const int gm = min(kGroupM, P.m_blocks - first_m);
-  const int in = r - group * kGroupM * P.n_blocks;
-  c.m_blk = first_m + in % gm;
-  c.n_blk = in / gm;
+  const uint32_t z = fdiv(zs, P.fd_split);
+  c.z = (int)z;
+  c.s = (int)(zs - z * P.fd_split.d);
+  const uint32_t group = fdiv(r, P.fd_grp);
+  const uint32_t first_m = group * kGroupM;
+  const uint32_t in = r - group * P.fd_grp.d;
+  uint32_t q, gm;
+  if (first_m + kGroupM <= (uint32_t)P.m_blocks) {  // a full group: constant divisor
+    q = in / kGroupM;
+    gm = kGroupM;
+  } else {  // the last, partial group
+    q = fdiv(in, P.fd_gmt);
+    gm = P.fd_gmt.d;
+  }
+  c.m_blk = (int)(first_m + (in - q * gm));
+  c.n_blk = (int)q;
   return c;
 }
 
@@ -321,7 +340,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
       uint32_t phase = 0;
       for (long long t = t_first; t < P.total_tiles; t += t_step) {
         const TileCoord tc = kLN ? TileCoord{0, 0, (int)t, (int)pr} : tile_coord(P, t);
-        const int b1 = tc.z % P.nb1, b2 = tc.z / P.nb1;
+        const int b2 = (int)fdiv((uint32_t)tc.z, P.fd_nb1), b1 = tc.z - b2 * P.nb1;
         const int m0 = tc.m_blk * (kBM * CG) + (int)rank * kBM;
         const int n0 = tc.n_blk * P.BN + (WN ? 0 : (int)rank * bn_cta);
         const int kb0 = tc.s * P.kb_per_split;
@@ -434,7 +453,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
     uint32_t acc_phase = 0;
     for (long long t = t_first; t < P.total_tiles; t += t_step) {
       const TileCoord tc = kLN ? TileCoord{0, 0, (int)t, (int)pr} : tile_coord(P, t);
-      const int b1 = tc.z % P.nb1, b2 = tc.z / P.nb1;
+      const int b2 = (int)fdiv((uint32_t)tc.z, P.fd_nb1), b1 = tc.z - b2 * P.nb1;
       const int row0 = tc.m_blk * (kBM * CG) + (int)rank * kBM + q * 32;
       const int row = row0 + lane;
       const int n0 = tc.n_blk * P.BN;
@@ -1171,6 +1190,13 @@ static int make_map_dt(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, 
   return 0;
 }
 
+// round-up multiplier for fdiv (s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1;
+// exact for every n < 2^31 — checked exhaustively on small d and at the n edges)
+static FastDiv make_fastdiv(uint32_t d) {
+  uint32_t s = 0;
+  while ((1ull << s) < d) ++s;
+  return FastDiv{d, (uint32_t)(((1ull << 32) * ((1ull << s) - d)) / d + 1), s};
+}
 static uint64_t nz_stride(int64_t s, uint64_t fallback) { return s > 0 ? (uint64_t)s : fallback; }
 static uint64_t ext(int64_t s, int n) { return s > 0 ? (uint64_t)n : 1u; }
 
@@ -1260,6 +1286,12 @@ extern "C" int mpx_gemm(const mpx_gemm_desc* g, void* stream) {
   P.k_blocks = (g->K + kBK - 1) / kBK;
   P.kb_per_split = (P.k_blocks + split - 1) / split;
   P.total_tiles = (long long)P.nbatch * split * P.m_blocks * P.n_blocks;
+  if (P.total_tiles >= (1ll << 31)) return fail(MPX_EINVAL, "mpx_gemm: more than 2^31 - 1 output tiles");
+  P.fd_mn = make_fastdiv((uint32_t)(P.m_blocks * P.n_blocks));
+  P.fd_split = make_fastdiv((uint32_t)split);
+  P.fd_grp = make_fastdiv((uint32_t)(kGroupM * P.n_blocks));
+  P.fd_gmt = make_fastdiv(P.m_blocks % kGroupM ? (uint32_t)(P.m_blocks % kGroupM) : 1u);
+  P.fd_nb1 = make_fastdiv((uint32_t)nb1);
   P.idesc = ptx::idesc_f16(fmt, kBM * CG, wide ? 256 : BN, g->a_mn_major, g->b_mn_major);
   P.idesc2 = ptx::idesc_f16(fmt, kBM * CG, wn == 2 ? 256 : 128, g->a_mn_major, g->b_mn_major);
   P.ab_fmt = fmt;
