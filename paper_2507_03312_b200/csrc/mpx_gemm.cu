@@ -197,6 +197,25 @@ __device__ __forceinline__ float2 gelu_grad2(float2 x) {
   return __ffma2_rn(__fmul2_rn(__fmul2_rn(x, f2(0.5f)), sech2), k, a);
 }
 
+template <int F>
+__device__ __forceinline__ float2 unpack2_fmt(uint32_t w) {  // (lo, hi) halves of w, exactly
+  if (F) return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+  return __half22float2(*reinterpret_cast<const __half2*>(&w));
+}
+// acc + the two half values packed in w (lo, hi): the conversion is exact and the
+// add rounds once, so this equals unpack-then-FADD bit for bit, in one FHADD each
+template <int F>
+__device__ __forceinline__ float2 add_h2(float2 acc, uint32_t w) {
+  float2 d;
+  if (F)
+    asm("{.reg .b16 lo, hi; mov.b32 {lo, hi}, %2;\n add.rn.f32.bf16 %0, lo, %3;\n add.rn.f32.bf16 %1, hi, %4;}"
+        : "=f"(d.x), "=f"(d.y) : "r"(w), "f"(acc.x), "f"(acc.y));
+  else
+    asm("{.reg .b16 lo, hi; mov.b32 {lo, hi}, %2;\n add.rn.f32.f16 %0, lo, %3;\n add.rn.f32.f16 %1, hi, %4;}"
+        : "=f"(d.x), "=f"(d.y) : "r"(w), "f"(acc.x), "f"(acc.y));
+  return d;
+}
+
 struct TileCoord {
   int z, s, m_blk, n_blk;
 };
@@ -808,6 +827,112 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
             }
           }
         };
+        // stage_group for the common case, everything known at compile time: a whole
+        // 64-column group inside N, 16-bit C, alpha 1, a lean variant (bias / residual /
+        // GELU' operand; half operands added by mixed-precision FHADD).  Rows past M run the same math (their A rows are TMA zero-fill,
+        // staged operands too; the TMA store clips them and the column sum skips them)
+        auto stage_full = [&](int g, uint8_t* bb, bool last) {  // (alpha == 1)
+          uint8_t* rowp = bb + lane * 128;
+          const int sw = lane & 7;
+          const uint16_t* bias = static_cast<const uint16_t*>(P.bias);
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {  // two chunks per TMEM wait (register budget)
+            uint32_t r[2][16];
+            tmem_ld16(taddr + g * GW + half * 32, r[0]);
+            tmem_ld16(taddr + g * GW + half * 32 + 16, r[1]);
+            tmem_ld_wait();
+            if (last && half == 1) release_acc();
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              const int k = 2 * half + kk;
+              float2 v[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                v[i] = make_float2(__uint_as_float(r[kk][2 * i]), __uint_as_float(r[kk][2 * i + 1]));
+              if (bias != nullptr) {
+                const uint4 b0 = *reinterpret_cast<const uint4*>(bias + n0 + g * GW + k * 16);
+                const uint4 b1_ = *reinterpret_cast<const uint4*>(bias + n0 + g * GW + k * 16 + 8);
+                const uint32_t bw[8] = {b0.x, b0.y, b0.z, b0.w, b1_.x, b1_.y, b1_.z, b1_.w};
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = add_h2<FMT>(v[i], bw[i]);
+              }
+              uint4* p0 = reinterpret_cast<uint4*>(rowp + (((2 * k) ^ sw) << 4));
+              uint4* p1 = reinterpret_cast<uint4*>(rowp + (((2 * k + 1) ^ sw) << 4));
+              if (kXin) {  // own row of the staged operand
+                const uint4 w0 = *p0, w1 = *p1;
+                const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+                if (XO == XOP_RES_IN || XO == XOP_RES_LN) {
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) v[i] = add_h2<FMT>(v[i], u[i]);
+                } else if (P.act == ACT_MUL_AUX) {  // XOP_AUX_IN: the saved GELU derivative
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) v[i] = __fmul2_rn(v[i], unpack2_fmt<FMT>(u[i]));
+                } else {  // XOP_AUX_IN: gelu' of the saved pre-activation
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) v[i] = __fmul2_rn(v[i], gelu_grad2(unpack2_fmt<FMT>(u[i])));
+                }
+              }
+              uint32_t pk[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) pk[i] = pack2_fmt(v[i].x, v[i].y, cf);
+              if (kLN) {  // row statistics of the ROUNDED stored values (the LayerNorm's input)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const float2 ab = unpack2_fmt<FMT>(pk[i]);
+                  ln_s1 = __fadd2_rn(ln_s1, ab);
+                  ln_s2 = __ffma2_rn(ab, ab, ln_s2);
+                }
+              }
+              *p0 = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              *p1 = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            }
+          }
+        };
+        // the same for the GELU-aux-out groups (32 columns, SW64, aux + C in one buffer)
+        auto stage_full_aux = [&](int g, uint8_t* bb, bool last) {  // (alpha == 1, kAuxGW == 32)
+          uint32_t r[2][16];
+          tmem_ld16(taddr + g * GW, r[0]);
+          tmem_ld16(taddr + g * GW + 16, r[1]);
+          tmem_ld_wait();
+          if (last) release_acc();
+          const uint16_t* bias = static_cast<const uint16_t*>(P.bias);
+          const bool dout = P.act == ACT_GELU_D;
+          const int s64 = (lane >> 1) & 3;
+          uint8_t* ra = bb + lane * 64;
+          uint8_t* rc = ra + 2048;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            float2 v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = make_float2(__uint_as_float(r[k][2 * i]), __uint_as_float(r[k][2 * i + 1]));
+            if (bias != nullptr) {
+              const uint4 b0 = *reinterpret_cast<const uint4*>(bias + n0 + g * GW + k * 16);
+              const uint4 b1_ = *reinterpret_cast<const uint4*>(bias + n0 + g * GW + k * 16 + 8);
+              const uint32_t bw[8] = {b0.x, b0.y, b0.z, b0.w, b1_.x, b1_.y, b1_.z, b1_.w};
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[i] = add_h2<FMT>(v[i], bw[i]);
+            }
+            uint32_t pa[8], pc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              pa[i] = pack2_fmt(v[i].x, v[i].y, FMT);  // the rounded pre-activation
+              const float2 ab = unpack2_fmt<FMT>(pa[i]);
+              if (dout) {  // aux = the rounded derivative, from the same tanh as the GELU
+                float2 y, d;
+                gelu_and_grad2(ab, y, d);
+                pc[i] = pack2_fmt(y.x, y.y, cf);
+                pa[i] = pack2_fmt(d.x, d.y, FMT);
+              } else {
+                const float2 y = gelu2(ab);
+                pc[i] = pack2_fmt(y.x, y.y, cf);
+              }
+            }
+            *reinterpret_cast<uint4*>(ra + (((2 * k) ^ s64) << 4)) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+            *reinterpret_cast<uint4*>(ra + (((2 * k + 1) ^ s64) << 4)) = make_uint4(pa[4], pa[5], pa[6], pa[7]);
+            *reinterpret_cast<uint4*>(rc + (((2 * k) ^ s64) << 4)) = make_uint4(pc[0], pc[1], pc[2], pc[3]);
+            *reinterpret_cast<uint4*>(rc + (((2 * k + 1) ^ s64) << 4)) = make_uint4(pc[4], pc[5], pc[6], pc[7]);
+          }
+        };
         auto store_group = [&](int g, uint8_t* bb) {  // lane 0
           if (P.split > 1) {
             tma_store_4d(&tmC, bb, n0 + g * GW, row0, tc.s, 0);
@@ -860,7 +985,15 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
             }
             __syncwarp();
           }
-          stage_group(g, nch, bb, j == my_groups - 1);
+          constexpr bool kFast = (XO == XOP_PLAIN || XO == XOP_RES_IN || XO == XOP_AUX_IN || XO == XOP_RES_LN) &&
+                                 kEpiWarps <= 8;
+          if (kFast && GW == 64 && nch == 4 && n0 + g * GW + 64 <= P.N && P.alpha == 1.f)
+            stage_full(g, bb, j == my_groups - 1);
+          else if (kAuxOut && kAuxGW == 32 && kEpiWarps <= 8 && GW == 32 && nch == 2 && n0 + g * GW + 32 <= P.N &&
+                   P.alpha == 1.f)
+            stage_full_aux(g, bb, j == my_groups - 1);
+          else
+            stage_group(g, nch, bb, j == my_groups - 1);
           if (batched && j + 1 < my_groups) continue;
           fence_async_smem();
           __syncwarp();
@@ -957,14 +1090,19 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
             const int g = h + kEpiPerQ * j;
             const int nch = min(GW / 16, (P.BN - g * GW) / 16);
             const uint32_t base = smem_u32(buf(j)) + ((lane & 3) << 2);
-            float s0 = 0.f, s1 = 0.f;
-#pragma unroll 8
-            for (int rr = 0; rr < 32; ++rr) {
+            float2 s = make_float2(0.f, 0.f);
+            auto add_row = [&](int rr) {
               uint32_t w;
               asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w) : "r"(base + rr * 128 + (((lane >> 2) ^ (rr & 7)) << 4)));
-              s0 += half_to_f32((uint16_t)(w & 0xFFFFu), cf);
-              s1 += half_to_f32((uint16_t)(w >> 16), cf);
+              s = add_h2<cf>(s, w);  // (mixed-precision adds: the same sums as unpack + FADD)
+            };
+            if (row0 + 32 <= P.M) {
+#pragma unroll 8
+              for (int rr = 0; rr < 32; ++rr) add_row(rr);
+            } else {  // rows past M hold no data (the fast path stages them)
+              for (int rr = 0; rr < P.M - row0; ++rr) add_row(rr);
             }
+            const float s0 = s.x, s1 = s.y;
             const int col = n0 + g * GW + 2 * lane;
             if (2 * lane < nch * 16 && col < P.N) {
               float* o = P.csum + (long long)(row0 >> 5) * P.N + col;
