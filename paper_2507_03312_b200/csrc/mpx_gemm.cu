@@ -168,23 +168,24 @@ __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float2 gelu2(float2 x) {
   const float c0 = 0.7978845608028654f, c1 = 0.044715f;
   const float2 x2 = __fmul2_rn(x, x);
-  const float2 u = __fmul2_rn(__fmul2_rn(x, __ffma2_rn(x2, f2(c1), f2(1.f))), f2(c0));
+  const float2 u = __fmul2_rn(x, __ffma2_rn(x2, f2(c0 * c1), f2(c0)));  // x c0 (1 + c1 x^2)
   const float2 th = make_float2(tanh_fast(u.x), tanh_fast(u.y));
   const float2 hx = __fmul2_rn(x, f2(0.5f));
   return __ffma2_rn(hx, th, hx);
 }
-// GELU and its derivative from one tanh (ACT_GELU_D)
+// GELU and its derivative from one tanh (ACT_GELU_D): with y = x/2 (1 + t),
+// d = (1 + t)/2 + x/2 (1 - t^2) k = (1 + t)/2 + (y - y t) k, k = c0 (1 + 3 c1 x^2)
 __device__ __forceinline__ void gelu_and_grad2(float2 x, float2& y, float2& d) {
   const float c0 = 0.7978845608028654f, c1 = 0.044715f;
   const float2 x2 = __fmul2_rn(x, x);
-  const float2 u = __fmul2_rn(__fmul2_rn(x, __ffma2_rn(x2, f2(c1), f2(1.f))), f2(c0));
+  const float2 u = __fmul2_rn(x, __ffma2_rn(x2, f2(c0 * c1), f2(c0)));
   const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
   const float2 hx = __fmul2_rn(x, f2(0.5f));
   y = __ffma2_rn(hx, t, hx);
   const float2 a = __ffma2_rn(t, f2(0.5f), f2(0.5f));                      // 0.5 (1 + t)
-  const float2 sech2 = __ffma2_rn(make_float2(-t.x, -t.y), t, f2(1.f));    // 1 - t^2
+  const float2 ymt = __ffma2_rn(make_float2(-y.x, -y.y), t, y);            // y (1 - t) = x/2 (1 - t^2)
   const float2 k = __ffma2_rn(x2, f2(3.f * c0 * c1), f2(c0));              // c0 (1 + 3 c1 x^2)
-  d = __ffma2_rn(__fmul2_rn(hx, sech2), k, a);
+  d = __ffma2_rn(ymt, k, a);
 }
 __device__ __forceinline__ float2 gelu_grad2(float2 x) {
   const float c0 = 0.7978845608028654f, c1 = 0.044715f;
@@ -410,6 +411,14 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      // SW128 descriptors = constant fields + (smem address >> 4) in the low 14 bits: the
+      // per-stage bases and per-k16 steps are 32-bit adds on the low word (no re-packing)
+      const uint64_t a_desc0 = sw128_desc(smem_u32(sA), P.a_mn ? 8192 : 16, 1024);
+      const uint64_t b_desc0 = sw128_desc(smem_u32(sB), P.b_mn ? 8192 : 16, 1024);
+      const uint64_t b2_desc0 = sw128_desc(smem_u32(sB) + 2 * 8192, 8192, 1024);  // WN: the second MMA's B (MN-major)
+      const uint32_t a_hi = (uint32_t)(a_desc0 >> 32), b_hi = (uint32_t)(b_desc0 >> 32);
+      const uint32_t b2_hi = (uint32_t)(b2_desc0 >> 32);
+      const uint32_t a_kstep = P.a_mn ? 2048 >> 4 : 32 >> 4, b_kstep = P.b_mn ? 2048 >> 4 : 32 >> 4;
       for (long long t = t_first; t < P.total_tiles; t += t_step) {
         const TileCoord tc = kLN ? TileCoord{0, 0, (int)t, (int)pr} : tile_coord(P, t);
         const int kb0 = tc.s * P.kb_per_split;
@@ -420,20 +429,20 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a = smem_u32(sA + stage * kATileBytes);
-          const uint32_t b = smem_u32(sB + stage * BT);
+          const uint32_t as = (uint32_t)a_desc0 + (uint32_t)(stage * kATileBytes >> 4);
+          const uint32_t bs = (uint32_t)b_desc0 + (uint32_t)(stage * BT >> 4);
+          const uint32_t b2s = (uint32_t)b2_desc0 + (uint32_t)(stage * BT >> 4);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t ad = P.a_mn ? sw128_desc(a + k * 2048, 8192, 1024) : sw128_desc(a + k * 32, 16, 1024);
-            const uint64_t bd = P.b_mn ? sw128_desc(b + k * 2048, 8192, 1024) : sw128_desc(b + k * 32, 16, 1024);
+            const uint32_t acc_in = (kb > kb0 || k > 0) ? 1u : 0u;
+            const uint32_t ad = as + k * a_kstep, bd = bs + k * b_kstep;
             if (WN) {
-              umma_f16_2sm(d, ad, bd, P.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-              umma_f16_2sm(d + 256, ad, sw128_desc(b + 2 * 8192 + k * 2048, 8192, 1024), P.idesc2,
-                           (kb > kb0 || k > 0) ? 1u : 0u);
+              umma_f16_2sm_w(d, ad, a_hi, bd, b_hi, P.idesc, acc_in);
+              umma_f16_2sm_w(d + 256, ad, a_hi, b2s + k * (2048 >> 4), b2_hi, P.idesc2, acc_in);
             } else if (CG == 2) {
-              umma_f16_2sm(d, ad, bd, P.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              umma_f16_2sm_w(d, ad, a_hi, bd, b_hi, P.idesc, acc_in);
             } else {
-              umma_f16(d, ad, bd, P.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              umma_f16_w(d, ad, a_hi, bd, b_hi, P.idesc, acc_in);
             }
           }
           // smem slot free (in both CTAs) once these MMAs have read it
