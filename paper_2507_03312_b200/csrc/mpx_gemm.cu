@@ -354,8 +354,9 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
   const uint32_t b_bytes = (uint32_t)bn_cta * kBK * 2;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------ TMA producer
+    {
+      // ------------------------------------------------ TMA producer (warp-wide loop,
+      // one elected lane issues: the loop's values stay warp-uniform)
       int stage = 0;
       uint32_t phase = 0;
       for (long long t = t_first; t < P.total_tiles; t += t_step) {
@@ -367,6 +368,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
         const int kb1 = min(P.k_blocks, kb0 + P.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (elect_one()) {
           if (leader) mbar_arrive_expect_tx(&full[stage], CG * (a_bytes + b_bytes));
           uint8_t* a = sA + stage * kATileBytes;
           uint8_t* b = sB + stage * BT;
@@ -397,6 +399,8 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
           } else {
             for (int c = 0; c < bn_cta / 64; ++c) load(b + c * 8192, &tmB, n0 + 64 * c, k0, bb1, bb2);
           }
+          }
+          __syncwarp();
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -405,8 +409,8 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      // ------------------------------------------------ MMA issuer
+    if (leader) {
+      // ------------------------------------------------ MMA issuer (warp-wide loop, one elected lane issues)
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -432,6 +436,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
           const uint32_t as = (uint32_t)a_desc0 + (uint32_t)(stage * kATileBytes >> 4);
           const uint32_t bs = (uint32_t)b_desc0 + (uint32_t)(stage * BT >> 4);
           const uint32_t b2s = (uint32_t)b2_desc0 + (uint32_t)(stage * BT >> 4);
+          if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint32_t acc_in = (kb > kb0 || k > 0) ? 1u : 0u;
@@ -450,15 +455,20 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
             umma_commit_2sm_mc(&empty[stage], pair_mask);
           else
             umma_commit(&empty[stage]);
+          }
+          __syncwarp();
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (CG == 2)
-          umma_commit_2sm_mc(&tfull[acc], pair_mask);  // accumulator ready for both epilogues
-        else
-          umma_commit(&tfull[acc]);
+        if (elect_one()) {
+          if (CG == 2)
+            umma_commit_2sm_mc(&tfull[acc], pair_mask);  // accumulator ready for both epilogues
+          else
+            umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
         if (!WN) acc ^= 1;  // (wide: one accumulator, its phase flips every tile)
         if (acc == 0) acc_phase ^= 1;
       }

@@ -234,6 +234,19 @@ __device__ __forceinline__ void umma_f16_w(uint32_t tmem_d, uint32_t a_lo, uint3
       "}\n" ::"r"(tmem_d),
       "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate));
 }
+// one lane of the (fully active) warp: the single-thread issue of TMA / MMA from a
+// warp-wide loop, so the loop's uniform values can live in uniform registers
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "elect.sync _|p, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(e));
+  return e != 0;
+}
 // commit: arrive on the barrier at this smem offset in every CTA of `mask`
 __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
