@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(kAttnThreadsF, 1)
   ::mpx::pdl_grid_sync();  // prologue done: wait for the predecessor's outputs
 
   if (warp == 0) {
-    if (lane == 0 && G > 0) {
+    if (G > 0) {  // warp-wide loop; one elected lane issues (operands stay warp-uniform)
       auto item_of = [&](int i) { return (int)blockIdx.x + i * (int)gridDim.x; };
       auto load_kq = [&](int i) {
         const int item = item_of(i), hh = item % P.H, bb = item / P.H;
@@ -390,8 +390,13 @@ __global__ void __launch_bounds__(kAttnThreadsF, 1)
         mbar_arrive_expect_tx(&bar[1], kAttnKV);
         tma_load_4d(sV, &tmV, &bar[1], 0, 0, item % P.H, item / P.H);
       };
-      load_kq(0);
-      load_v(0);
+      if (elect_one()) {
+        load_kq(0);
+        load_v(0);
+      }
+      __syncwarp();
+      constexpr uint32_t kHi = 0x40004040u;  // SW128 descriptor high word (SBO 1024, version, swizzle)
+      auto lo = [](uint32_t addr, uint32_t lbo) { return (addr >> 4) | ((lbo >> 4) << 16); };
       const uint32_t idesc1 = idesc_f16(FMT, 128, 16 * n_chunks, 0, 0);  // keys past N: never computed
       const uint32_t idesc2 = idesc_f16(FMT, 128, 64, 0, 1);
       const uint32_t k = smem_u32(sK), v = smem_u32(sV), p = smem_u32(sP);
@@ -401,14 +406,17 @@ __global__ void __launch_bounds__(kAttnThreadsF, 1)
         if (gs >= 2) mbar_wait(&bar[7 + buf], ((gs >> 1) - 1) & 1);       // O_{gs-2} read out of the buffer
         tc_fence_after();
         const uint32_t q = smem_u32(sQ + t * kAttnQ);
+        if (elect_one()) {
 #pragma unroll
-        for (int s = 0; s < 4; ++s)
-          umma_f16(tmem + 256 * buf, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), idesc1,
-                   s > 0);
-        umma_commit(&bar[2 + buf]);
+          for (int s = 0; s < 4; ++s)
+            umma_f16_w(tmem + 256 * buf, lo(q, 16) + s * 2, kHi, lo(k, 16) + s * 2, kHi, idesc1, s > 0);
+          umma_commit(&bar[2 + buf]);
+        }
+        __syncwarp();
         if (t == T - 1 && i + 1 < n_items) {  // K and the Q tiles are free once these S MMAs completed
           mbar_wait(&bar[2 + buf], (gs >> 1) & 1);
-          load_kq(i + 1);
+          if (elect_one()) load_kq(i + 1);
+          __syncwarp();
         }
       };
       issue_s(0);
@@ -420,20 +428,24 @@ __global__ void __launch_bounds__(kAttnThreadsF, 1)
         if (t == 0) mbar_wait(&bar[1], i & 1);  // V landed
         mbar_wait(&bar[4], g & 1);              // P_g written (S_g consumed)
         tc_fence_after();
-        if (P.psave) {  // the rounded P tile as the MMAs read it (rows < N, keys < 16 n_chunks)
-          for (int blk = 0; blk * 4 < n_chunks; ++blk)
-            tma_store_4d(&tmP, sP + blk * 16384, blk * 64, t * 128, item_of(i), 0);
-          bulk_commit();
+        if (elect_one()) {
+          if (P.psave) {  // the rounded P tile as the MMAs read it (rows < N, keys < 16 n_chunks)
+            for (int blk = 0; blk * 4 < n_chunks; ++blk)
+              tma_store_4d(&tmP, sP + blk * 16384, blk * 64, t * 128, item_of(i), 0);
+            bulk_commit();
+          }
+          for (int s = 0; s < n_chunks; ++s)  // O_g = P_g V
+            umma_f16_w(tmem + 256 * buf, lo(p, 16) + (s >> 2) * 1024 + (s & 3) * 2, kHi, lo(v, 8192) + s * 128, kHi,
+                       idesc2, s > 0);
+          umma_commit(&bar[5 + buf]);
+          if (P.psave) bulk_wait_read0();  // (the bulk group belongs to the issuing thread)
+          mbar_arrive(&bar[9]);
         }
-        for (int s = 0; s < n_chunks; ++s)  // O_g = P_g V
-          umma_f16(tmem + 256 * buf, sw128_desc(p + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
-                   sw128_desc(v + s * 2048, 8192, 1024), idesc2, s > 0);
-        umma_commit(&bar[5 + buf]);
-        if (P.psave) bulk_wait_read0();
-        mbar_arrive(&bar[9]);
+        __syncwarp();
         if (t == T - 1 && i + 1 < n_items) {  // V is free once this P V completed
           mbar_wait(&bar[5 + buf], (g >> 1) & 1);
-          load_v(i + 1);
+          if (elect_one()) load_v(i + 1);
+          __syncwarp();
         }
       }
     }
@@ -615,7 +627,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   ::mpx::pdl_grid_sync();  // prologue done: wait for the predecessor's outputs
 
   if (warp == 0) {
-    if (lane == 0) {
+    {  // warp-wide loop; one elected lane issues (operands stay warp-uniform)
       // persistent: items blockIdx.x, + gridDim.x, ...  Every operand tile is
       // reloaded the moment its last reader has finished, on its own barrier,
       // so loads stream while the MMAs and the softmax warps work:
@@ -656,12 +668,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t id_q = idesc_f16(FMT, 128, 64, 0, 1);    // dQ: A K-major, B MN-major
       uint32_t gt = 0;  // tiles so far (barrier phases)
       int it = 0;       // items so far
-      if (blockIdx.x < P.items) {
+      if (blockIdx.x < P.items && elect_one()) {
         load_v(blockIdx.x);
         load_dop(blockIdx.x, 0);
         load_k(blockIdx.x);
         load_q(blockIdx.x, 0);
       }
+      __syncwarp();
+      // SW128 descriptor low words ((address >> 4) | (LBO >> 4) << 16); the high word is constant
+      constexpr uint32_t kHi = 0x40004040u;
+      auto lo = [](uint32_t addr, uint32_t lbo) { return (addr >> 4) | ((lbo >> 4) << 16); };
       for (int item = blockIdx.x; item < P.items; item += gridDim.x, ++it) {
         const int next = item + (int)gridDim.x;
         if (it == kTraceIt) ATRACE(0);
@@ -677,61 +693,80 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             if (t == 0) mbar_wait(&bar[12], it & 1);
             mbar_wait(&bar[11], ph);
             tc_fence_after();
+            if (elect_one()) {
 #pragma unroll
-            for (int s = 0; s < 4; ++s)  // S = Q K^T
-              umma_f16(tmem, sw128_desc(q + s * 32, 16, 1024), sw128_desc(k + s * 32, 16, 1024), id_nk, s > 0);
-            umma_commit(&bar[2]);
+              for (int s = 0; s < 4; ++s)  // S = Q K^T
+                umma_f16_w(tmem, lo(q, 16) + s * 2, kHi, lo(k, 16) + s * 2, kHi, id_nk, s > 0);
+              umma_commit(&bar[2]);
+            }
+            __syncwarp();
             mbar_wait(&bar[3], ph);  // P_t written (S consumed)
             if (it == kTraceIt) ATRACE(3 + 8 * t);
             tc_fence_after();
           }
+          if (elect_one()) {
 #pragma unroll
-          for (int s = 0; s < 4; ++s)  // dP = dO V^T
-            umma_f16(tmem, sw128_desc(dO + s * 32, 16, 1024), sw128_desc(v + s * 32, 16, 1024), id_nk, s > 0);
-          umma_commit(&bar[4]);
+            for (int s = 0; s < 4; ++s)  // dP = dO V^T
+              umma_f16_w(tmem, lo(dO, 16) + s * 2, kHi, lo(v, 16) + s * 2, kHi, id_nk, s > 0);
+            umma_commit(&bar[4]);
+          }
+          __syncwarp();
           // dV needs only P_t and dO_t: it runs on the tensor pipe while the
           // softmax warps turn dP into dS (TMEM cols 256-383, disjoint from dP)
           if (t == 0 && it > 0) {
             mbar_wait(&bar[10], (it - 1) & 1);  // last item's dV/dK read out of TMEM
             tc_fence_after();
           }
-          for (int half = 0; half < halves; ++half) {
+          if (elect_one()) {
+            for (int half = 0; half < halves; ++half) {
 #pragma unroll
-            for (int s = 0; s < 8; ++s)  // dV += P^T dO
-              umma_f16(tmem + 256 + half * 64, sw128_desc(pp + half * 32768 + s * 2048, 16384, 1024),
-                       sw128_desc(dO + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
+              for (int s = 0; s < 8; ++s)  // dV += P^T dO
+                umma_f16_w(tmem + 256 + half * 64, lo(pp + half * 32768, 16384) + s * 128, kHi,
+                           lo(dO, 8192) + s * 128, kHi, id_kv, (t > 0 || s > 0));
+            }
+            umma_commit(&bar[9]);
           }
-          umma_commit(&bar[9]);
+          __syncwarp();
           mbar_wait(&bar[5], ph);  // dS_t written (dP consumed, P_t no longer read by the softmax warps)
           if (it == kTraceIt) ATRACE(4 + 8 * t);
-          if (t == T - 1 && next < P.items) load_v(next);  // the item's dP MMAs are done with V
+          if (t == T - 1 && next < P.items && elect_one()) load_v(next);  // the item's dP MMAs are done with V
+          __syncwarp();
           if (t == 0) mbar_wait(&bar[12], it & 1);  // K
           tc_fence_after();
           // dQ first, so the softmax warps read it out while dK runs
-          for (int s = 0; s < n_chunks; ++s)  // dQ = dS K
-            umma_f16(tmem, sw128_desc(ds + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024),
-                     sw128_desc(k + s * 2048, 8192, 1024), id_q, s > 0);
-          umma_commit(&bar[6]);
+          if (elect_one()) {
+            for (int s = 0; s < n_chunks; ++s)  // dQ = dS K
+              umma_f16_w(tmem, lo(ds, 16) + (s >> 2) * 1024 + (s & 3) * 2, kHi, lo(k, 8192) + s * 128, kHi, id_q,
+                         s > 0);
+            umma_commit(&bar[6]);
+          }
+          __syncwarp();
           mbar_wait(&bar[11], ph);  // Q_t
           tc_fence_after();
-          for (int half = 0; half < halves; ++half) {
+          if (elect_one()) {
+            for (int half = 0; half < halves; ++half) {
 #pragma unroll
-            for (int s = 0; s < 8; ++s)  // over the 128 queries of the tile: dK += dS^T Q
-              umma_f16(tmem + 384 + half * 64, sw128_desc(ds + half * 32768 + s * 2048, 16384, 1024),
-                       sw128_desc(q + s * 2048, 8192, 1024), id_kv, (t > 0 || s > 0));
+              for (int s = 0; s < 8; ++s)  // over the 128 queries of the tile: dK += dS^T Q
+                umma_f16_w(tmem + 384 + half * 64, lo(ds + half * 32768, 16384) + s * 128, kHi,
+                           lo(q, 8192) + s * 128, kHi, id_kv, (t > 0 || s > 0));
+            }
+            umma_commit(&bar[8]);
           }
-          umma_commit(&bar[8]);
+          __syncwarp();
           const bool more = t + 1 < T;
           if (more || next < P.items) {
             const int li = more ? item : next, lt = more ? t + 1 : 0;
             mbar_wait(&bar[9], ph);  // dV_t done: dO and P free (the dS pass finished with P_t)
-            load_dop(li, lt);
+            if (elect_one()) load_dop(li, lt);
+            __syncwarp();
             if (!more) {
               mbar_wait(&bar[6], ph);  // the item's last dQ is done with K
-              load_k(next);
+              if (elect_one()) load_k(next);
+              __syncwarp();
             }
             mbar_wait(&bar[8], ph);  // dK_t done: Q free
-            load_q(li, lt);
+            if (elect_one()) load_q(li, lt);
+            __syncwarp();
           }
         }
       }
