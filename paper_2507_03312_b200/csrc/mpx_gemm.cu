@@ -480,6 +480,9 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
     // chunks h, h + kEpiPerQ, ... (direct path)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int h = (warp - 2) >> 2;
+    // (single-thread TMA / bulk-group work below runs on the elect.sync lane — lane 0
+    // of the full warp every time, so the per-thread bulk groups stay consistent — which
+    // keeps the TMA operands in uniform registers)
     // kBufPerWarp 4 KB staging buffers per warp (32 rows x 128 B, swizzled),
     // used in turn by successive column groups
     uint8_t* obuf = stage_epi + (warp - 2) * (kBufPerWarp * 4096);
@@ -554,7 +557,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
           }
         }
         // exchange with the partner warp through the (idle) staging buffers
-        if (lane == 0) bulk_wait_read0();
+        if (elect_one()) bulk_wait_read0();
         __syncwarp();
         float* mine = reinterpret_cast<float*>(stg);
         mine[lane] = m;
@@ -971,7 +974,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
         // aux-out groups, > 2 groups) ping-pong the buffers group by group.
         const bool batched = !kAuxOut && my_groups <= kBufPerWarp;  // GELU-aux-out: both buffers per group
         if (batched) {
-          if (lane == 0) {
+          if (elect_one()) {
             bulk_wait_read0();
             if (kXin && my_groups > 0) {
               const int xb1 = (XO == XOP_RES_IN || XO == XOP_RES_LN) && P.r_sb1 == 0 ? 0 : b1;
@@ -982,7 +985,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
             }
           }
           __syncwarp();
-        } else if (kXin && lane == 0 && my_groups > 0) {
+        } else if (kXin && my_groups > 0 && elect_one()) {
           x_load(h, gcount);
         }
         if (my_groups == 0) release_acc();
@@ -996,7 +999,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
               eph ^= 1u;
             }
           } else if (!batched) {
-            if (lane == 0) {  // the store that last used this buffer (both, for 64-column GELU-aux-out) has read it
+            if (elect_one()) {  // the store that last used this buffer (both, for 64-column GELU-aux-out) has read it
               if (kAuxOut && kAuxGW != 32)
                 bulk_wait_read0();
               else
@@ -1016,7 +1019,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
           if (batched && j + 1 < my_groups) continue;
           fence_async_smem();
           __syncwarp();
-          if (lane == 0) {
+          if (elect_one()) {
             if (batched) {
               for (int jj = 0; jj < my_groups; ++jj) store_group(h + kEpiPerQ * jj, buf(jj));
             } else {
@@ -1044,7 +1047,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
           const int r = q * 32 + lane;
           // (the phase completes when this CTA has armed it and all 3 x 128 partials have landed:
           // st.async signals the destination's barrier itself — no cluster-scope fences)
-          if (warp == 2 && lane == 0) mbar_arrive_expect_tx(&lnbar[slot], 3u * 128u * 8u);
+          if (warp == 2 && elect_one()) mbar_arrive_expect_tx(&lnbar[slot], 3u * 128u * 8u);
           if (h == 0) {
 #pragma unroll
             for (int dst = 0; dst < 3; ++dst)
@@ -1067,7 +1070,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
             P.ln_rstd[row] = rstd;
           }
           // (4) once the x stores have read the staging buffers, y = LN(x) in place -> TMA store
-          if (lane == 0) bulk_wait_read0();
+          if (elect_one()) bulk_wait_read0();
           __syncwarp();
           const int sw = lane & 7;
           for (int j = 0; j < my_groups; ++j) {
@@ -1095,7 +1098,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
           }
           fence_async_smem();
           __syncwarp();
-          if (lane == 0) {
+          if (elect_one()) {
             for (int j = 0; j < my_groups; ++j) tma_store_4d(&tmL, buf(j), n0 + (h + kEpiPerQ * j) * GW, row0, 0, 0);
             bulk_commit();
           }
@@ -1177,7 +1180,7 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
       if (!WN) acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (P.tma_store && lane == 0) bulk_wait0();
+    if (P.tma_store && elect_one()) bulk_wait0();
   }
   __syncthreads();
   if (CG == 2) cluster_sync();  // no CTA leaves while its peer may still signal it
