@@ -132,9 +132,9 @@ __device__ __forceinline__ void grid_scores16(const uint32_t* a, const ScoreGrid
 // Forward softmax of row r, one TMEM pass: the thread's chunks c = split +
 // NS j (< n_chunks) stay in registers (scores on the half grid, then e); the
 // row max is exchanged through red_m, e = 2^(sv sl - M log2 e), and the row
-// sum L is the chunk sums (pairs accumulated in order, then .x + .y) added in
-// chunk order — the canonical order the backward's recompute follows, so its
-// P is bit-identical.  Keys past N in the tail chunk are masked (e = 0); full
+// sum L is each split's chunk sums (pairs accumulated in order, then .x + .y)
+// added in chunk order, then the split partials added in split order — the
+// canonical order the backward's recompute follows, so its P is bit-identical.  Keys past N in the tail chunk are masked (e = 0); full
 // chunks run unpredicated.  Returns (M, 1/L); softmax_store_p then writes P.
 template <int FMT>
 __device__ __forceinline__ uint32_t pack2T(float a, float b) {
@@ -201,15 +201,18 @@ __device__ __forceinline__ float2 softmax_fwd_regs(uint32_t trow, int split, int
     }
     return acc.x + acc.y;
   };
+  float part = 0.f;  // this split's chunk sums, in chunk order
 #pragma unroll
   for (int j = 0; j < KC; ++j) {
     const int c = split + NS * j;
     if (c < n_chunks)
-      red_l[c * 128 + r] = (c == n_chunks - 1 && tail < 16) ? expc(a[j], std::true_type{}) : expc(a[j], std::false_type{});
+      part += (c == n_chunks - 1 && tail < 16) ? expc(a[j], std::true_type{}) : expc(a[j], std::false_type{});
   }
+  red_l[split * 128 + r] = part;
   quarter_sync<NS>(q);
-  float L = 0.f;
-  for (int c = 0; c < n_chunks; ++c) L += red_l[c * 128 + r];
+  float L = 0.f;  // the split partials in split order (the canonical order; softmax_bwd_p repeats it)
+#pragma unroll
+  for (int j = 0; j < NS; ++j) L += red_l[j * 128 + r];
   return make_float2(M, 1.f / L);
 }
 
@@ -236,8 +239,9 @@ __device__ __forceinline__ void softmax_store_p(int split, int r, int N, float i
 
 // Backward: P_t of row r recomputed from the forward's (M, 1/L) when given,
 // else from statistics recomputed here in the forward's canonical order (exact
-// row max; chunk sums, each as softmax_fwd_regs forms it, added in chunk order
-// through `lsc` [16 chunks][128 rows]) — the same bits as the forward.
+// row max; chunk sums, each as softmax_fwd_regs forms it, through `lsc` [16
+// chunks][128 rows], added per forward split and then in split order) — the
+// same bits as the forward.
 template <int NS>
 __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, int q, int N, float scale, int fmt,
                                               float* red, float* lsc, uint8_t* sP, const float2* stats) {
@@ -287,8 +291,13 @@ __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, i
       lsc[c * 128 + r] = acc.x + acc.y;
     }
     quarter_sync<NS>(q);
-    float L = 0.f;
-    for (int c = 0; c < n_chunks; ++c) L += lsc[c * 128 + r];
+    float L = 0.f;  // the forward's order: per forward split (chunks s, s + kSplitF, ...), then the splits
+#pragma unroll
+    for (int sp = 0; sp < kSplitF; ++sp) {
+      float part = 0.f;
+      for (int c = sp; c < n_chunks; c += kSplitF) part += lsc[c * 128 + r];
+      L += part;
+    }
     quarter_sync<NS>(q);  // red[] / lsc[] are reused by the caller
     inv = 1.f / L;
   }
@@ -337,7 +346,10 @@ __device__ __forceinline__ void softmax_bwd_p(uint32_t trow, int split, int r, i
 // written, 5/6 O in buffer 0/1, 7/8 buffer 0/1 read out, 9 P tile's TMA store
 // has read it
 // ===========================================================================
-constexpr size_t kAttnSmemF = 1024 + 2 * kAttnKV + 2 * kAttnQ + kAttnP + (kSplitF + 16) * 128 * 4 + 128;
+// dynamic: the 1 KB-aligned tiles; the row-exchange scratch and the barriers are static
+// __shared__ arrays (constant-offset LDS/STS addressing, nothing for the compiler to
+// rematerialise in the register-capped softmax warps)
+constexpr size_t kAttnSmemF = 1024 + 2 * kAttnKV + 2 * kAttnQ + kAttnP;
 
 template <int KC, int FMT>
 __global__ void __launch_bounds__(kAttnThreadsF, 1)
@@ -345,15 +357,15 @@ __global__ void __launch_bounds__(kAttnThreadsF, 1)
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmP,
                     const __grid_constant__ AttnParams P) {
   extern __shared__ uint8_t smem_raw[];
+  __shared__ float red_m[kSplitF * 128];
+  __shared__ float red_l[kSplitF * 128];
+  __shared__ uint64_t bar[10];
+  __shared__ uint32_t tmem_slot[1];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sK = smem;
   uint8_t* sV = sK + kAttnKV;
   uint8_t* sQ = sV + kAttnKV;  // Q_0, Q_1
   uint8_t* sP = sQ + 2 * kAttnQ;
-  float* red_m = reinterpret_cast<float*>(sP + kAttnP);
-  float* red_l = red_m + kSplitF * 128;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(red_l + 16 * 128);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int T = P.m_tiles;
