@@ -789,14 +789,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const uint32_t trow = tmem + ((uint32_t)(qd * 32) << 16);
     const int n_chunks = (P.N + 15) / 16;
     const int sw = r & 7;
-    auto read_p = [&](int c, float* pv) {  // own row of P_t, keys 16c..16c+15
+    auto read_pw = [&](int c, uint32_t* u) {  // own row of P_t, keys 16c..16c+15, as 8 packed pairs
       const uint8_t* rowp = sP + (c >> 2) * 16384 + r * 128;
       const int u0 = (c & 3) * 2;
       const uint4 w0 = *reinterpret_cast<const uint4*>(rowp + ((u0 ^ sw) << 4));
       const uint4 w1 = *reinterpret_cast<const uint4*>(rowp + (((u0 + 1) ^ sw) << 4));
-      const uint32_t u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i) unpack2(u[i], FMT, pv[2 * i], pv[2 * i + 1]);
+      u[0] = w0.x, u[1] = w0.y, u[2] = w0.z, u[3] = w0.w, u[4] = w1.x, u[5] = w1.y, u[6] = w1.z, u[7] = w1.w;
     };
     constexpr int kMaxC = 16 / kSplit;  // chunks per thread
     static_assert(kSplit == 4, "dQ readout: one chunk per split");
@@ -833,17 +831,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       for (int j = 0; j < kMaxC; ++j) {
         const int c = split + j * kSplit;
         if (c < n_chunks) {
-          uint32_t a[16];
-          float pv[16];
+          uint32_t a[16], pw[8];
           tmem_ld16(trow + c * 16, a);
-          read_p(c, pv);
+          read_pw(c, pw);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < 8; ++i) {  // P * dP on the half pairs: FHFMA, the same bits as unpack + FFMA2
             dpk[j][i] = pack2_fmt(__uint_as_float(a[2 * i]), __uint_as_float(a[2 * i + 1]), FMT);
-            float d0, d1;
-            unpack2(dpk[j][i], FMT, d0, d1);
-            tsum2 = __ffma2_rn(make_float2(pv[2 * i], pv[2 * i + 1]), make_float2(d0, d1), tsum2);
+            tsum2 = fma_h2<FMT>(pw[i], dpk[j][i], tsum2);
           }
         }
       }
@@ -857,15 +852,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       for (int j = 0; j < kMaxC; ++j) {
         const int c = split + j * kSplit;
         if (c < n_chunks) {
-          float pv[16];
-          read_p(c, pv);
+          uint32_t pw[8];
+          read_pw(c, pw);
           uint32_t pk[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float d0, d1;
-            unpack2(dpk[j][i], FMT, d0, d1);
-            const float2 ds = __fmul2_rn(make_float2(pv[2 * i], pv[2 * i + 1]),
-                                         __fadd2_rn(make_float2(d0, d1), f2(-tsum)));
+          for (int i = 0; i < 8; ++i) {  // dS = P (dP - t): dP - t by FHADD on the packed dP
+            const float2 ds = __fmul2_rn(unpack2_fmt<FMT>(pw[i]), add_h2<FMT>(f2(-tsum), dpk[j][i]));
             pk[i] = pack2_fmt(ds.x, ds.y, FMT);
           }
           store_p_chunk(sdS, c, r, pk);

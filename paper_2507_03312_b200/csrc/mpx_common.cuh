@@ -145,6 +145,40 @@ __device__ __forceinline__ uint32_t pack2_fmt(float a, float b, int bf16) {
 }
 
 // round an f32 onto DT's grid, staying in f32 (quantize_array semantics)
+template <int F>
+__device__ __forceinline__ float2 unpack2_fmt(uint32_t w) {  // (lo, hi) halves of w, exactly
+  if (F) return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+  return __half22float2(*reinterpret_cast<const __half2*>(&w));
+}
+// acc + the two half values packed in w (lo, hi): the conversion is exact and the
+// add rounds once, so this equals unpack-then-FADD bit for bit, in one FHADD each
+template <int F>
+__device__ __forceinline__ float2 add_h2(float2 acc, uint32_t w) {
+  float2 d;
+  if (F)
+    asm("{.reg .b16 lo, hi; mov.b32 {lo, hi}, %2;\n add.rn.f32.bf16 %0, lo, %3;\n add.rn.f32.bf16 %1, hi, %4;}"
+        : "=f"(d.x), "=f"(d.y) : "r"(w), "f"(acc.x), "f"(acc.y));
+  else
+    asm("{.reg .b16 lo, hi; mov.b32 {lo, hi}, %2;\n add.rn.f32.f16 %0, lo, %3;\n add.rn.f32.f16 %1, hi, %4;}"
+        : "=f"(d.x), "=f"(d.y) : "r"(w), "f"(acc.x), "f"(acc.y));
+  return d;
+}
+
+// (a_lo * b_lo + acc.x, a_hi * b_hi + acc.y) for half pairs a, b: the product of two
+// halves is exact in f32 and the add rounds once — the same bits as unpack + FFMA2
+template <int F>
+__device__ __forceinline__ float2 fma_h2(uint32_t a, uint32_t b, float2 acc) {
+  float2 d;
+  if (F)
+    asm("{.reg .b16 al, ah, bl, bh; mov.b32 {al, ah}, %2; mov.b32 {bl, bh}, %3;\n"
+        " fma.rn.f32.bf16 %0, al, bl, %4;\n fma.rn.f32.bf16 %1, ah, bh, %5;}"
+        : "=f"(d.x), "=f"(d.y) : "r"(a), "r"(b), "f"(acc.x), "f"(acc.y));
+  else
+    asm("{.reg .b16 al, ah, bl, bh; mov.b32 {al, ah}, %2; mov.b32 {bl, bh}, %3;\n"
+        " fma.rn.f32.f16 %0, al, bl, %4;\n fma.rn.f32.f16 %1, ah, bh, %5;}"
+        : "=f"(d.x), "=f"(d.y) : "r"(a), "r"(b), "f"(acc.x), "f"(acc.y));
+  return d;
+}
 template <int DT> __device__ __forceinline__ float quantize_f32(float x) {
   return to_f32<DT>(from_f32<DT>(x));
 }

@@ -198,25 +198,6 @@ __device__ __forceinline__ float2 gelu_grad2(float2 x) {
   return __ffma2_rn(__fmul2_rn(__fmul2_rn(x, f2(0.5f)), sech2), k, a);
 }
 
-template <int F>
-__device__ __forceinline__ float2 unpack2_fmt(uint32_t w) {  // (lo, hi) halves of w, exactly
-  if (F) return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
-  return __half22float2(*reinterpret_cast<const __half2*>(&w));
-}
-// acc + the two half values packed in w (lo, hi): the conversion is exact and the
-// add rounds once, so this equals unpack-then-FADD bit for bit, in one FHADD each
-template <int F>
-__device__ __forceinline__ float2 add_h2(float2 acc, uint32_t w) {
-  float2 d;
-  if (F)
-    asm("{.reg .b16 lo, hi; mov.b32 {lo, hi}, %2;\n add.rn.f32.bf16 %0, lo, %3;\n add.rn.f32.bf16 %1, hi, %4;}"
-        : "=f"(d.x), "=f"(d.y) : "r"(w), "f"(acc.x), "f"(acc.y));
-  else
-    asm("{.reg .b16 lo, hi; mov.b32 {lo, hi}, %2;\n add.rn.f32.f16 %0, lo, %3;\n add.rn.f32.f16 %1, hi, %4;}"
-        : "=f"(d.x), "=f"(d.y) : "r"(w), "f"(acc.x), "f"(acc.y));
-  return d;
-}
-
 struct TileCoord {
   int z, s, m_blk, n_blk;
 };
