@@ -12,6 +12,7 @@ from paper_2507_03312_b200 import _native as N  # noqa: E402
 
 M, D = 256 * 197, 768
 bf = torch.bfloat16
+torch.manual_seed(0)
 dev = "cuda"
 x = torch.randn(M, D, device=dev).to(bf)
 g = (1 + 0.1 * torch.randn(D, device=dev)).to(bf)
@@ -49,5 +50,15 @@ ref = rs[:, None] * (d - d.mean(1, keepdim=True) - xh * (d * xh).mean(1, keepdim
 err = ((dx.float() - ref).abs().max() / ref.abs().max()).item()
 e_dg = ((dg.float() - (dy.float() * xh).sum(0)).abs().max() / (dy.float() * xh).sum(0).abs().max()).item()
 e_xs = ((dxs.float() - dx.float().sum(0)).abs().max() / dx.float().sum(0).abs().max()).item()
-print(json.dumps({"ln_bwd2_us": round(e0.elapsed_time(e1) / ITERS * 1000, 1), "dx_rel": err, "dgain_rel": e_dg,
-                  "dxsum_rel": e_xs}))
+import hashlib  # noqa: E402
+
+digest = hashlib.sha1(b"".join(t.view(torch.int16).cpu().numpy().tobytes() for t in (dx, dg, db, dxs))).hexdigest()[:12]
+out = {"ln_bwd2_us": round(e0.elapsed_time(e1) / ITERS * 1000, 1), "dx_rel": err, "dgain_rel": e_dg, "dxsum_rel": e_xs,
+       "digest": digest}
+if len(sys.argv) > 2:  # steady-state time and NVML energy (power-capped regime): [iters] [seconds]
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from energy import Meter  # noqa: E402
+
+    n, ms, j, w, mhz = Meter(0).run(run, float(sys.argv[2]))
+    out.update({"steady_us": round(ms * 1e3, 2), "mJ": round(j * 1e3, 2), "W": round(w, 1), "sm_mhz": mhz})
+print(json.dumps(out))
