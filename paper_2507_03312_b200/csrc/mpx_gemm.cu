@@ -151,15 +151,26 @@ __device__ __forceinline__ float tanh_fast(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// tanh-approximation GELU and its derivative (tensors.py:196-200, autodiff.py:173-185)
+// tanh-approximation GELU and its derivative (tensors.py:196-200, autodiff.py:173-185),
+// the same operations as the packed versions below (so every epilogue path of the
+// GEMM gives the same bits): u = x c0 (1 + c1 x^2), y = x/2 + x/2 t,
+// gelu' = (1 + t)/2 + (y - y t) c0 (1 + 3 c1 x^2)
 __device__ __forceinline__ float gelu_f(float x) {
   const float c0 = 0.7978845608028654f, c1 = 0.044715f;
-  return 0.5f * x * (1.f + tanh_fast(c0 * (x + c1 * x * x * x)));
+  const float x2 = __fmul_rn(x, x);
+  const float t = tanh_fast(__fmul_rn(x, __fmaf_rn(x2, c0 * c1, c0)));
+  const float hx = __fmul_rn(x, 0.5f);
+  return __fmaf_rn(hx, t, hx);
 }
 __device__ __forceinline__ float gelu_grad_f(float x) {
   const float c0 = 0.7978845608028654f, c1 = 0.044715f;
-  const float t = tanh_fast(c0 * (x + c1 * x * x * x));
-  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c0 * (1.f + 3.f * c1 * x * x);
+  const float x2 = __fmul_rn(x, x);
+  const float t = tanh_fast(__fmul_rn(x, __fmaf_rn(x2, c0 * c1, c0)));
+  const float hx = __fmul_rn(x, 0.5f);
+  const float y = __fmaf_rn(hx, t, hx);
+  const float a = __fmaf_rn(t, 0.5f, 0.5f);
+  const float ymt = __fmaf_rn(-y, t, y);
+  return __fmaf_rn(ymt, __fmaf_rn(x2, 3.f * c0 * c1, c0), a);
 }
 
 // packed-f32x2 (FFMA2 / FMUL2) versions for the lean epilogues: two columns per
@@ -188,14 +199,9 @@ __device__ __forceinline__ void gelu_and_grad2(float2 x, float2& y, float2& d) {
   d = __ffma2_rn(ymt, k, a);
 }
 __device__ __forceinline__ float2 gelu_grad2(float2 x) {
-  const float c0 = 0.7978845608028654f, c1 = 0.044715f;
-  const float2 x2 = __fmul2_rn(x, x);
-  const float2 u = __fmul2_rn(__fmul2_rn(x, __ffma2_rn(x2, f2(c1), f2(1.f))), f2(c0));
-  const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
-  const float2 a = __ffma2_rn(t, f2(0.5f), f2(0.5f));                      // 0.5 (1 + t)
-  const float2 sech2 = __ffma2_rn(make_float2(-t.x, -t.y), t, f2(1.f));    // 1 - t^2
-  const float2 k = __ffma2_rn(x2, f2(3.f * c0 * c1), f2(c0));              // c0 (1 + 3 c1 x^2)
-  return __ffma2_rn(__fmul2_rn(__fmul2_rn(x, f2(0.5f)), sech2), k, a);
+  float2 y, d;
+  gelu_and_grad2(x, y, d);
+  return d;
 }
 
 struct TileCoord {

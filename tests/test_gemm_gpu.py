@@ -250,3 +250,34 @@ def test_transpose_batch(cuda, dt):
     out = torch.empty(128, 264, device=cuda, dtype=dt)[:, :256]
     VK.transpose_batch([big], [out])
     assert torch.equal(out, big.t())
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("shape", [(1000, 768, 256), (333, 200, 128), (4096, 3072, 768)])
+def test_epilogue_paths_bit_identical(cuda, dt, shape):
+    """The staged epilogue variants (whole-group fast paths with FHADD operand adds,
+    the packed GELU math, partial groups) against the generic direct-store epilogue
+    (tma_store=-1) on the same tiles: the accumulators are the same MMAs, so every
+    epilogue must give the same bits — bias, bias + residual, the saved GELU
+    derivative as a product (MUL_AUX), gelu' of a saved pre-activation, and GELU with
+    the pre-activation or the derivative written out."""
+    M, N, K = shape
+    g = torch.Generator(device=cuda).manual_seed(M + N)
+    x = torch.randn(M, K, device=cuda, generator=g).to(dt)
+    w = (torch.randn(K, N, device=cuda, generator=g) * 0.05).to(dt)
+    bias = torch.randn(N, device=cuda, generator=g).to(dt)
+    res = torch.randn(M, N, device=cuda, generator=g).to(dt)
+    aux = torch.randn(M, N, device=cuda, generator=g).to(dt)
+    common = dict(M=M, N=N, K=K, lda=K, ldb=N, b_mn=True)
+    cases = [dict(), dict(bias=bias), dict(bias=bias, residual=res, ldr=N), dict(aux=aux, ld_aux=N, act=VK.ACT_MUL_AUX),
+             dict(aux=aux, ld_aux=N, act=VK.ACT_GELU_BWD)]
+    for kw in cases:
+        y0 = VK.gemm(x, w, **common, **kw)
+        y1 = VK.gemm(x, w, **common, tma_store=-1, **kw)
+        assert torch.equal(y0.view(torch.int16), y1.view(torch.int16)), list(kw)
+    for act in (VK.ACT_GELU, VK.ACT_GELU_D):
+        a0, a1 = torch.empty_like(aux), torch.empty_like(aux)
+        y0 = VK.gemm(x, w, **common, bias=bias, aux=a0, ld_aux=N, act=act)
+        y1 = VK.gemm(x, w, **common, tma_store=-1, bias=bias, aux=a1, ld_aux=N, act=act)
+        assert torch.equal(y0.view(torch.int16), y1.view(torch.int16)), act
+        assert torch.equal(a0.view(torch.int16), a1.view(torch.int16)), act
