@@ -994,11 +994,10 @@ __global__ void __launch_bounds__(EpiCfg<XO>::kThreads, 1)
             }
             __syncwarp();
           }
-          constexpr bool kFast = (XO == XOP_PLAIN || XO == XOP_RES_IN || XO == XOP_AUX_IN || XO == XOP_RES_LN) &&
-                                 kEpiWarps <= 8;
+          constexpr bool kFast = XO == XOP_PLAIN || XO == XOP_RES_IN || XO == XOP_AUX_IN || XO == XOP_RES_LN;
           if (kFast && GW == 64 && nch == 4 && n0 + g * GW + 64 <= P.N && P.alpha == 1.f)
             stage_full(g, bb, j == my_groups - 1);
-          else if (kAuxOut && kAuxGW == 32 && kEpiWarps <= 8 && GW == 32 && nch == 2 && n0 + g * GW + 32 <= P.N &&
+          else if (kAuxOut && kAuxGW == 32 && GW == 32 && nch == 2 && n0 + g * GW + 32 <= P.N &&
                    P.alpha == 1.f)
             stage_full_aux(g, bb, j == my_groups - 1);
           else
