@@ -577,16 +577,30 @@ struct AttnBwdParams {
   const uint8_t* psaved;  // optional: the forward's P tiles (attn_fwd psave) — reloaded instead of recomputed
 };
 
-// 16 values per lane -> column sums over the warp's 32 lanes (rows) by recursive
-// halving (16 shuffles, fixed order); returns the sum of column col16(lane)
-__device__ __forceinline__ float warp_colsum16(float* v, int lane) {
+// 16 half values per lane (8 packed words) -> column sums over the warp's 32 lanes
+// (rows) by recursive halving (fixed order); returns the sum of column col16(lane).
+// The first step exchanges packed words (4 shuffles instead of 8) and adds the two
+// rows' halves straight into f32 (unpack + FHADD) — the same additions in the same
+// tree as halving the unpacked values, so the same bits
+template <int FMT>
+__device__ __forceinline__ float warp_colsum16w(const uint32_t (&w)[8], int lane) {
+  float v[8];
+  const bool up = (lane & 16) != 0;
 #pragma unroll
-  for (int w = 8, m = 16; w >= 1; w >>= 1, m >>= 1) {
-    const bool up = (lane & m) != 0;
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t send = up ? w[i] : w[i + 4];
+    const uint32_t keep = up ? w[i + 4] : w[i];
+    const float2 s2 = add_h2<FMT>(unpack2_fmt<FMT>(keep), __shfl_xor_sync(0xffffffffu, send, 16));
+    v[2 * i] = s2.x;
+    v[2 * i + 1] = s2.y;
+  }
 #pragma unroll
-    for (int i = 0; i < w; ++i) {
-      const float send = up ? v[i] : v[i + w];
-      const float keep = up ? v[i + w] : v[i];
+  for (int w2 = 4, m = 8; w2 >= 1; w2 >>= 1, m >>= 1) {
+    const bool u = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < w2; ++i) {
+      const float send = u ? v[i] : v[i + w2];
+      const float keep = u ? v[i + w2] : v[i];
       v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
     }
   }
@@ -886,13 +900,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
         if (P.csum) {  // column sums of the stored (rounded) dQ rows
-          float v[16];
+          uint32_t wv[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            unpack2(pk[i], FMT, v[2 * i], v[2 * i + 1]);
-            if (qrow >= P.N) v[2 * i] = v[2 * i + 1] = 0.f;
-          }
-          qsum += warp_colsum16(v, lane);
+          for (int i = 0; i < 8; ++i) wv[i] = qrow < P.N ? pk[i] : 0u;
+          qsum += warp_colsum16w<FMT>(wv, lane);
         }
       }
       tc_fence_before();
@@ -923,13 +934,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
         if (P.csum) {
-          float v[16];
+          uint32_t wv[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            unpack2(pk[i], FMT, v[2 * i], v[2 * i + 1]);
-            if (key >= P.N) v[2 * i] = v[2 * i + 1] = 0.f;
-          }
-          kvsum[c] = warp_colsum16(v, lane);
+          for (int i = 0; i < 8; ++i) wv[i] = key < P.N ? pk[i] : 0u;
+          kvsum[c] = warp_colsum16w<FMT>(wv, lane);
         }
       }
     }
