@@ -891,6 +891,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         uint32_t a[16];
         tmem_ld16(trow + c * 16, a);
         tmem_ld_wait();
+        // dQ is in registers: free its TMEM columns for the next tile's MMAs first, then
+        // store it and take its column sums off the MMA critical path
+        tc_fence_before();
+        mbar_arrive(&bar[7]);
         uint32_t pk[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
@@ -906,8 +910,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           qsum += warp_colsum16w<FMT>(wv, lane);
         }
       }
-      tc_fence_before();
-      mbar_arrive(&bar[7]);
       if (warp == 4 && lane == 0 && it == kTraceIt) ATRACE(8 + 8 * t);
     }
     // ---- dV, dK (keys r and 128 + r of this head): 4 (half, which) combos split over the warps,
@@ -925,6 +927,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         uint32_t a[16];
         tmem_ld16(trow + 256 + which * 128 + half * 64 + c * 16, a);
         tmem_ld_wait();
+        if (c == 3) {  // the last dV/dK read: the next item may accumulate into TMEM cols 256-511
+          tc_fence_before();  // while this item's stores, column sums and combine finish
+          mbar_arrive(&bar[10]);
+        }
         uint32_t pk[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
@@ -963,9 +969,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       asm volatile("bar.sync 6, %0;" ::"n"(128 * kSplit) : "memory");  // scratch read before the next P tile
     }
-    // dV/dK (and the scratch) consumed: the next item may accumulate into TMEM cols 256-511
-    tc_fence_before();
-    mbar_arrive(&bar[10]);
+    // (the dS scratch is reused by these warps only after the barrier above)
     if (warp == 4 && lane == 0 && it == kTraceIt) ATRACE(20);
     }
   }
