@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(256) ln_dx_kernel(const void* __restrict__ x, 
 // in a fixed order; ws layout [3][gridDim.x][D] for partials_reduce3_kernel.
 // ===========================================================================
 template <int V, int FMT>  // FMT (0 f16, 1 bf16) compiled in: one conversion path
-__global__ void __launch_bounds__(128, 4) ln_bwd_fused_kernel(const void* __restrict__ x, long long ldx,
+__global__ void __launch_bounds__(128, V >= 4 ? 2 : 4) ln_bwd_fused_kernel(const void* __restrict__ x, long long ldx,
                                                            const void* __restrict__ g, const float* __restrict__ mean,
                                                            const float* __restrict__ rstd, const void* __restrict__ dy,
                                                            long long lddy, const void* __restrict__ dres,
@@ -1393,14 +1393,15 @@ int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, 
     MPX_LAUNCH_CHECK("partials_reduce3_kernel");
     return 0;
   }
-  if (D <= 768 && !fused_off) {  // one pass: dx + all column partials (shared-memory slabs)
+  if (D <= 1024 && !fused_off) {  // one pass: dx + all column partials (shared-memory slabs; ViT-L's D = 1024)
     const int nsum = dxsum ? 3 : 2;
-    int blocks = current_num_sms() * 4;
+    int blocks = current_num_sms() * (D > 768 ? 2 : 4);  // (D = 1024: 2 blocks per SM, 255 registers)
     while ((long long)nsum * blocks * D > workspace_floats && blocks > 1) blocks /= 2;
     const size_t shb = (size_t)4 * 3 * D * sizeof(float);  // per-warp accumulator slabs
-    const void* ks[6] = {(const void*)ln_bwd_fused_kernel<1, 0>, (const void*)ln_bwd_fused_kernel<2, 0>,
-                         (const void*)ln_bwd_fused_kernel<3, 0>, (const void*)ln_bwd_fused_kernel<1, 1>,
-                         (const void*)ln_bwd_fused_kernel<2, 1>, (const void*)ln_bwd_fused_kernel<3, 1>};
+    const void* ks[8] = {(const void*)ln_bwd_fused_kernel<1, 0>, (const void*)ln_bwd_fused_kernel<2, 0>,
+                         (const void*)ln_bwd_fused_kernel<3, 0>, (const void*)ln_bwd_fused_kernel<4, 0>,
+                         (const void*)ln_bwd_fused_kernel<1, 1>, (const void*)ln_bwd_fused_kernel<2, 1>,
+                         (const void*)ln_bwd_fused_kernel<3, 1>, (const void*)ln_bwd_fused_kernel<4, 1>};
     for (const void* k : ks) MPX_CUDA_CHECK(ensure_smem_attr(k, 48 * 1024));
     auto launch = [&](auto k) {
       return ::mpx::launch_k(k, blocks, 128, shb, st, x, ldx, gain, mean, rstd, dy, lddy, dres, ldres, dx, lddx,
@@ -1409,7 +1410,8 @@ int mpx_layernorm_bwd2(int dtype, const void* x, int64_t ldx, const void* gain, 
     switch (D / 256) {
       case 1: MPX_CUDA_CHECK(f ? launch(ln_bwd_fused_kernel<1, 1>) : launch(ln_bwd_fused_kernel<1, 0>)); break;
       case 2: MPX_CUDA_CHECK(f ? launch(ln_bwd_fused_kernel<2, 1>) : launch(ln_bwd_fused_kernel<2, 0>)); break;
-      default: MPX_CUDA_CHECK(f ? launch(ln_bwd_fused_kernel<3, 1>) : launch(ln_bwd_fused_kernel<3, 0>)); break;
+      case 3: MPX_CUDA_CHECK(f ? launch(ln_bwd_fused_kernel<3, 1>) : launch(ln_bwd_fused_kernel<3, 0>)); break;
+      default: MPX_CUDA_CHECK(f ? launch(ln_bwd_fused_kernel<4, 1>) : launch(ln_bwd_fused_kernel<4, 0>)); break;
     }
     MPX_LAUNCH_CHECK("ln_bwd_fused_kernel");
     MPX_CUDA_CHECK(::mpx::launch_k(partials_reduce3_kernel, dim3((D + 31) / 32, nsum), 1024, 0, st, workspace, blocks, D, dgain, dbias, dxsum, f));

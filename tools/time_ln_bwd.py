@@ -10,7 +10,7 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2507_03312_b200 import _native as N  # noqa: E402
 
-M, D = 256 * 197, 768
+M, D = 256 * 197, int(sys.argv[3]) if len(sys.argv) > 3 else 768  # argv[3]: width (1024 = ViT-L)
 bf = torch.bfloat16
 torch.manual_seed(0)
 dev = "cuda"
