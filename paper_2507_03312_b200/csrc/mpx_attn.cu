@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(kAttnThreadsF, 1)
 // 224 KB of tiles + 2 KB reduction scratch + barriers: the alignment slack is
 // trimmed to fit the 227 KB limit (the dynamic window starts 1 KB-aligned when
 // the kernel has no static shared memory; checked at run time)
-constexpr size_t kAttnBwdBody = 2 * kAttnQ + 2 * kAttnKV + 2 * kAttnP + kSplit * 128 * 4 + 128;
+constexpr size_t kAttnBwdBody = 2 * kAttnQ + 2 * kAttnKV + 2 * kAttnP + kSplit * 128 * 4 + 160;
 constexpr size_t kAttnBwdSmem = 232448;
 static_assert(kAttnBwdBody <= kAttnBwdSmem, "attention backward tiles exceed shared memory");
 
@@ -577,38 +577,6 @@ struct AttnBwdParams {
   const uint8_t* psaved;  // optional: the forward's P tiles (attn_fwd psave) — reloaded instead of recomputed
 };
 
-// 16 half values per lane (8 packed words) -> column sums over the warp's 32 lanes
-// (rows) by recursive halving (fixed order); returns the sum of column col16(lane).
-// The first step exchanges packed words (4 shuffles instead of 8) and adds the two
-// rows' halves straight into f32 (unpack + FHADD) — the same additions in the same
-// tree as halving the unpacked values, so the same bits
-template <int FMT>
-__device__ __forceinline__ float warp_colsum16w(const uint32_t (&w)[8], int lane) {
-  float v[8];
-  const bool up = (lane & 16) != 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t send = up ? w[i] : w[i + 4];
-    const uint32_t keep = up ? w[i + 4] : w[i];
-    const float2 s2 = add_h2<FMT>(unpack2_fmt<FMT>(keep), __shfl_xor_sync(0xffffffffu, send, 16));
-    v[2 * i] = s2.x;
-    v[2 * i + 1] = s2.y;
-  }
-#pragma unroll
-  for (int w2 = 4, m = 8; w2 >= 1; w2 >>= 1, m >>= 1) {
-    const bool u = (lane & m) != 0;
-#pragma unroll
-    for (int i = 0; i < w2; ++i) {
-      const float send = u ? v[i] : v[i + w2];
-      const float keep = u ? v[i + w2] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-    }
-  }
-  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
-}
-__device__ __forceinline__ int col16(int lane) {
-  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-}
 
 template <int FMT>  // 0 f16, 1 bf16: one conversion path compiled
 __global__ void __launch_bounds__(kAttnThreads, 1)
@@ -631,11 +599,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   // TMEM cols 256-511), 11 Q_t landed, 12 K landed
   float* red = reinterpret_cast<float*>(sdS + kAttnP);
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + kSplit * 128);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+  uint64_t* cready = bar + 13;  // qkv-bias column sums handed to warps 1-3: cready[2], cdone[2]
+  uint64_t* cdone = bar + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int T = P.m_tiles;
   const long long D = (long long)P.H * P.hd;
+  // qkv-bias column sums, off the softmax warps: cready[s] completes when every softmax
+  // thread has stored item it's dQ / dK / dV rows (s = it & 1), cdone[s] when warps 1-3
+  // have summed them (the softmax warps wait for it two items later)
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tmQ);
@@ -643,6 +616,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     tma_prefetch(&tmV);
     tma_prefetch(&tmdO);
     for (int i = 0; i < 13; ++i) mbar_init(&bar[i], (i == 3 || i == 5 || i == 7 || i == 10) ? 128 * kSplit : 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&cready[i], 128 * kSplit);
+      mbar_init(&cdone[i], 3);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -797,6 +774,55 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
       }
     }
+  } else if (warp <= 3) {
+    if (P.csum) {  // warps 1-3 (q, k, v): per item, the column sums of the part's stored rows (fresh
+                   // in L2): lane = 8 rp + co sums columns 8co..8co+7 over rows rp, rp + 4, ... with
+                   // 16-byte loads, 8 rows in flight; the 4 row phases are then added in a fixed tree
+      const int part = warp - 1, rp = lane >> 3, co = lane & 7;
+      int it = 0;
+      for (int item = blockIdx.x; item < P.items; item += gridDim.x, ++it) {
+        const int s = it & 1;
+        mbar_wait(&cready[s], (uint32_t)(it >> 1) & 1u);
+        const int h = item % P.H, b = item / P.H;
+        const uint16_t* col = static_cast<const uint16_t*>(P.dqkv) + (long long)b * P.N * P.ld + part * D +
+                              (long long)h * P.hd + 8 * co;
+        float2 acc[4] = {f2(0.f), f2(0.f), f2(0.f), f2(0.f)};
+        int rr = rp;
+        for (; rr + 28 < P.N; rr += 32) {
+          uint4 w[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) w[u] = *reinterpret_cast<const uint4*>(col + (long long)(rr + 4 * u) * P.ld);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            acc[0] = add_h2<FMT>(acc[0], w[u].x);
+            acc[1] = add_h2<FMT>(acc[1], w[u].y);
+            acc[2] = add_h2<FMT>(acc[2], w[u].z);
+            acc[3] = add_h2<FMT>(acc[3], w[u].w);
+          }
+        }
+        for (; rr < P.N; rr += 4) {
+          const uint4 w = *reinterpret_cast<const uint4*>(col + (long long)rr * P.ld);
+          acc[0] = add_h2<FMT>(acc[0], w.x);
+          acc[1] = add_h2<FMT>(acc[1], w.y);
+          acc[2] = add_h2<FMT>(acc[2], w.z);
+          acc[3] = add_h2<FMT>(acc[3], w.w);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // (p0 + p1) + (p2 + p3) over the row phases
+          acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, 8);
+          acc[i].y += __shfl_xor_sync(0xffffffffu, acc[i].y, 8);
+          acc[i].x += __shfl_xor_sync(0xffffffffu, acc[i].x, 16);
+          acc[i].y += __shfl_xor_sync(0xffffffffu, acc[i].y, 16);
+        }
+        if (rp == 0) {
+          float4* o = reinterpret_cast<float4*>(P.csum + (long long)b * 3 * D + part * D + (long long)h * P.hd + 8 * co);
+          o[0] = make_float4(acc[0].x, acc[0].y, acc[1].x, acc[1].y);
+          o[1] = make_float4(acc[2].x, acc[2].y, acc[3].x, acc[3].y);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cdone[s]);
+      }
+    }
   } else if (warp >= 4) {
     const int qd = warp & 3, split = (warp - 4) >> 2;
     const int r = qd * 32 + lane;
@@ -816,7 +842,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     int it = 0;       // items so far
     for (int item = blockIdx.x; item < P.items; item += gridDim.x, ++it) {
     const int h = item % P.H, b = item / P.H;
-    float qsum = 0.f;  // column col16(lane) of chunk `split` of dQ, summed over this warp's rows and the tiles
     for (int t = 0; t < T; ++t, ++gt) {
       const uint32_t ph = gt & 1;
       if (P.psaved == nullptr) {
@@ -903,12 +928,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
-        if (P.csum) {  // column sums of the stored (rounded) dQ rows
-          uint32_t wv[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) wv[i] = qrow < P.N ? pk[i] : 0u;
-          qsum += warp_colsum16w<FMT>(wv, lane);
-        }
       }
       if (warp == 4 && lane == 0 && it == kTraceIt) ATRACE(8 + 8 * t);
     }
@@ -916,7 +935,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // once the last tile's dK MMAs (issued after its dQ) have completed
     mbar_wait(&bar[8], (gt - 1) & 1);
     tc_fence_after();
-    float kvsum[4] = {0.f, 0.f, 0.f, 0.f};  // per chunk: column col16(lane), this warp's 32 keys
     const int half = split >> 1, which = split & 1;  // kSplit == 4: one combo per split
     {
       const int key = half * 128 + r;
@@ -939,37 +957,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
-        if (P.csum) {
-          uint32_t wv[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) wv[i] = key < P.N ? pk[i] : 0u;
-          kvsum[c] = warp_colsum16w<FMT>(wv, lane);
-        }
       }
     }
-    if (P.csum) {
-      // combine the warps' partials through the (now idle) dS tile — the next
-      // item's Q / P may already be landing: slots
-      // [part q/k/v][quarter (and key half)][64 columns], then one fixed-order sum
-      float* sc = reinterpret_cast<float*>(sdS);
-      if ((lane & 1) == 0) {
-        sc[(0 * 8 + qd) * 64 + split * 16 + col16(lane)] = qsum;
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          sc[((1 + (which ? 0 : 1)) * 8 + half * 4 + qd) * 64 + c * 16 + col16(lane)] = kvsum[c];
-      }
-      asm volatile("bar.sync 6, %0;" ::"n"(128 * kSplit) : "memory");
-      const int tid = threadIdx.x - 128;
-      if (tid < 192) {
-        const int part = tid >> 6, col = tid & 63;  // part 0 q, 1 k, 2 v
-        float a = 0.f;
-        const int nslot = part == 0 ? 4 : 8;
-        for (int j = 0; j < nslot; ++j) a += sc[(part * 8 + j) * 64 + col];
-        P.csum[(long long)b * 3 * D + part * D + (long long)h * P.hd + col] = a;
-      }
-      asm volatile("bar.sync 6, %0;" ::"n"(128 * kSplit) : "memory");  // scratch read before the next P tile
+    if (P.csum) {  // this item's rows are stored: hand them to warps 1-3 (after they took item it - 2)
+      if (it >= 2) mbar_wait(&cdone[it & 1], (uint32_t)((it >> 1) - 1) & 1u);
+      mbar_arrive(&cready[it & 1]);
     }
-    // (the dS scratch is reused by these warps only after the barrier above)
     if (warp == 4 && lane == 0 && it == kTraceIt) ATRACE(20);
     }
   }

@@ -281,3 +281,24 @@ def test_epilogue_paths_bit_identical(cuda, dt, shape):
         y1 = VK.gemm(x, w, **common, tma_store=-1, bias=bias, aux=a1, ld_aux=N, act=act)
         assert torch.equal(y0.view(torch.int16), y1.view(torch.int16)), act
         assert torch.equal(a0.view(torch.int16), a1.view(torch.int16)), act
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+def test_fused_attention_backward_many_items(cuda, dt):
+    """Several (image, head) items per CTA of the persistent backward: the qkv-bias column
+    sums handed from the softmax warps to warps 1-3 item by item (double-buffered barriers
+    with back-pressure) against the column sums of the stored rows; repeated launches agree."""
+    Bsz, Nt, H, hd = 64, 197, 12, 64
+    D = H * hd
+    g = torch.Generator(device=cuda).manual_seed(11)
+    qkv = torch.randn(Bsz * Nt, 3 * D, device=cuda, generator=g).to(dt)
+    dO = torch.randn(Bsz * Nt, D, device=cuda, generator=g).to(dt)
+    psave = torch.empty(VK.attention_psave_bytes(Bsz, Nt, H), dtype=torch.uint8, device=cuda)
+    VK.attention_fwd(qkv, Bsz, Nt, H, hd, 0.125, p_save=psave)
+    cs = torch.empty(3 * D, device=cuda, dtype=dt)
+    dqkv = VK.attention_bwd(qkv, dO, Bsz, Nt, H, hd, 0.125, p_saved=psave, colsum_out=cs)
+    want = dqkv.float().sum(0)
+    assert torch.allclose(cs.float(), want, rtol=1e-2, atol=1e-2 * want.abs().max().item())
+    cs2 = torch.empty_like(cs)
+    dqkv2 = VK.attention_bwd(qkv, dO, Bsz, Nt, H, hd, 0.125, p_saved=psave, colsum_out=cs2)
+    assert torch.equal(dqkv2, dqkv) and torch.equal(cs2, cs)
